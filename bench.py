@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Benchmark: simulated workload traces/s on B200 (BASELINE.json `metric`).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+A "step" simulates the configuration's whole per-GPU trace batch (default C2:
+1M traces x 64 apps) under every policy of the configuration (C2: all four),
+i.e. one launch of K1 trace_sim + one of K2 stats_reduce (+ the cross-GPU
+aggregate all-reduce for N > 1).  The unit is one trace simulated under one
+policy.  Scaling is weak: every rank simulates its own contiguous trace-id
+shard of the configured size, generated on its GPU before timing.
+
+`value` is device-timed (CUDA events, max over ranks) with inputs resident
+in HBM (1 GiB of T0 records per GPU, larger than L2).  `e2e` is the same
+metric through the C ABI host-buffer call (sg_simulate_batch_host) with
+pinned host inputs/outputs and all copies inside the timed region.
+`cpu_baseline` times the reference's own simulate() (memshare, installed in
+oracle/_ref) on the host cores over a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import multiprocessing as mp
+import os
+import platform
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+REF_DIR = os.path.join(ROOT, "oracle", "_ref")
+TIME_SCALE_DYADIC = 1000.0 / 1024.0
+FALLBACK_HBM_GBS = 6650.0
+
+
+# ------------------------------------------------------------- CPU reference
+
+def _ref_worker(args):
+    """Time the reference's simulate() on traces [t0, t1) of cfg under every
+    policy until `budget_s` elapses.  Profiles are built before the timer."""
+    cfg_name, n_traces_override, t0, t1, budget_s = args
+    sys.path.insert(0, REF_DIR)
+    sys.path.insert(0, ROOT)
+    import memshare.device as rdev
+    import memshare.harness as rh
+    import memshare.policy as rp
+    from paper_1712_04495_b200.tracegen import CONFIGS, as_u32x4, generate
+
+    cfg = CONFIGS[cfg_name]
+    apps = as_u32x4(generate(cfg.gen, t0, t1 - t0))
+    ndev = cfg.ndev
+    specs = []
+    for t in range(t1 - t0):
+        for pol in cfg.policies:
+            kind = rp.PolicyKind.parse(pol)
+            for d in range(ndev):
+                rows = [r for r in apps[t] if ((int(r[3]) >> 8) & 0xFF) == d] if ndev > 1 else apps[t]
+                insts = [rh.AppProfile(f"a{i}", [rh.Phase(cpu_ms=int(a)),
+                                                 rh.Phase(alloc_mib=int(m), busy_ms=int(b),
+                                                          free_mib=int(m))], priority=int(at) & 0xFF)
+                         for i, (a, m, b, at) in enumerate(rows)]
+                specs.append((t, rh.WorkloadSpec(
+                    instances=insts, policy=kind,
+                    devices=rdev.parse_device_config({"devices": [{"mib": cfg.cap_mib[d]}]}),
+                    time_scale=TIME_SCALE_DYADIC)))
+    per_trace = len(cfg.policies) * ndev
+    done = 0
+    start = time.perf_counter()
+    for i, (_, spec) in enumerate(specs):
+        rh.simulate(spec)
+        if (i + 1) % per_trace == 0:
+            done += len(cfg.policies)
+            if time.perf_counter() - start >= budget_s:
+                break
+    return done, time.perf_counter() - start
+
+
+def cpu_reference_rate(cfg_name: str, budget_s: float, pool=None, cores=None, seed_base=10_000_000):
+    """traces/s (trace x policy simulations) of the reference simulate() over
+    all host cores, each core on its own contiguous trace range."""
+    cores = cores or os.cpu_count() or 1
+    from paper_1712_04495_b200.tracegen import CONFIGS
+    cfg = CONFIGS[cfg_name]
+    # enough traces per worker for the budget (reference ~1e3 traces/s/core at 64 apps)
+    per = max(8, int(budget_s * 2000 * 64 / cfg.gen.apps_per_trace / len(cfg.policies)) + 1)
+    jobs = [(cfg_name, None, seed_base + w * per, seed_base + (w + 1) * per, budget_s)
+            for w in range(cores)]
+    own = pool is None
+    if own:
+        pool = mp.get_context("fork").Pool(cores)
+    try:
+        res = pool.map(_ref_worker, jobs, chunksize=1)
+    finally:
+        if own:
+            pool.close()
+            pool.join()
+    total = sum(d for d, _ in res)
+    wall = max(t for _, t in res)
+    return total / wall, total, wall, cores
+
+
+def cpu_port_rate(cfg_name: str, n_traces: int):
+    """The C restatement (oracle/, OpenMP over all cores) on a sample: a
+    second, faster CPU point of comparison."""
+    from oracle import oracle as O
+    from paper_1712_04495_b200.tracegen import CONFIGS, as_u32x4, generate
+    cfg = CONFIGS[cfg_name]
+    apps = as_u32x4(generate(cfg.gen, 20_000_000, n_traces))
+    t0 = time.perf_counter()
+    for pol in cfg.policies:
+        O.simulate_burst(apps, cfg.cap_mib, pol, threads=0)
+    dt = time.perf_counter() - t0
+    return n_traces * len(cfg.policies) / dt, dt
+
+
+# ------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out, _ = self.proc.communicate()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                rows.append((float(f[1]), float(f[2]), f[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows),
+                "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------- helpers
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------- reference arm
+
+def run_reference_arm(args, ws, rank):
+    from paper_1712_04495_b200.tracegen import CONFIGS
+    cfg = CONFIGS[args.config]
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    pool = mp.get_context("fork").Pool(cores)
+    try:
+        budget = args.ref_step_s
+        for _ in range(args.warmup):
+            cpu_reference_rate(args.config, min(budget, 1.0), pool, cores, seed_base=30_000_000)
+        rates, totals, walls = [], 0, 0.0
+        for k in range(args.steps):
+            r, tot, wall, _ = cpu_reference_rate(args.config, budget, pool, cores,
+                                                 seed_base=40_000_000 + k * 1_000_000)
+            rates.append(r)
+            totals += tot
+            walls += wall
+    finally:
+        pool.close()
+        pool.join()
+    value = totals / walls
+    line = {
+        "impl": "reference", "metric": "simulated workload traces/s",
+        "value": value, "unit": "traces/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * walls / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic", "config": config_block(cfg, args, ws),
+        "cpu_baseline": {"value": value, "unit": "traces/s", "cores": cores, "kind": "reference",
+                         "sample": f"{totals} trace-policy simulations of {args.config} "
+                                   f"(memshare.harness.simulate, {args.steps} steps of "
+                                   f"~{budget:.1f} s on {cores} processes)",
+                         "cpu": platform.processor() or platform.machine(),
+                         "python": platform.python_version()},
+        "e2e": {"value": value, "unit": "traces/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_block(cfg, args, ws):
+    return {"workload": f"{cfg.name}: {cfg.description}", "traces_per_gpu": args.traces,
+            "apps_per_trace": cfg.gen.apps_per_trace, "policies": list(cfg.policies),
+            "devices_per_trace": cfg.ndev, "cap_mib": list(cfg.cap_mib), "seed": cfg.gen.seed,
+            "unit": "one trace simulated under one policy",
+            "l2": "inputs (16 B/app, >= 1 GiB per GPU at C2) exceed the 126 MB L2",
+            "parallelism": f"trace shards x{ws}"}
+
+
+# ------------------------------------------------------------- our arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--traces", type=int, default=0, help="traces per GPU (default: config)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-step-s", type=float, default=4.0)
+    ap.add_argument("--chunk", type=int, default=0)
+    args = ap.parse_args()
+    ws, rank, local = dist_env()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    from paper_1712_04495_b200.tracegen import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.traces <= 0:
+        args.traces = cfg.n_traces // max(cfg.gpus, 1) if cfg.gpus > 1 else cfg.n_traces
+
+    if args.impl == "reference":
+        return run_reference_arm(args, ws, rank)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1712_04495_b200 import batch as B
+    from paper_1712_04495_b200 import parallel as PAR
+    from paper_1712_04495_b200.policy import policy_mask
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    n = args.traces
+    t_begin = rank * n
+    napp = cfg.gen.apps_per_trace
+    _, pols = policy_mask(cfg.policies)
+    npol = len(pols)
+    apps = B.generate_traces(cfg.gen, t_begin, n, device=local)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    launches = 0
+
+    def step(i=None):
+        nonlocal launches
+        if i is not None:
+            ev[i][0].record(stream)
+        res = B.simulate_batch(apps, pols, cfg.cap_mib, stream=stream)
+        if i is not None:
+            ev[i][1].record(stream)
+        agg = B.reduce_stats(res.stats_raw, stream=stream)
+        launches += 2
+        if ws > 1:
+            agg = PAR.allreduce_aggregate(agg)
+        return res, agg
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches = 0
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        for i in range(args.steps):
+            res, agg = step(i)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    kern_ms = [a.elapsed_time(b) for a, b in ev]
+    tt = torch.tensor([elapsed_ms, max(kern_ms)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(tt[0])
+    aggd = B.aggr_to_dict(agg)
+    units_per_step = n * npol * ws
+    value = units_per_step * args.steps / (elapsed_ms / 1000.0)
+    ms_per_step = elapsed_ms / args.steps
+
+    # roofline of K1: algorithmic bytes per launch / mean launch duration
+    in_b = n * napp * 16
+    out_b = n * npol * (napp * 8 + cfg.ndev * (32 + 16))
+    alg_bytes = in_b + out_b
+    mean_k = statistics.mean(kern_ms) / 1000.0
+    peak, peak_src = hbm_peak()
+    achieved = alg_bytes / mean_k / 1e9
+
+    # e2e through the C ABI host-buffer pipeline
+    e2e = None
+    if not args.no_e2e:
+        host_apps = B.pinned_apps(n, napp)
+        host_apps[...] = apps.cpu().numpy().view(np.uint32)
+        outb = B.HostBuffers(npol, n, napp, cfg.ndev)
+        for _ in range(1):
+            B.simulate_batch_host(host_apps, pols, cfg.cap_mib, device=local, out=outb,
+                                  chunk_traces=args.chunk)
+        e2e_steps = max(1, min(args.steps, 5))
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            B.simulate_batch_host(host_apps, pols, cfg.cap_mib, device=local, out=outb,
+                                  chunk_traces=args.chunk)
+            _ = float(outb.stats["makespan"][0, 0, 0])
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": units_per_step * e2e_steps / float(dt[0]), "unit": "traces/s",
+               "h2d_bytes_per_step": int(host_apps.nbytes), "d2h_bytes_per_step": int(outb.d2h_bytes()),
+               "api": "sg_simulate_batch_host (C ABI, pinned host buffers, 3-stream pipeline)",
+               "steps": e2e_steps}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        try:
+            r, tot, wall, cores = cpu_reference_rate(args.config, args.cpu_budget)
+            cpu = {"value": r, "unit": "traces/s", "cores": cores, "kind": "reference",
+                   "sample": f"{tot} trace-policy simulations of {args.config} traces "
+                             f"[10M, ...) in {wall:.1f} s: memshare.harness.simulate "
+                             f"(oracle/_ref) on {cores} processes",
+                   "python": platform.python_version()}
+        except Exception as exc:  # pragma: no cover - reported, not fatal
+            cpu = {"value": None, "unit": "traces/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {exc!r}"}
+        try:
+            pr, pdt = cpu_port_rate(args.config, 20_000 if napp <= 64 else 5_000)
+            cpu["port"] = {"value": pr, "unit": "traces/s", "cores": os.cpu_count(),
+                           "kind": "port", "sample": f"oracle/ C restatement, OpenMP, {pdt:.1f} s"}
+        except Exception as exc:  # pragma: no cover
+            cpu["port"] = {"value": None, "sample": f"unavailable: {exc!r}"}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": "simulated workload traces/s", "value": value, "unit": "traces/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (counter-based SplitMix64 generator, generated on-GPU before timing)",
+            "config": config_block(cfg, args, ws),
+            "decisions_per_s": aggd["sum_grants"] / (ms_per_step / 1000.0),
+            "events_per_s": aggd["sum_pops"] / (ms_per_step / 1000.0),
+            "aggregate": aggd,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "kernel": "trace_sim_kernel", "alg_bytes_per_launch": alg_bytes,
+                         "mean_launch_ms": mean_k * 1000.0},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

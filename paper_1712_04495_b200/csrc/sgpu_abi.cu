@@ -1,0 +1,272 @@
+// sgpu_abi.cu — extern "C" entry points of libsgpu.so (include/sgpu.h):
+// argument validation, kernel dispatch, and the host-buffer pipeline.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "sgpu_common.cuh"
+#include "sgpu_internal.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+constexpr int E_ARG = -1;
+constexpr int E_CUDA = -2;
+constexpr int E_RANGE = -3;
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+struct Shape {
+    uint32_t npol = 0;
+    uint32_t policies[4] = {0, 0, 0, 0};
+    bool program = false, f64 = false, multi = false;
+    uint32_t n_pad = 0;
+};
+
+int validate(const sg_batch* in, Shape& s) {
+    if (!in) return fail(E_ARG, "null batch");
+    if (in->policy_mask == 0 || (in->policy_mask & ~0xFu))
+        return fail(E_ARG, "policy_mask must be a non-empty subset of 0xF (got 0x%x)", in->policy_mask);
+    for (uint32_t p = 0; p < 4; p++)
+        if (in->policy_mask & (1u << p)) s.policies[s.npol++] = p;
+    if (in->ndev < 1 || in->ndev > SG_MAX_DEV) return fail(E_ARG, "ndev must be 1..%d", SG_MAX_DEV);
+    for (uint32_t d = 0; d < in->ndev; d++)
+        if (in->cap_mib[d] == 0 || in->cap_mib[d] >= 0x7FFFFFFFu)
+            return fail(E_RANGE, "cap_mib[%u] must be in [1, 2^31-1)", d);
+    if (in->time_mode != SG_TIME_TICKS && in->time_mode != SG_TIME_F64)
+        return fail(E_ARG, "unknown time_mode %u", in->time_mode);
+    s.program = in->steps != nullptr;
+    if (s.program && !in->step_offsets) return fail(E_ARG, "steps given without step_offsets");
+    s.f64 = in->time_mode == SG_TIME_F64;
+    if (s.f64 && !s.program) return fail(E_ARG, "SG_TIME_F64 requires step-program mode");
+    if (in->tick_log2 < -64 || in->tick_log2 > 64) return fail(E_RANGE, "tick_log2 out of range");
+    s.multi = in->ndev > 1;
+    const uint32_t maxn = in->trace_offsets ? in->max_apps : in->apps_per_trace;
+    if (maxn > SG_MAX_APPS) return fail(E_RANGE, "traces longer than %d apps are not supported", SG_MAX_APPS);
+    if (in->n_traces && maxn && !in->apps) return fail(E_ARG, "null apps");
+    if (reinterpret_cast<uintptr_t>(in->apps) & 15u) return fail(E_ARG, "apps must be 16-byte aligned");
+    s.n_pad = (maxn + 31u) & ~31u;
+    if (s.n_pad == 0) s.n_pad = 32;
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sg_abi_version(void) { return SG_ABI_VERSION; }
+
+const char* sg_last_error(void) { return g_err; }
+
+int sg_device_info(int cuda_device, int* sm_count, int* warps_per_sm) {
+    int sms = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    if (sm_count) *sm_count = sms;
+    if (warps_per_sm) *warps_per_sm = 0;
+    return 0;
+}
+
+static int simulate_device(const sg_batch* in, const sg_out* out, cudaStream_t stream,
+                           uint64_t n_apps_total) {
+    Shape s;
+    int rc = validate(in, s);
+    if (rc) return rc;
+    if (!out || !out->stats) return fail(E_ARG, "sg_out.stats is required");
+    if (out->events && out->events_per_trace == 0) return fail(E_ARG, "events_per_trace must be > 0");
+    if (in->n_traces == 0) return 0;
+    sg::SimParams p;
+    memset(&p, 0, sizeof(p));
+    p.n_traces = in->n_traces;
+    p.trace_offsets = in->trace_offsets;
+    p.apps_per_trace = in->apps_per_trace;
+    p.n_pad = s.n_pad;
+    p.apps = in->apps;
+    p.steps = in->steps;
+    p.step_offsets = in->step_offsets;
+    for (uint32_t i = 0; i < 4; i++) p.policies[i] = s.policies[i];
+    p.npol = s.npol;
+    p.ndev = in->ndev;
+    for (uint32_t d = 0; d < SG_MAX_DEV; d++) p.cap[d] = d < in->ndev ? in->cap_mib[d] : 1;
+    p.tick_log2 = in->tick_log2;
+    p.ev_cap = out->events_per_trace;
+    p.n_apps_total = n_apps_total;
+    p.grant = out->grant;
+    p.end = out->end;
+    p.stats = out->stats;
+    p.mem_pct = out->mem_pct;
+    p.dev_pct = out->dev_pct;
+    p.events = out->events;
+    p.event_counts = out->event_counts;
+    sg::sim_layout(p, s.program, s.f64);
+    if (p.warp_bytes * sg::kSimWarpsPerBlock > 227u * 1024u)
+        return fail(E_RANGE, "shared memory per block exceeds 227 KB (n_pad=%u)", s.n_pad);
+    cudaError_t e = sg::launch_sim(p, s.program, s.f64, s.multi, stream, nullptr);
+    if (e != cudaSuccess) return cuda_fail(e, "trace_sim launch");
+    return 0;
+}
+
+int sg_simulate_batch(const sg_batch* in, const sg_out* out, void* stream) {
+    if (!in) return fail(E_ARG, "null batch");
+    uint64_t n_apps_total;
+    if (in->trace_offsets) {
+        // the total is only needed as the per-policy output stride
+        uint64_t o[2] = {0, 0};
+        cudaError_t e = cudaMemcpy(&o[0], in->trace_offsets, 8, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(&o[1], in->trace_offsets + in->n_traces, 8, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_fail(e, "reading trace_offsets");
+        n_apps_total = o[1] - o[0];
+    } else {
+        n_apps_total = in->n_traces * (uint64_t)in->apps_per_trace;
+    }
+    return simulate_device(in, out, static_cast<cudaStream_t>(stream), n_apps_total);
+}
+
+// Host-buffer pipeline: chunks of traces cycle through NBUF device buffer
+// sets on NBUF streams; each chunk is H2D -> trace_sim -> D2H on its stream,
+// so the copies of one chunk overlap the simulation of the next.
+int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_device,
+                           uint64_t chunk_traces) {
+    Shape s;
+    int rc = validate(in, s);
+    if (rc) return rc;
+    if (!out || !out->stats) return fail(E_ARG, "sg_out.stats is required");
+    if (out->events) return fail(E_ARG, "event logs are not supported on the host path");
+    if (in->trace_offsets) return fail(E_ARG, "host path takes fixed-length traces");
+    if (s.program) return fail(E_ARG, "host path takes T0 (burst) traces");
+    if (in->n_traces == 0) return 0;
+    cudaError_t e = cudaSetDevice(cuda_device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+
+    const uint64_t N = in->n_traces;
+    const uint32_t napps = in->apps_per_trace;
+    const uint32_t ndev = in->ndev;
+    if (chunk_traces == 0) chunk_traces = 1u << 16;
+    if (chunk_traces > N) chunk_traces = N;
+    constexpr int NBUF = 3;
+    const size_t app_b = chunk_traces * napps * sizeof(sg_app);
+    const size_t tick_b = (size_t)s.npol * chunk_traces * napps * sizeof(uint32_t);
+    const size_t st_b = (size_t)s.npol * chunk_traces * ndev * sizeof(sg_trace_stats);
+    const size_t pct_b = (size_t)s.npol * chunk_traces * ndev * sizeof(double);
+    const bool want_pct = out->mem_pct || out->dev_pct;
+
+    struct Buf {
+        cudaStream_t st = nullptr;
+        sg_app* apps = nullptr;
+        uint32_t *grant = nullptr, *end = nullptr;
+        sg_trace_stats* stats = nullptr;
+        double *mem = nullptr, *dev = nullptr;
+    } B[NBUF];
+    auto cleanup = [&]() {
+        for (auto& b : B) {
+            if (b.st) cudaStreamSynchronize(b.st);
+            cudaFree(b.apps); cudaFree(b.grant); cudaFree(b.end); cudaFree(b.stats);
+            cudaFree(b.mem); cudaFree(b.dev);
+            if (b.st) cudaStreamDestroy(b.st);
+        }
+    };
+    for (auto& b : B) {
+        e = cudaStreamCreateWithFlags(&b.st, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaMalloc(&b.apps, app_b);
+        if (e == cudaSuccess && out->grant) e = cudaMalloc(&b.grant, tick_b);
+        if (e == cudaSuccess && out->end) e = cudaMalloc(&b.end, tick_b);
+        if (e == cudaSuccess) e = cudaMalloc(&b.stats, st_b);
+        if (e == cudaSuccess && want_pct) e = cudaMalloc(&b.mem, pct_b);
+        if (e == cudaSuccess && want_pct) e = cudaMalloc(&b.dev, pct_b);
+        if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "allocating pipeline buffers"); }
+    }
+    const uint64_t n_apps_total = N * napps;
+    uint64_t chunk = 0;
+    for (uint64_t t0 = 0; t0 < N; t0 += chunk_traces, chunk++) {
+        Buf& b = B[chunk % NBUF];
+        const uint64_t nt = (N - t0 < chunk_traces) ? N - t0 : chunk_traces;
+        const uint64_t a0 = t0 * napps, na = nt * napps;
+        e = cudaMemcpyAsync(b.apps, in->apps + a0, na * sizeof(sg_app), cudaMemcpyHostToDevice, b.st);
+        if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "H2D apps"); }
+        sg_batch cb = *in;
+        cb.n_traces = nt;
+        cb.apps = b.apps;
+        sg_out co;
+        memset(&co, 0, sizeof(co));
+        co.grant = b.grant;
+        co.end = b.end;
+        co.stats = b.stats;
+        co.mem_pct = out->mem_pct ? b.mem : nullptr;
+        co.dev_pct = out->dev_pct ? b.dev : nullptr;
+        rc = simulate_device(&cb, &co, b.st, na);
+        if (rc) { cleanup(); return rc; }
+        for (uint32_t p = 0; p < s.npol; p++) {
+            const uint64_t ho = (uint64_t)p * n_apps_total + a0;
+            const uint64_t hs = ((uint64_t)p * N + t0) * ndev;
+            const uint64_t dsrc = (uint64_t)p * nt * ndev;
+            if (out->grant)
+                e = cudaMemcpyAsync(static_cast<uint32_t*>(out->grant) + ho, b.grant + (uint64_t)p * na,
+                                    na * 4, cudaMemcpyDeviceToHost, b.st);
+            if (e == cudaSuccess && out->end)
+                e = cudaMemcpyAsync(static_cast<uint32_t*>(out->end) + ho, b.end + (uint64_t)p * na,
+                                    na * 4, cudaMemcpyDeviceToHost, b.st);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(static_cast<sg_trace_stats*>(out->stats) + hs, b.stats + dsrc,
+                                    nt * ndev * sizeof(sg_trace_stats), cudaMemcpyDeviceToHost, b.st);
+            if (e == cudaSuccess && out->mem_pct)
+                e = cudaMemcpyAsync(out->mem_pct + hs, b.mem + dsrc, nt * ndev * 8,
+                                    cudaMemcpyDeviceToHost, b.st);
+            if (e == cudaSuccess && out->dev_pct)
+                e = cudaMemcpyAsync(out->dev_pct + hs, b.dev + dsrc, nt * ndev * 8,
+                                    cudaMemcpyDeviceToHost, b.st);
+            if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "D2H outputs"); }
+        }
+    }
+    for (auto& b : B) {
+        e = cudaStreamSynchronize(b.st);
+        if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "pipeline"); }
+    }
+    cleanup();
+    return 0;
+}
+
+int sg_reduce_stats(const sg_trace_stats* stats, uint64_t count, sg_aggr* out, void* stream) {
+    if (!out || (count && !stats)) return fail(E_ARG, "null pointer");
+    cudaError_t e = sg::launch_reduce(stats, count, out, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "stats_reduce");
+    return 0;
+}
+
+int sg_generate_traces(const sg_gen_params* p, uint64_t trace_begin, uint64_t n_traces,
+                       sg_app* out, void* stream) {
+    if (!p || (n_traces && !out)) return fail(E_ARG, "null pointer");
+    if (p->apps_per_trace == 0 || p->apps_per_trace > SG_MAX_APPS)
+        return fail(E_RANGE, "apps_per_trace must be 1..%d", SG_MAX_APPS);
+    if (p->prio_levels < 1 || p->prio_levels > 8) return fail(E_RANGE, "prio_levels must be 1..8");
+    if (p->ndev < 1 || p->ndev > SG_MAX_DEV) return fail(E_RANGE, "ndev must be 1..8");
+    if (p->arr_hi < p->arr_lo || p->mem_hi < p->mem_lo || p->busy_hi < p->busy_lo)
+        return fail(E_RANGE, "empty generator range");
+    cudaError_t e = sg::launch_generate(*p, trace_begin, n_traces, out, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "trace_gen");
+    return 0;
+}
+
+int sg_select_grants_batch(uint64_t n_queues, const uint64_t* qoff, const int64_t* nbytes,
+                           const int32_t* prio, const int64_t* free_bytes, const uint32_t* kind,
+                           uint8_t* granted, void* stream) {
+    if (n_queues && (!qoff || !free_bytes || !kind)) return fail(E_ARG, "null pointer");
+    cudaError_t e = sg::launch_select(n_queues, qoff, nbytes, prio, free_bytes, kind, granted,
+                                      static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "select_grants");
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,54 @@
+// sgpu_internal.h — launch parameters shared by the ABI layer and kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/sgpu.h"
+
+namespace sg {
+
+constexpr int kSimWarpsPerBlock = 4;
+
+struct SimParams {
+    uint64_t n_traces;
+    const uint64_t* trace_offsets;  // optional CSR
+    uint32_t apps_per_trace;
+    uint32_t n_pad;                 // per-warp app capacity (multiple of 32)
+    const sg_app* apps;
+    const sg_step* steps;           // program mode
+    const uint32_t* step_offsets;
+    uint32_t policies[4];
+    uint32_t npol;
+    uint32_t ndev;
+    uint32_t cap[SG_MAX_DEV];
+    int32_t tick_log2;
+    uint32_t ev_cap;
+    uint64_t n_apps_total;          // per-policy stride of grant/end
+    void* grant;
+    void* end;
+    void* stats;
+    double* mem_pct;
+    double* dev_pct;
+    sg_event* events;
+    uint32_t* event_counts;
+    // per-warp shared-memory layout (bytes)
+    uint32_t off_app, off_q, off_grant, off_end, off_pc, off_held, off_bar, warp_bytes;
+};
+
+// Shared-memory layout for one warp simulating traces of up to n_pad apps.
+void sim_layout(SimParams& p, bool program_mode, bool f64);
+
+// Launch K1 (trace simulation).  Returns a cudaError_t.
+cudaError_t launch_sim(const SimParams& p, bool program_mode, bool f64, bool multi,
+                       cudaStream_t stream, int* grid_out);
+
+cudaError_t launch_reduce(const sg_trace_stats* stats, uint64_t count, sg_aggr* out,
+                          cudaStream_t stream);
+cudaError_t launch_generate(const sg_gen_params& p, uint64_t trace_begin, uint64_t n_traces,
+                            sg_app* out, cudaStream_t stream);
+cudaError_t launch_select(uint64_t n_queues, const uint64_t* qoff, const int64_t* nbytes,
+                          const int32_t* prio, const int64_t* free_bytes, const uint32_t* kind,
+                          uint8_t* granted, cudaStream_t stream);
+
+}  // namespace sg

@@ -1,0 +1,361 @@
+"""Drop-in for the reference's simulated workload path (memshare/harness.py).
+
+Same public names and semantics as the reference module's SIMULATED mode:
+`Phase`, `AppProfile`, `builtin_profiles`, `DEFAULT_DEVICE`, `WorkloadSpec`
+(+ `from_json`), `MetricsReport` (+ `summary`/`to_json`/`to_csv`), `TICK_MS`
+and `simulate(spec) -> MetricsReport`.  The real-process runner, sequential
+baseline and overhead bench of the reference (harness.py:173-370, 575-678)
+are out of scope.
+
+`simulate` runs the spec as ONE trace through the CUDA engine
+(K1 `trace_sim`, step-program mode, event log on) and rebuilds the
+reference's report from the GPU's outputs:
+  * times: if every step duration `ms * time_scale / 1000.0` (computed with
+    the reference's own float expression, harness.py:483,487) lies on a
+    2^-e s grid with all sums exact, the engine runs in integer ticks of
+    2^-e s — every event time is then bit-identical to the reference's float
+    time; otherwise it runs in float64 mode, which repeats the reference's
+    float additions (`now + arg`) in the same order;
+  * makespan, utilisation percentages and max concurrent holders come from
+    the kernel's fused statistics (harness.py:373-461 semantics);
+  * the event list / instance table / 100 ms memory trace are assembled on
+    the host from the GPU event log, exactly as the reference formats them
+    (stable sort by t, harness.py:567; trace loop, harness.py:439-450).
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import struct
+from dataclasses import dataclass, field
+from fractions import Fraction
+
+import numpy as np
+
+from . import _lib
+from .batch import STEP_DTYPE, simulate_batch
+from .device import MIB, DeviceSpec, parse_device_config
+from .errors import SchemaError, SgpuUnavailable
+from .policy import PolicyKind
+
+TICK_MS = 100  # utilisation sampling tick (harness.py:36)
+
+
+@dataclass
+class Phase:
+    cpu_ms: float = 0.0
+    alloc_mib: int = 0
+    busy_ms: float = 0.0
+    free_mib: int = 0
+
+
+@dataclass
+class AppProfile:
+    name: str
+    phases: list[Phase]
+    priority: int = 0
+
+    def peak_mib(self) -> int:
+        held = peak = 0
+        for p in self.phases:
+            held += p.alloc_mib
+            peak = max(peak, held)
+            held -= p.free_mib
+        return peak
+
+    def total_ms(self) -> float:
+        """Sequential (uncontended) run time: the speed-up denominator."""
+        return sum(p.cpu_ms + p.busy_ms for p in self.phases)
+
+
+def builtin_profiles() -> dict[str, AppProfile]:
+    """The reference's three desk-scale application shapes
+    (memshare/harness.py:65-83): ara-like (CPU-heavy, short 768 MiB burst at
+    the end), mummer-like (720 MiB held through 10 alternating 500 ms
+    cpu/busy rounds), blast-like (1750 MiB, 8 s busy between 1 s cpu)."""
+    ara = AppProfile("ara-like", [Phase(cpu_ms=9500),
+                                  Phase(alloc_mib=768, busy_ms=500, free_mib=768)])
+    rounds = [Phase(cpu_ms=500), Phase(busy_ms=500)] * 10
+    mummer = AppProfile("mummer-like", [Phase(alloc_mib=720)] + rounds + [Phase(free_mib=720)])
+    blast = AppProfile("blast-like", [Phase(alloc_mib=1750, cpu_ms=1000), Phase(busy_ms=8000),
+                                      Phase(cpu_ms=1000, free_mib=1750)])
+    return {p.name: p for p in (ara, mummer, blast)}
+
+
+DEFAULT_DEVICE = {"devices": [{"name": "K20m-sim", "mib": 4799}]}
+
+
+@dataclass
+class WorkloadSpec:
+    instances: list[AppProfile]  # one entry per instance, in queue order
+    policy: PolicyKind = PolicyKind.FIFO
+    backend: str = "shm"
+    devices: list[DeviceSpec] = None
+    seed: int = 0
+    time_scale: float = 1.0
+    timeout_ms: float = math.inf
+    kill_plan: list[tuple[int, float]] = field(default_factory=list)
+
+    def __post_init__(self):
+        if self.devices is None:
+            self.devices = parse_device_config(DEFAULT_DEVICE)
+
+    @classmethod
+    def from_json(cls, doc: dict) -> "WorkloadSpec":
+        """Workload JSON (memshare/harness.py:104-130; README.md:98-109)."""
+        profiles = dict(builtin_profiles())
+        for p in doc.get("profiles", []):
+            phases = [Phase(ph.get("cpu_ms", 0), ph.get("alloc_mib", 0),
+                            ph.get("busy_ms", 0), ph.get("free_mib", 0)) for ph in p["phases"]]
+            profiles[p["name"]] = AppProfile(p["name"], phases, p.get("priority", 0))
+        instances = []
+        for name, count in doc.get("instances", []):
+            if name not in profiles:
+                raise SchemaError(f"unknown profile {name!r}")
+            instances.extend([profiles[name]] * int(count))
+        if not instances:
+            raise SchemaError("workload has no instances")
+        devices = parse_device_config(doc["device"]) if "device" in doc else None
+        return cls(instances=instances, policy=PolicyKind.parse(doc.get("policy", "fifo")),
+                   backend=doc.get("backend", "shm"), devices=devices,
+                   seed=int(doc.get("seed", 0)),
+                   time_scale=float(doc.get("time_scale", 1.0)),
+                   timeout_ms=float(doc.get("timeout_ms", math.inf)))
+
+
+@dataclass
+class MetricsReport:
+    makespan_ms: float
+    instances: dict[int, dict]
+    events: list[dict]
+    mem_trace: list[tuple[float, float]]
+    avg_mem_util_pct: float
+    avg_device_util_pct: float
+    oom_count: int
+    max_concurrent_holders: int
+    final_audit: list[str] = field(default_factory=list)
+
+    def summary(self) -> dict:
+        return {
+            "makespan_ms": round(self.makespan_ms, 3),
+            "avg_mem_util_pct": round(self.avg_mem_util_pct, 4),
+            "avg_device_util_pct": round(self.avg_device_util_pct, 4),
+            "oom_count": self.oom_count,
+            "max_concurrent_holders": self.max_concurrent_holders,
+            "instances": len(self.instances),
+            "audit_ok": not self.final_audit,
+        }
+
+    def to_json(self) -> str:
+        return json.dumps(self.summary(), indent=2)
+
+    def to_csv(self) -> str:
+        lines = ["t_ms,instance,event,device,bytes"]
+        for e in self.events:
+            lines.append(f"{e['t_ms']:.3f},{e['instance']},{e['event']},{e['device']},{e['bytes']}")
+        s = self.summary()
+        lines.append(f"# makespan_ms={s['makespan_ms']} avg_mem_util_pct={s['avg_mem_util_pct']} "
+                     f"avg_device_util_pct={s['avg_device_util_pct']} oom_count={s['oom_count']}")
+        return "\n".join(lines) + "\n"
+
+
+# ------------------------------------------------------------------ encoding
+
+@dataclass
+class EncodedTrace:
+    """One workload as a step program (the general mode of include/sgpu.h)."""
+    steps: np.ndarray          # STEP_DTYPE
+    step_offsets: np.ndarray   # uint32, n + 1
+    attr: np.ndarray           # uint32, n (priority rank | device << 8)
+    time_mode: int
+    tick_log2: int
+    cap_mib: int
+
+
+def _flatten(spec: WorkloadSpec) -> list[list[tuple[int, object]]]:
+    """harness.py:478-490: cpu -> alloc -> busy -> free per phase, zero fields
+    skipped, durations with the reference's float expression."""
+    progs = []
+    for prof in spec.instances:
+        flat = []
+        for ph in prof.phases:
+            if ph.cpu_ms:
+                flat.append((_lib.OP_CPU, ph.cpu_ms * spec.time_scale / 1000.0))
+            if ph.alloc_mib:
+                flat.append((_lib.OP_ALLOC, ph.alloc_mib))
+            if ph.busy_ms:
+                flat.append((_lib.OP_BUSY, ph.busy_ms * spec.time_scale / 1000.0))
+            if ph.free_mib:
+                flat.append((_lib.OP_FREE, ph.free_mib))
+        progs.append(flat)
+    return progs
+
+
+def _tick_grid(durations: list[float], cap_mib: int):
+    """Smallest e such that every duration is an integer number of 2^-e s
+    ticks and every reference float sum is exact (all times < 2^32 ticks,
+    memory integral < 2^53).  None => use float64 mode."""
+    if not durations:
+        return 10
+    fr = [Fraction(d) for d in durations]
+    e = max(f.denominator.bit_length() - 1 for f in fr)
+    if e > 62:
+        return None
+    total = sum(int(f * (1 << e)) for f in fr)
+    if total >= 0xFFFFFFFE or cap_mib * total >= (1 << 53):
+        return None
+    return e
+
+
+def encode_spec(spec: WorkloadSpec) -> EncodedTrace:
+    progs = _flatten(spec)
+    cap_mib = spec.devices[0].total_bytes // MIB
+    if spec.devices[0].total_bytes % MIB:
+        raise ValueError("device capacity must be a whole number of MiB")
+    durations = []
+    for flat in progs:
+        for op, arg in flat:
+            if op in (_lib.OP_CPU, _lib.OP_BUSY):
+                if not (arg >= 0) or math.isinf(arg):
+                    raise ValueError(f"step durations must be finite and >= 0 (got {arg!r})")
+                durations.append(arg)
+            else:
+                if int(arg) != arg or not 0 < int(arg) < 0x7FFFFFFF:
+                    raise ValueError(f"memory sizes must be whole MiB in (0, 2^31) (got {arg!r})")
+    e = _tick_grid(durations, cap_mib)
+    mode = _lib.TIME_TICKS if e is not None else _lib.TIME_F64
+    # priorities: only order and equality matter (policy.py:58-63) -> dense ranks
+    prios = sorted({int(p.priority) for p in spec.instances})
+    if len(prios) > 256:
+        raise ValueError("at most 256 distinct priorities per workload")
+    rank = {p: i for i, p in enumerate(prios)}
+    n = len(progs)
+    offs = np.zeros(n + 1, dtype=np.uint32)
+    rows = []
+    for i, flat in enumerate(progs):
+        for op, arg in flat:
+            if op in (_lib.OP_CPU, _lib.OP_BUSY):
+                if mode == _lib.TIME_TICKS:
+                    dur = int(Fraction(arg) * (1 << e))
+                else:
+                    dur = struct.unpack("<Q", struct.pack("<d", float(arg)))[0]
+                rows.append((op, 0, dur))
+            else:
+                rows.append((op, int(arg), 0))
+        offs[i + 1] = len(rows)
+    steps = np.array(rows, dtype=STEP_DTYPE) if rows else np.zeros(1, dtype=STEP_DTYPE)
+    attr = np.array([rank[int(p.priority)] for p in spec.instances], dtype=np.uint32)
+    return EncodedTrace(steps, offs, attr, mode, e if e is not None else 0, cap_mib)
+
+
+# ------------------------------------------------------------------ simulate
+
+def _gpu_device():
+    import torch
+    if not torch.cuda.is_available():
+        raise SgpuUnavailable("simulate() runs on the GPU; no CUDA device is available")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def run_encoded(enc: EncodedTrace, policy) -> dict:
+    """Run one encoded trace on the GPU with the event log; returns host
+    copies of the outputs."""
+    import torch
+    dev = _gpu_device()
+    n = len(enc.attr)
+    apps = np.zeros((n, 4), dtype=np.uint32)
+    apps[:, 3] = enc.attr
+    steps_t = torch.from_numpy(enc.steps.view(np.int32).reshape(-1, 4).copy()).to(dev)
+    offs_t = torch.from_numpy(enc.step_offsets.view(np.int32).copy()).to(dev)
+    apps_t = torch.from_numpy(apps.view(np.int32).reshape(1, n, 4).copy()).to(dev)
+    ev_cap = 2 * n + 3 * int(enc.step_offsets[-1]) + 8
+    res = simulate_batch(apps_t, (policy,), enc.cap_mib, steps=steps_t, step_offsets=offs_t,
+                         time_mode=enc.time_mode, tick_log2=enc.tick_log2,
+                         events_per_trace=ev_cap)
+    stats = res.stats()[0, 0]
+    count = int(res.event_counts[0, 0].item())
+    ev = res.events[0, 0, :min(count, ev_cap)].cpu().numpy().copy().view(
+        np.dtype([("t", "<u8"), ("app", "<u2"), ("kind", "u1"), ("dev", "u1"),
+                  ("mib", "<u4")])).reshape(-1)
+    return {"stats": stats, "events": ev, "count": count, "ev_cap": ev_cap,
+            "mem_pct": float(res.mem_pct[0, 0, 0].item()),
+            "dev_pct": float(res.dev_pct[0, 0, 0].item())}
+
+
+def _time_of(enc: EncodedTrace, raw: int) -> float:
+    if enc.time_mode == _lib.TIME_TICKS:
+        return math.ldexp(float(raw), -enc.tick_log2)
+    return struct.unpack("<d", struct.pack("<Q", int(raw)))[0]
+
+
+def simulate(spec: WorkloadSpec) -> MetricsReport:
+    """Discrete-event prediction of `spec` (memshare/harness.py:475-572) on
+    the GPU.  Deterministic; bit-identical to the reference's report."""
+    if not spec.instances:
+        return MetricsReport(0.0, {}, [], [], 0.0, 0.0, 0, 0)
+    enc = encode_spec(spec)
+    out = run_encoded(enc, spec.policy)
+    st = out["stats"]
+    if out["count"] > out["ev_cap"]:
+        raise _lib.SgpuError("event log overflow")
+    status = int(st["status"])
+    if status & (_lib.ST_TICK_OVERFLOW | _lib.ST_COUNTER_OVERFLOW | _lib.ST_BAD_DEVICE):
+        raise _lib.SgpuError(f"simulation status 0x{status:x}")
+    capacity = spec.devices[0].total_bytes
+    raw = [(_time_of(enc, int(e["t"])), int(e["app"]), int(e["kind"]), int(e["mib"]))
+           for e in out["events"]]
+    raw.sort(key=lambda x: x[0])  # stable, harness.py:567
+    if enc.time_mode == _lib.TIME_TICKS:
+        t_end = math.ldexp(float(st["makespan"]), -enc.tick_log2)
+    else:
+        t_end = float(st["makespan_s"])
+    makespan_s = max(t_end - 0.0, 1e-9)
+    instances: dict[int, dict] = {}
+    out_events = []
+    mem_points = []
+    for t, idx, kind, mib in raw:
+        name = _lib.EVENT_NAMES[kind]
+        nbytes = mib * MIB if kind in (_lib.EV_REQUEST, _lib.EV_GRANT, _lib.EV_ALLOC,
+                                       _lib.EV_FREE) else 0
+        out_events.append({"t_ms": (t - 0.0) * 1000.0, "instance": idx, "event": name,
+                           "device": 0, "bytes": nbytes})
+        inst = instances.setdefault(idx, {})
+        if kind == _lib.EV_START:
+            inst["start_ms"] = t * 1000.0
+        elif kind == _lib.EV_END:
+            inst["end_ms"] = t * 1000.0
+        elif kind == _lib.EV_ALLOC:
+            mem_points.append((t, nbytes))
+        elif kind == _lib.EV_FREE:
+            mem_points.append((t, -nbytes))
+    # 100 ms memory-utilisation samples (harness.py:439-450)
+    trace = []
+    level = 0
+    pts = iter(sorted(mem_points))
+    nxt = next(pts, None)
+    t = 0.0
+    while t <= makespan_s + 1e-9:
+        while nxt is not None and nxt[0] <= t:
+            level += nxt[1]
+            nxt = next(pts, None)
+        trace.append((t * 1000.0, level / capacity))
+        t += TICK_MS / 1000.0
+    report = MetricsReport(makespan_ms=makespan_s * 1000.0, instances=instances,
+                           events=out_events, mem_trace=trace,
+                           avg_mem_util_pct=out["mem_pct"], avg_device_util_pct=out["dev_pct"],
+                           oom_count=0, max_concurrent_holders=int(st["max_holders"]))
+    for idx, prof in enumerate(spec.instances):
+        report.instances.setdefault(idx, {})["name"] = prof.name
+        report.instances[idx]["exit"] = 0
+    return report
+
+
+def sequential_ms(spec: WorkloadSpec) -> float:
+    """Sequential makespan of the spec (sum of AppProfile.total_ms scaled),
+    the denominator of the concurrent speed-up (test_harness.py:119-126)."""
+    return sum(p.total_ms() for p in spec.instances) * spec.time_scale
+
+
+__all__ = ["Phase", "AppProfile", "builtin_profiles", "DEFAULT_DEVICE", "WorkloadSpec",
+           "MetricsReport", "simulate", "encode_spec", "sequential_ms", "TICK_MS"]

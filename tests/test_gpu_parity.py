@@ -1,0 +1,235 @@
+"""GPU parity: the sm_100a engine through the C ABI against the reference's
+golden vectors (tests/golden/, produced by the real memshare simulator) and
+the CPU oracle (oracle/, a C restatement of the same simulator) on seeded
+inputs.  Bit-exact on every integer and on the float64 percentages."""
+
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_1712_04495_b200 import batch as B
+from paper_1712_04495_b200.tracegen import CONFIGS, GenParams, as_u32x4, generate
+from util import NEVER, POLICIES, floats_equal, golden
+
+pytestmark = pytest.mark.gpu
+
+
+def to_dev(apps_u32, dev):
+    a = np.ascontiguousarray(apps_u32, dtype=np.uint32)
+    return torch.from_numpy(a.view(np.int32)).to(dev)
+
+
+def run(apps_u32, policies, caps, dev, **kw):
+    res = B.simulate_batch(to_dev(apps_u32, dev), policies, caps, **kw)
+    torch.cuda.synchronize()
+    return res
+
+
+def check_against_oracle(apps, caps, dev, policies=POLICIES):
+    res = run(apps, policies, caps, dev)
+    st = res.stats()
+    grant = res.ticks("grant").reshape(len(res.policies), *apps.shape[:2])
+    end = res.ticks("end").reshape(len(res.policies), *apps.shape[:2])
+    mem = res.mem_pct.cpu().numpy()
+    devp = res.dev_pct.cpu().numpy()
+    for pi, pol in enumerate(res.policies):
+        g, e, s = O.simulate_burst(apps, caps, pol.value)
+        np.testing.assert_array_equal(grant[pi], g, err_msg=f"grant {pol}")
+        np.testing.assert_array_equal(end[pi], e, err_msg=f"end {pol}")
+        for f in ("makespan", "busy", "mem_integral", "grants", "pops", "max_holders",
+                  "unfinished", "status"):
+            np.testing.assert_array_equal(st[pi][f], s[f], err_msg=f"{f} {pol}")
+        for d in range(len(caps)):
+            _, mp, dp = O.pct_from_stats(s[:, d], caps[d])
+            assert floats_equal(mem[pi][:, d], mp), pol
+            assert floats_equal(devp[pi][:, d], dp), pol
+    return res
+
+
+# ------------------------------------------------------------ golden vectors
+
+@pytest.mark.parametrize("cname", ["C1", "C2", "C3", "C4"])
+def test_golden_burst(cname, cuda):
+    z = golden("ref_burst.npz")
+    apps = z[f"{cname}_apps"]
+    caps = tuple(int(c) for c in z[f"{cname}_cap"])
+    res = run(apps, POLICIES, caps, cuda)
+    st = res.stats()
+    n_tr, n = apps.shape[:2]
+    grant = res.ticks("grant").reshape(4, n_tr, n)
+    end = res.ticks("end").reshape(4, n_tr, n)
+    mem = res.mem_pct.cpu().numpy()[..., 0]
+    devp = res.dev_pct.cpu().numpy()[..., 0]
+    for pi, pol in enumerate(POLICIES):
+        assert res.policies[pi].value == pol
+        np.testing.assert_array_equal(grant[pi], z[f"{cname}_{pol}_grant"])
+        np.testing.assert_array_equal(end[pi], z[f"{cname}_{pol}_end"])
+        np.testing.assert_array_equal(st[pi][:, 0]["makespan"], z[f"{cname}_{pol}_T"])
+        fl = z[f"{cname}_{pol}_floats"]
+        ms, _, _ = B.pct_host(st[pi][:, 0], caps[0])
+        assert floats_equal(ms, fl[:, 0])
+        assert floats_equal(mem[pi], fl[:, 1])
+        assert floats_equal(devp[pi], fl[:, 2])
+        ints = z[f"{cname}_{pol}_ints"]
+        np.testing.assert_array_equal(st[pi][:, 0]["max_holders"], ints[:, 0])
+        np.testing.assert_array_equal(st[pi][:, 0]["grants"], ints[:, 1])
+        np.testing.assert_array_equal(st[pi][:, 0]["unfinished"], ints[:, 2])
+
+
+def test_golden_readme_burst_c1(cuda):
+    """README burst x8 @4799 (config 1): grants at 900 and 1000 ticks,
+    6 concurrent holders, identical for all four policies."""
+    apps = as_u32x4(generate(CONFIGS["C1"].gen, 0, 1))
+    res = run(apps, POLICIES, (4799,), cuda)
+    st = res.stats()
+    for pi in range(4):
+        g = res.ticks("grant")[pi]
+        assert sorted(set(g.tolist())) == [900, 1000]
+        assert (g == 900).sum() == 6
+        assert st[pi][0, 0]["max_holders"] == 6
+        assert st[pi][0, 0]["makespan"] == 1100
+
+
+def test_golden_multidev(cuda):
+    z = golden("ref_multidev.npz")
+    apps = z["apps"]
+    caps = tuple(int(c) for c in z["cap"])
+    res = run(apps, POLICIES, caps, cuda)
+    st = res.stats()
+    n_tr, n = apps.shape[:2]
+    mem = res.mem_pct.cpu().numpy()
+    devp = res.dev_pct.cpu().numpy()
+    for pi, pol in enumerate(POLICIES):
+        np.testing.assert_array_equal(res.ticks("grant")[pi].reshape(n_tr, n), z[f"{pol}_grant"])
+        np.testing.assert_array_equal(res.ticks("end")[pi].reshape(n_tr, n), z[f"{pol}_end"])
+        np.testing.assert_array_equal(st[pi]["makespan"], z[f"{pol}_T"])
+        fl = z[f"{pol}_floats"]
+        assert floats_equal(mem[pi], fl[..., 1])
+        assert floats_equal(devp[pi], fl[..., 2])
+        ints = z[f"{pol}_ints"]
+        np.testing.assert_array_equal(st[pi]["max_holders"], ints[..., 0])
+        np.testing.assert_array_equal(st[pi]["grants"], ints[..., 1])
+        np.testing.assert_array_equal(st[pi]["unfinished"], ints[..., 2])
+
+
+# ------------------------------------------------------------ oracle, seeded
+
+@pytest.mark.parametrize("cname,nt", [("C2", 3000), ("C3", 300), ("C4", 2000), ("C5", 1500)])
+def test_oracle_seeded(cname, nt, cuda):
+    cfg = CONFIGS[cname]
+    apps = as_u32x4(generate(dataclasses.replace(cfg.gen, seed=101), 5000, nt))
+    check_against_oracle(apps, cfg.cap_mib, cuda, cfg.policies)
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 100, 255, 256, 257, 700, 1024])
+def test_apps_per_trace_shapes(n, cuda):
+    """Every K instantiation (1, 2, 4, 8, 32 apps per lane) incl. max size."""
+    g = GenParams(seed=n, apps_per_trace=n, arr_hi=3 * n, mem_lo=1, mem_hi=60_000)
+    apps = as_u32x4(generate(g, 0, 40 if n < 500 else 8))
+    check_against_oracle(apps, (184_320,), cuda)
+
+
+def test_edge_cases(cuda):
+    """Zero fields, stuck oversize requests, simultaneous arrivals, exact fits."""
+    rng = np.random.default_rng(3)
+    traces = []
+    n = 48
+    for k in range(64):
+        a = np.zeros((n, 4), dtype=np.uint32)
+        a[:, 0] = rng.choice([0, 0, 1, 5, 9], n)              # many simultaneous arrivals
+        a[:, 1] = rng.choice([0, 100, 250, 500, 1000, 1001], n)  # 0 = no alloc, 1001 > cap
+        a[:, 2] = rng.choice([0, 0, 1, 3, 7], n)              # busy 0 => free at grant
+        a[:, 3] = rng.integers(0, 4, n)
+        traces.append(a)
+    apps = np.stack(traces)
+    check_against_oracle(apps, (1000,), cuda)
+    # all-zero apps: end at t=0
+    z = np.zeros((3, 5, 4), dtype=np.uint32)
+    res = check_against_oracle(z, (10,), cuda)
+    assert (res.ticks("end") == 0).all() and (res.ticks("grant") == NEVER).all()
+
+
+def test_ragged_offsets(cuda):
+    rng = np.random.default_rng(9)
+    lens = rng.integers(0, 90, 300)
+    lens[:3] = [0, 1, 0]
+    total = int(lens.sum())
+    g = GenParams(seed=4, apps_per_trace=1)
+    flat = as_u32x4(generate(dataclasses.replace(g, apps_per_trace=total), 0, 1))[0]
+    offs = np.zeros(len(lens) + 1, dtype=np.int64)
+    np.cumsum(lens, out=offs[1:])
+    res = B.simulate_batch(to_dev(flat, cuda), POLICIES, 184_320,
+                           trace_offsets=torch.from_numpy(offs).to(cuda))
+    torch.cuda.synchronize()
+    st = res.stats()
+    for pi, pol in enumerate(res.policies):
+        for t in range(len(lens)):
+            a = flat[offs[t]:offs[t + 1]][None]
+            gg, ee, ss = O.simulate_burst(a, (184_320,), pol.value)
+            np.testing.assert_array_equal(res.ticks("grant")[pi][offs[t]:offs[t + 1]], gg[0])
+            np.testing.assert_array_equal(res.ticks("end")[pi][offs[t]:offs[t + 1]], ee[0])
+            for f in ("makespan", "busy", "mem_integral", "max_holders", "pops", "grants"):
+                assert st[pi][t, 0][f] == ss[0, 0][f], (pol, t, f)
+
+
+def test_single_policy_subsets(cuda):
+    cfg = CONFIGS["C2"]
+    apps = as_u32x4(generate(cfg.gen, 0, 200))
+    for pols in (("pmmu",), ("mmu", "pfifo")):
+        check_against_oracle(apps, cfg.cap_mib, cuda, pols)
+
+
+# ------------------------------------------------------------ other kernels
+
+@pytest.mark.parametrize("cname", ["C2", "C3", "C5"])
+def test_generator_bit_identical(cname, cuda):
+    gen = CONFIGS[cname].gen
+    t = B.generate_traces(gen, 12345, 777, device=0)
+    torch.cuda.synchronize()
+    want = as_u32x4(generate(gen, 12345, 777))
+    np.testing.assert_array_equal(t.cpu().numpy().view(np.uint32), want)
+
+
+def test_reduce_stats(cuda):
+    cfg = CONFIGS["C4"]
+    apps = as_u32x4(generate(cfg.gen, 0, 5000))
+    res = run(apps, POLICIES, cfg.cap_mib, cuda)
+    agg = B.aggr_to_dict(B.reduce_stats(res.stats_raw))
+    st = res.stats().reshape(-1)
+    assert agg["records"] == st.size
+    assert agg["sum_makespan"] == int(st["makespan"].astype(np.uint64).sum())
+    assert agg["sum_mem_integral"] == int(st["mem_integral"].astype(np.uint64).sum())
+    assert agg["sum_busy"] == int(st["busy"].astype(np.uint64).sum())
+    assert agg["sum_grants"] == int(st["grants"].astype(np.uint64).sum())
+    assert agg["sum_pops"] == int(st["pops"].astype(np.uint64).sum())
+    assert agg["max_makespan"] == int(st["makespan"].max())
+    assert agg["max_holders"] == int(st["max_holders"].max())
+    assert agg["sum_unfinished"] == int(st["unfinished"].astype(np.uint64).sum())
+
+
+def test_select_grants_batch_golden(cuda):
+    from paper_1712_04495_b200.policy import select_grants_batch
+    z = golden("ref_select.npz")
+    off = z["offsets"]
+    queues = [(z["nbytes"][off[i]:off[i + 1]], z["prio"][off[i]:off[i + 1]])
+              for i in range(len(off) - 1)]
+    masks = select_grants_batch(queues, z["free"], z["kind"].tolist())
+    got = np.concatenate([m.astype(np.uint8) for m in masks])
+    np.testing.assert_array_equal(got, z["granted"])
+
+
+def test_host_pipeline_matches_device(cuda):
+    cfg = CONFIGS["C2"]
+    apps = as_u32x4(generate(cfg.gen, 0, 10_000))
+    dres = run(apps, POLICIES, cfg.cap_mib, cuda)
+    pin = B.pinned_apps(*apps.shape[:2])
+    pin[...] = apps
+    host = B.simulate_batch_host(pin, POLICIES, cfg.cap_mib, chunk_traces=1536)
+    np.testing.assert_array_equal(host.grant, dres.ticks("grant"))
+    np.testing.assert_array_equal(host.end, dres.ticks("end"))
+    np.testing.assert_array_equal(host.stats.view(np.uint8), dres.stats().view(np.uint8))
+    assert floats_equal(host.mem_pct, dres.mem_pct.cpu().numpy())
+    assert floats_equal(host.dev_pct, dres.dev_pct.cpu().numpy())
