@@ -273,7 +273,7 @@ def run_encoded(enc: EncodedTrace, policy) -> dict:
     res = simulate_batch(apps_t, (policy,), enc.cap_mib, steps=steps_t, step_offsets=offs_t,
                          time_mode=enc.time_mode, tick_log2=enc.tick_log2,
                          events_per_trace=ev_cap)
-    stats = res.stats()[0, 0]
+    stats = res.stats()[0, 0, 0]
     count = int(res.event_counts[0, 0].item())
     ev = res.events[0, 0, :min(count, ev_cap)].cpu().numpy().copy().view(
         np.dtype([("t", "<u8"), ("app", "<u2"), ("kind", "u1"), ("dev", "u1"),

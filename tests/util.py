@@ -9,8 +9,15 @@ POLICIES = ("fifo", "mmu", "pfifo", "pmmu")
 NEVER = 0xFFFFFFFF
 
 
+_CACHE = {}
+
+
 def golden(name):
-    return np.load(os.path.join(GOLDEN, name))
+    """All arrays of a golden .npz, decompressed once."""
+    if name not in _CACHE:
+        with np.load(os.path.join(GOLDEN, name)) as z:
+            _CACHE[name] = {k: z[k] for k in z.files}
+    return _CACHE[name]
 
 
 def floats_equal(a, b):
