@@ -15,7 +15,8 @@ import threading
 from .errors import SgpuError, SgpuUnavailable
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsgpu.so")
+# SGPU_LIB: developer override (A/B builds of the same ABI); default in-tree
+LIB_PATH = os.environ.get("SGPU_LIB") or os.path.join(HERE, "libsgpu.so")
 ABI_VERSION = 1
 MAX_APPS = 1024
 MAX_DEV = 8

@@ -47,21 +47,28 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = LIB_PATH,
+          defines: tuple[str, ...] = ()) -> str:
+    if not force and out == LIB_PATH and not _stale():
         return LIB_PATH
-    tmp = LIB_PATH + f".tmp{os.getpid()}"
-    cmd = [nvcc_path(), *NVCC_FLAGS, "-I", INCLUDE, "-o", tmp,
+    tmp = out + f".tmp{os.getpid()}"
+    cmd = [nvcc_path(), *NVCC_FLAGS, "-I", INCLUDE, *[f"-D{d}" for d in defines], "-o", tmp,
            *[os.path.join(CSRC, s) for s in SOURCES]]
     t0 = time.time()
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB_PATH)
+    os.replace(tmp, out)
     if verbose:
-        print(f"built {LIB_PATH} in {time.time() - t0:.1f}s", file=sys.stderr)
-    return LIB_PATH
+        print(f"built {out} in {time.time() - t0:.1f}s", file=sys.stderr)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--out", default=LIB_PATH)
+    ap.add_argument("-D", dest="defines", action="append", default=[])
+    a = ap.parse_args()
+    build(force=a.force, verbose=True, out=a.out, defines=tuple(a.defines))

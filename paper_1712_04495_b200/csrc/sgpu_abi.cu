@@ -57,8 +57,11 @@ int validate(const sg_batch* in, Shape& s) {
     if (maxn > SG_MAX_APPS) return fail(E_RANGE, "traces longer than %d apps are not supported", SG_MAX_APPS);
     if (in->n_traces && maxn && !in->apps) return fail(E_ARG, "null apps");
     if (reinterpret_cast<uintptr_t>(in->apps) & 15u) return fail(E_ARG, "apps must be 16-byte aligned");
-    s.n_pad = (maxn + 31u) & ~31u;
-    if (s.n_pad == 0) s.n_pad = 32;
+    // apps per lane K in {1, 2, 4, 8, 16, 32}: the kernel instantiation buckets
+    const uint32_t chunks = (maxn + 31u) / 32u;
+    const uint32_t k = chunks <= 1 ? 1 : chunks <= 2 ? 2 : chunks <= 4 ? 4 : chunks <= 8 ? 8
+                       : chunks <= 16 ? 16 : 32;
+    s.n_pad = 32u * k;
     return 0;
 }
 
@@ -86,6 +89,8 @@ static int simulate_device(const sg_batch* in, const sg_out* out, cudaStream_t s
     if (rc) return rc;
     if (!out || !out->stats) return fail(E_ARG, "sg_out.stats is required");
     if (out->events && out->events_per_trace == 0) return fail(E_ARG, "events_per_trace must be > 0");
+    if (out->events && !s.program) return fail(E_ARG, "event logs require step-program mode");
+    if (out->events && s.multi) return fail(E_ARG, "event logs require ndev == 1");
     if (in->n_traces == 0) return 0;
     sg::SimParams p;
     memset(&p, 0, sizeof(p));
@@ -96,7 +101,7 @@ static int simulate_device(const sg_batch* in, const sg_out* out, cudaStream_t s
     p.apps = in->apps;
     p.steps = in->steps;
     p.step_offsets = in->step_offsets;
-    for (uint32_t i = 0; i < 4; i++) p.policies[i] = s.policies[i];
+    for (uint32_t i = 0; i < s.npol; i++) p.policy_list |= s.policies[i] << (4 * i);
     p.npol = s.npol;
     p.ndev = in->ndev;
     for (uint32_t d = 0; d < SG_MAX_DEV; d++) p.cap[d] = d < in->ndev ? in->cap_mib[d] : 1;
@@ -111,9 +116,9 @@ static int simulate_device(const sg_batch* in, const sg_out* out, cudaStream_t s
     p.events = out->events;
     p.event_counts = out->event_counts;
     sg::sim_layout(p, s.program, s.f64);
-    if (p.warp_bytes * sg::kSimWarpsPerBlock > 227u * 1024u)
-        return fail(E_RANGE, "shared memory per block exceeds 227 KB (n_pad=%u)", s.n_pad);
-    cudaError_t e = sg::launch_sim(p, s.program, s.f64, s.multi, stream, nullptr);
+    if (p.warp_bytes > 227u * 1024u)
+        return fail(E_RANGE, "shared memory per warp exceeds 227 KB (n_pad=%u)", s.n_pad);
+    cudaError_t e = sg::launch_sim(p, s.program, s.f64, stream, nullptr);
     if (e != cudaSuccess) return cuda_fail(e, "trace_sim launch");
     return 0;
 }

@@ -18,7 +18,7 @@ struct SimParams {
     const sg_app* apps;
     const sg_step* steps;           // program mode
     const uint32_t* step_offsets;
-    uint32_t policies[4];
+    uint32_t policy_list;           // policy codes, 4 bits each, in output order
     uint32_t npol;
     uint32_t ndev;
     uint32_t cap[SG_MAX_DEV];
@@ -33,15 +33,16 @@ struct SimParams {
     sg_event* events;
     uint32_t* event_counts;
     // per-warp shared-memory layout (bytes)
-    uint32_t off_app, off_q, off_grant, off_end, off_pc, off_held, off_bar, warp_bytes;
+    uint32_t off_app, off_sub, off_idx, off_key, off_kc, off_q, off_grant, off_end, off_st, off_held,
+        off_bar, warp_bytes;
 };
 
 // Shared-memory layout for one warp simulating traces of up to n_pad apps.
 void sim_layout(SimParams& p, bool program_mode, bool f64);
 
 // Launch K1 (trace simulation).  Returns a cudaError_t.
-cudaError_t launch_sim(const SimParams& p, bool program_mode, bool f64, bool multi,
-                       cudaStream_t stream, int* grid_out);
+cudaError_t launch_sim(const SimParams& p, bool program_mode, bool f64, cudaStream_t stream,
+                       int* grid_out);
 
 cudaError_t launch_reduce(const sg_trace_stats* stats, uint64_t count, sg_aggr* out,
                           cudaStream_t stream);

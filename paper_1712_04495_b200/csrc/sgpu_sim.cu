@@ -12,119 +12,156 @@
 //                    busy union, max concurrent holders), fused incrementally
 //
 // B200 mapping:
-//   * warp per trace, all policies of a trace back to back on the staged copy;
-//     persistent grid (SMs x resident blocks), grid-stride over traces
+//   * warp per trace, all requested policies of a trace back to back on one
+//     staged copy; persistent grid (SMs x resident blocks), grid-stride
 //   * the trace's 16 B/app records are staged global->shared by the TMA bulk
 //     engine (cp.async.bulk + mbarrier), double-buffered so trace i+1 streams
 //     in while trace i is simulated
-//   * the heap is a per-app (t, counter) key held in registers (lane l owns
-//     apps l, l+32, ...); the next event is a two-step REDUX min (time, then
-//     counter) — exact restatement of heapq's tuple order
-//   * the wait queue (enqueue order) lives in shared memory; FIFO grants are a
-//     warp prefix-sum + ballot, MMU first-fit is a __ballot_sync/__ffs loop,
-//     priority classes a REDUX max — no atomics anywhere on event times
+//   * the heap is a per-app packed (t, counter, app) key in shared memory; lane
+//     l owns apps l, l+32, ...; each pop is one lane-local min over its slots
+//     plus a two-step REDUX min (time, then counter) — the exact tuple order of
+//     heapq; grants write their keys lane-parallel
+//   * the wait queue lives in shared memory in enqueue order.  T0 apps enqueue
+//     at most once, so the queue is position-stable with a presence bitmask per
+//     32 entries (no compaction); FIFO and MMU selection are __ballot_sync/__ffs
+//     loops, the priority class a REDUX max — no atomics on event times
+//   * all control flow is warp-uniform: every lane holds the same scalar state
+//     (ledger, counters, statistics) in registers
+//   * traces with several simulated devices run as per-device sub-traces: the
+//     devices share only the global push counter, whose interleaving cannot
+//     reorder events of one device (pinned by tests/golden/ref_multidev.npz)
 #include <cmath>
+#include <type_traits>
 
 #include "sgpu_common.cuh"
 #include "sgpu_internal.h"
 
 namespace sg {
 
-constexpr uint32_t kBusyFlag = 0x8000u;   // s_pc bit: the pending pop ends a busy step
+constexpr uint32_t kBusyFlag = 0x8000u;   // s_st bit: the pending pop ends a busy step
+constexpr uint32_t kAllocPending = 0x2u;  // s_st bit (T0): the alloc step has not run
 constexpr uint32_t kSat = 0x7FFFFFFFu;    // MiB saturation for FIFO prefix sums
 constexpr uint32_t kAppBits = 10;         // SG_MAX_APPS == 1 << kAppBits
+constexpr uint32_t kAppMask = (1u << kAppBits) - 1;
 constexpr uint32_t kCounterLimit = 1u << (32 - kAppBits);
 constexpr double kMiB = 1048576.0;
 
 // ------------------------------------------------------------ time models
 
+// Integer ticks.  Heap key = t << 32 | counter << 10 | app (one u64).
 struct TickTM {
     using T = uint32_t;
-    using Key = uint32_t;
     using Acc = uint64_t;
+    using Key = uint64_t;
     static constexpr bool F64 = false;
-    static constexpr Key INFK = 0xFFFFFFFFu;
-    static __device__ __forceinline__ Key key(T t) { return t; }
-    static __device__ __forceinline__ T time(Key k) { return k; }
+    static __device__ __forceinline__ Key inf() { return ~0ull; }
+    static __device__ __forceinline__ Key make_key(T t, uint32_t c, uint32_t app) {
+        return ((uint64_t)t << 32) | (c << kAppBits) | app;
+    }
+    static __device__ __forceinline__ bool less(Key a, Key b) { return a < b; }
+    static __device__ __forceinline__ Key load(const uint64_t* kt, const uint32_t*, uint32_t i) {
+        return kt[i];
+    }
+    static __device__ __forceinline__ void store(uint64_t* kt, uint32_t*, uint32_t i, Key k) {
+        kt[i] = k;
+    }
+    // heapq order: min time, then min counter; false when the heap is empty
+    static __device__ __forceinline__ bool argmin(Key lk, T& now, uint32_t& app) {
+        const uint32_t hi = __reduce_min_sync(FULL, (uint32_t)(lk >> 32));
+        const uint32_t lo = __reduce_min_sync(FULL, (uint32_t)(lk >> 32) == hi ? (uint32_t)lk : ~0u);
+        now = hi;
+        app = lo & kAppMask;
+        return hi != ~0u;
+    }
     static __device__ __forceinline__ T zero() { return 0u; }
     static __device__ __forceinline__ T never() { return SG_NEVER; }
     static __device__ __forceinline__ bool is_never(T t) { return t == SG_NEVER; }
-    static __device__ __forceinline__ T add(T now, uint64_t dur, bool& ovf) {
-        uint64_t s = (uint64_t)now + dur;
-        if (s > 0xFFFFFFFEull) { ovf = true; s = 0xFFFFFFFEull; }
+    static __device__ __forceinline__ T add(T now, uint64_t dur, uint32_t& status) {
+        const uint64_t s = (uint64_t)now + dur;
+        if (s > 0xFFFFFFFEull) { status |= SG_ST_TICK_OVERFLOW; return 0xFFFFFFFEu; }
         return (T)s;
     }
-    static __device__ __forceinline__ Key warp_min(Key k) { return __reduce_min_sync(FULL, k); }
     static __device__ __forceinline__ uint64_t bits(T t) { return t; }
 };
 
+// float64 seconds (reference arithmetic).  Heap key = (t bits, counter/app).
 struct F64TM {
     using T = double;
-    using Key = uint64_t;
     using Acc = double;
+    struct Key {
+        uint64_t t;
+        uint32_t c;
+    };
     static constexpr bool F64 = true;
-    static constexpr Key INFK = 0xFFFFFFFFFFFFFFFFull;
-    // Event times are non-negative doubles: their IEEE bit patterns order
-    // like the values, so the heap key is the raw bits.
-    static __device__ __forceinline__ Key key(T t) { return (Key)__double_as_longlong(t); }
-    static __device__ __forceinline__ T time(Key k) { return __longlong_as_double((long long)k); }
+    static __device__ __forceinline__ Key inf() { return Key{~0ull, ~0u}; }
+    // event times are non-negative doubles: their bit patterns order like values
+    static __device__ __forceinline__ Key make_key(T t, uint32_t c, uint32_t app) {
+        return Key{(uint64_t)__double_as_longlong(t), (c << kAppBits) | app};
+    }
+    static __device__ __forceinline__ bool less(Key a, Key b) {
+        return a.t < b.t || (a.t == b.t && a.c < b.c);
+    }
+    static __device__ __forceinline__ Key load(const uint64_t* kt, const uint32_t* kc, uint32_t i) {
+        return Key{kt[i], kc[i]};
+    }
+    static __device__ __forceinline__ void store(uint64_t* kt, uint32_t* kc, uint32_t i, Key k) {
+        kt[i] = k.t;
+        kc[i] = k.c;
+    }
+    static __device__ __forceinline__ bool argmin(Key lk, T& now, uint32_t& app) {
+        const uint64_t t = warp_min_u64(lk.t);
+        const uint32_t c = __reduce_min_sync(FULL, lk.t == t ? lk.c : ~0u);
+        now = __longlong_as_double((long long)t);
+        app = c & kAppMask;
+        return t != ~0ull;
+    }
     static __device__ __forceinline__ T zero() { return 0.0; }
     static __device__ __forceinline__ T never() { return __longlong_as_double(-1LL); }  // NaN
     static __device__ __forceinline__ bool is_never(T t) { return isnan(t); }
-    static __device__ __forceinline__ T add(T now, uint64_t dur, bool&) {
+    static __device__ __forceinline__ T add(T now, uint64_t dur, uint32_t&) {
         return __dadd_rn(now, __longlong_as_double((long long)dur));  // harness.py:517,519
     }
-    static __device__ __forceinline__ Key warp_min(Key k) { return warp_min_u64(k); }
     static __device__ __forceinline__ uint64_t bits(T t) { return (uint64_t)__double_as_longlong(t); }
-};
-
-template <class TM>
-struct DevState {
-    typename TM::T last;       // time of the latest pop of this device's apps = makespan
-    typename TM::T mem_t;      // time of the previous memory point
-    typename TM::T busy_prev;  // time of the previous busy point
-    typename TM::Acc I;        // memory integral (MiB*ticks, or byte-seconds)
-    typename TM::Acc B;        // busy union (ticks, or seconds)
-    int64_t used;              // MiB held
-    int32_t busy_level;
-    int32_t holders;
-    uint32_t maxh;
-    uint32_t grants;
-    uint32_t pops;
 };
 
 __device__ __forceinline__ uint32_t q_app(uint64_t e) { return (uint32_t)(e >> 32) & 0xFFFFu; }
 __device__ __forceinline__ uint32_t q_prio(uint64_t e) { return (uint32_t)(e >> 48) & 0xFFu; }
-__device__ __forceinline__ uint32_t q_dev(uint64_t e) { return (uint32_t)(e >> 56); }
-__device__ __forceinline__ uint64_t q_pack(uint32_t app, uint32_t mib, uint32_t prio, uint32_t d) {
-    return ((uint64_t)d << 56) | ((uint64_t)(prio & 0xFF) << 48) | ((uint64_t)app << 32) | mib;
+__device__ __forceinline__ uint64_t q_pack(uint32_t app, uint32_t mib, uint32_t prio) {
+    return ((uint64_t)(prio & 0xFF) << 48) | ((uint64_t)app << 32) | mib;
 }
 
-template <class TM, int K, bool PROG, bool MULTI>
+// One (sub-)trace of n apps on one simulated device under one policy.
+template <class TM, int K, bool PROG>
 struct TraceSim {
     using T = typename TM::T;
     using Key = typename TM::Key;
-    using DS = DevState<TM>;
+    using Used = typename std::conditional<PROG, int64_t, uint32_t>::type;
 
     const SimParams& P;
     const uint32_t lane;
     // per-warp shared memory
     const uint4* s_app;
     uint64_t* s_q;
+    uint64_t* s_kt;
+    uint32_t* s_kc;
     T* s_grant;
     T* s_end;
-    uint16_t* s_pc;
+    uint16_t* s_st;
     int32_t* s_held;
     // trace / policy
-    uint32_t n;
+    uint32_t n, cap;
     bool prio_pol, mmu;
-    // simulation state (warp-uniform unless noted)
-    uint32_t qlen, counter, status;
-    Key kt[K];        // per-lane: pending time key of apps lane + 32*j
-    uint32_t kc[K];   // per-lane: counter << 10 | app
-    Key lt;           // per-lane: local minimum key
-    uint32_t lc;
-    DS ds[MULTI ? SG_MAX_DEV : 1];
+    // warp-uniform simulation state
+    uint32_t counter, status;
+    uint32_t qlen;            // PROG: compacted queue length; T0: waiting entries
+    uint32_t qtail;           // T0: next queue position (apps enqueue at most once)
+    uint32_t qm_lane;         // T0: lane j holds the presence bits of queue positions 32j..32j+31
+    // statistics (harness.py:373-461 integer forms)
+    T last, mem_t, busy_prev;
+    typename TM::Acc I, B;
+    Used used;
+    int32_t busy_level, holders;
+    uint32_t maxh, grants, pops;
     sg_event* ev;
     uint32_t ev_n;
 
@@ -133,184 +170,217 @@ struct TraceSim {
         : P(p), lane(lane_) {
         s_app = apps_smem;
         s_q = reinterpret_cast<uint64_t*>(ws + p.off_q);
+        s_kt = reinterpret_cast<uint64_t*>(ws + p.off_key);
+        s_kc = reinterpret_cast<uint32_t*>(ws + p.off_kc);
         s_grant = reinterpret_cast<T*>(ws + p.off_grant);
         s_end = reinterpret_cast<T*>(ws + p.off_end);
-        s_pc = reinterpret_cast<uint16_t*>(ws + p.off_pc);
+        s_st = reinterpret_cast<uint16_t*>(ws + p.off_st);
         s_held = reinterpret_cast<int32_t*>(ws + p.off_held);
     }
 
-    __device__ __forceinline__ DS& dev(uint32_t d) {
-        if constexpr (MULTI) return ds[d];
-        else return ds[0];
-    }
-    __device__ __forceinline__ uint32_t dev_of(uint32_t attr) {
-        if constexpr (MULTI) {
-            uint32_t d = (attr >> 8) & 0xFF;
-            return d < P.ndev ? d : 0;
-        } else {
-            return 0;
-        }
-    }
-
-    // ---------------------------------------------------------------- keys
-    __device__ __forceinline__ void set_key(uint32_t app, Key k, uint32_t c) {
-        const uint32_t owner = app & 31, slot = app >> 5;
-#pragma unroll
-        for (int j = 0; j < K; j++)
-            if (lane == owner && slot == (uint32_t)j) { kt[j] = k; kc[j] = (c << kAppBits) | app; }
-    }
-    __device__ __forceinline__ void clear_key(uint32_t app) {
-        const uint32_t owner = app & 31, slot = app >> 5;
-#pragma unroll
-        for (int j = 0; j < K; j++)
-            if (lane == owner && slot == (uint32_t)j) { kt[j] = TM::INFK; kc[j] = 0xFFFFFFFFu; }
-    }
-    __device__ __forceinline__ void local_min() {
-        lt = kt[0];
-        lc = kc[0];
-#pragma unroll
-        for (int j = 1; j < K; j++)
-            if (kt[j] < lt || (kt[j] == lt && kc[j] < lc)) { lt = kt[j]; lc = kc[j]; }
-    }
-    // harness.py:505-508
-    __device__ __forceinline__ void push(uint32_t app, T t) {
+    // harness.py:505-508: a push takes the next counter value
+    __device__ __forceinline__ Key push_key(T t, uint32_t app) {
         counter += 1;
         if (counter >= kCounterLimit) status |= SG_ST_COUNTER_OVERFLOW;
-        set_key(app, TM::key(t), counter);
+        return TM::make_key(t, counter, app);
     }
 
     // -------------------------------------------------------------- events
-    __device__ __forceinline__ void emit(T t, uint32_t app, uint32_t kind, uint32_t d, uint32_t mib) {
-        if (ev != nullptr) {
-            if (lane == 0 && ev_n < P.ev_cap) {
-                sg_event e;
-                e.t = TM::bits(t);
-                e.app = (uint16_t)app;
-                e.kind = (uint8_t)kind;
-                e.dev = (uint8_t)d;
-                e.mib = mib;
-                ev[ev_n] = e;
+    __device__ __forceinline__ void emit(T t, uint32_t app, uint32_t kind, uint32_t mib) {
+        if constexpr (PROG) {
+            if (ev != nullptr) {
+                if (lane == 0 && ev_n < P.ev_cap) {
+                    sg_event e;
+                    e.t = TM::bits(t);
+                    e.app = (uint16_t)app;
+                    e.kind = (uint8_t)kind;
+                    e.dev = 0;
+                    e.mib = mib;
+                    ev[ev_n] = e;
+                }
+                ev_n++;
             }
-            ev_n++;
         }
     }
 
     // ---------------------------------------------------------- statistics
     // Memory point: total += level * (t - prev) (harness.py:414-426).
-    __device__ __forceinline__ void mem_point(DS& D, T now, int64_t delta) {
+    __device__ __forceinline__ void mem_point(T now) {
         if constexpr (TM::F64) {
-            D.I = __dadd_rn(D.I, __dmul_rn(__ll2double_rn(D.used * 1048576LL), __dsub_rn(now, D.mem_t)));
+            I = __dadd_rn(I, __dmul_rn(__ll2double_rn((int64_t)used * 1048576LL), __dsub_rn(now, mem_t)));
+        } else if constexpr (PROG) {
+            I += (uint64_t)(used * (int64_t)(now - mem_t));
         } else {
-            D.I += (uint64_t)(D.used * (int64_t)(now - D.mem_t));
+            I += (uint64_t)used * (uint32_t)(now - mem_t);
         }
-        D.mem_t = now;
-        D.used += delta;
+        mem_t = now;
     }
     // Busy point in time order: the sweep of harness.py:429-437.  Points of
     // equal time add zero, so pop order within a tick is immaterial.
-    __device__ __forceinline__ void busy_point(DS& D, T now, int32_t delta) {
-        if (D.busy_level > 0) {
-            if constexpr (TM::F64) D.B = __dadd_rn(D.B, __dsub_rn(now, D.busy_prev));
-            else D.B += (uint64_t)(now - D.busy_prev);
+    __device__ __forceinline__ void busy_point(T now, int32_t delta) {
+        if (busy_level > 0) {
+            if constexpr (TM::F64) B = __dadd_rn(B, __dsub_rn(now, busy_prev));
+            else B += (uint32_t)(now - busy_prev);
         }
-        D.busy_prev = now;
-        D.busy_level += delta;
+        busy_prev = now;
+        busy_level += delta;
     }
 
-    // ------------------------------------------------------- grant_waiters
-    // harness.py:545-558 with select_grants (policy.py:52-74) inlined as warp
-    // scans over the shared-memory queue (device d's entries only).
-    __device__ void grant_waiters(uint32_t d, T now) {
+    // ------------------------------------------- grant_waiters (T0 traces)
+    // harness.py:545-558 + policy.py:52-74 over the position-stable queue.
+    __device__ __forceinline__ void grant_waiters_t0(T now) {
         if (qlen == 0) return;
-        DS& D = dev(d);
-        const int64_t cap = (int64_t)P.cap[MULTI ? d : 0];
         while (true) {
-            int64_t budget = cap - D.used;
+            uint32_t budget = cap - used;
+            const uint32_t budget0 = budget;
             uint32_t top = 0;
-            if (prio_pol || MULTI) {
-                // top = max priority among device-d waiters (policy.py:58-63)
-                uint32_t best = 0;  // priority + 1, 0 = none
-                for (uint32_t base = 0; base < qlen; base += 32) {
-                    const uint32_t i = base + lane;
-                    if (i < qlen) {
-                        const uint64_t e = s_q[i];
-                        if (!MULTI || q_dev(e) == d) best = max(best, q_prio(e) + 1);
+            const uint32_t active = __ballot_sync(FULL, qm_lane != 0);  // chunks with waiters
+            if (prio_pol) {
+                // top = max waiting priority (policy.py:58-63)
+                uint32_t best = 0;
+                for (uint32_t a = active; a; a &= a - 1) {
+                    const uint32_t j = __ffs(a) - 1;
+                    const uint32_t m = __shfl_sync(FULL, qm_lane, j);
+                    const uint64_t e = s_q[32 * j + lane];
+                    if ((m >> lane) & 1u) best = max(best, q_prio(e) + 1);
+                }
+                top = __reduce_max_sync(FULL, best) - 1;
+            }
+            uint32_t granted = 0;
+            bool stop = false;
+            for (uint32_t a = active; a && !stop; a &= a - 1) {
+                const uint32_t j = __ffs(a) - 1;
+                uint32_t rem = __shfl_sync(FULL, qm_lane, j);
+                const uint64_t e = s_q[32 * j + lane];
+                const uint32_t mib = (uint32_t)e;
+                const uint32_t app_l = q_app(e);
+                if (prio_pol) rem &= __ballot_sync(FULL, q_prio(e) == top);
+                const bool cand = (rem >> lane) & 1u;
+                uint32_t gm = 0;
+                if (!mmu) {
+                    // FIFO: grant from the head while it fits; a misfit blocks.
+                    while (rem) {
+                        const uint32_t h = __ffs(rem) - 1;
+                        const uint32_t mh = __shfl_sync(FULL, mib, h);
+                        if (mh > budget) { stop = true; break; }
+                        gm |= 1u << h;
+                        budget -= mh;
+                        rem &= rem - 1;
+                    }
+                } else {
+                    // MMU: first fit with a shrinking budget, skip misfits.
+                    while (rem) {
+                        const uint32_t fm = __ballot_sync(FULL, cand && mib <= budget) & rem;
+                        if (!fm) break;
+                        const uint32_t h = __ffs(fm) - 1;
+                        gm |= 1u << h;
+                        budget -= __shfl_sync(FULL, mib, h);
+                        rem &= (h == 31) ? 0u : (0xFFFFFFFFu << (h + 1));
                     }
                 }
-                best = __reduce_max_sync(FULL, best);
-                if (best == 0) return;
-                top = best - 1;
+                if (gm) {
+                    // grants in queue order: pc past the alloc, push (now, ++counter)
+                    if ((gm >> lane) & 1u) {
+                        TM::store(s_kt, s_kc, app_l,
+                                  TM::make_key(now, counter + __popc(gm & lanemask_lt()) + 1, app_l));
+                        s_grant[app_l] = now;
+                        s_st[app_l] = 0;
+                    }
+                    const uint32_t g = __popc(gm);
+                    counter += g;
+                    granted += g;
+                    if (lane == j) qm_lane &= ~gm;
+                }
+            }
+            if (granted) {
+                mem_point(now);
+                used += budget0 - budget;
+                holders += (int32_t)granted;
+                maxh = max(maxh, (uint32_t)holders);
+                grants += granted;
+                qlen -= granted;
+                if (counter >= kCounterLimit) status |= SG_ST_COUNTER_OVERFLOW;
+            }
+            // FIFO/MMU: a second round is provably empty; priority policies
+            // drain the top class and may serve the next one (harness.py:547-550)
+            if (granted == 0 || !prio_pol || qlen == 0) return;
+        }
+    }
+
+    // ----------------------------------------- grant_waiters (step programs)
+    // Apps may wait several times: the queue is compacted after each round.
+    __device__ __forceinline__ void grant_waiters_prog(T now) {
+        if (qlen == 0) return;
+        while (true) {
+            int64_t budget = (int64_t)cap - (int64_t)used;
+            uint32_t top = 0;
+            if (prio_pol) {
+                uint32_t best = 0;
+                for (uint32_t base = 0; base < qlen; base += 32) {
+                    const uint32_t i = base + lane;
+                    if (i < qlen) best = max(best, q_prio(s_q[i]) + 1);
+                }
+                top = __reduce_max_sync(FULL, best) - 1;
             }
             uint32_t removed = 0;
             bool stop = false;
-            int64_t carry = 0;
             for (uint32_t base = 0; base < qlen; base += 32) {
                 const uint32_t i = base + lane;
                 const bool valid = i < qlen;
                 const uint64_t e = valid ? s_q[i] : 0ull;
                 const uint32_t mib = (uint32_t)e;
                 const uint32_t app_l = q_app(e);
-                const bool cand = valid && !stop && (!MULTI || q_dev(e) == d) &&
-                                  (!prio_pol || q_prio(e) == top);
+                const bool cand = valid && !stop && (!prio_pol || q_prio(e) == top);
+                uint32_t rem = __ballot_sync(FULL, cand);
                 uint32_t gm = 0;
-                if (__any_sync(FULL, cand)) {
-                    if (!mmu) {
-                        // FIFO: longest prefix whose running sum fits.
-                        uint32_t incl = cand ? min(mib, kSat) : 0u;
-#pragma unroll
-                        for (int off = 1; off < 32; off <<= 1) {
-                            const uint32_t y = __shfl_up_sync(FULL, incl, off);
-                            if (lane >= (uint32_t)off) incl = min(incl + y, kSat);
-                        }
-                        const bool fits = cand && (carry + (int64_t)incl <= budget);
-                        gm = __ballot_sync(FULL, fits);
-                        if (__ballot_sync(FULL, cand && !fits)) stop = true;
-                        carry += (int64_t)__shfl_sync(FULL, incl, 31);
-                    } else {
-                        // MMU: first fit with a shrinking budget, skip misfits.
-                        uint32_t rem = __ballot_sync(FULL, cand);
-                        while (rem) {
-                            const uint32_t fm = __ballot_sync(FULL, cand && (int64_t)mib <= budget) & rem;
-                            if (!fm) break;
-                            const uint32_t j = __ffs(fm) - 1;
-                            gm |= 1u << j;
-                            budget -= (int64_t)__shfl_sync(FULL, mib, j);
-                            rem &= (j == 31) ? 0u : (0xFFFFFFFFu << (j + 1));
-                        }
+                if (!mmu) {
+                    while (rem) {
+                        const uint32_t h = __ffs(rem) - 1;
+                        const int64_t mh = __shfl_sync(FULL, mib, h);
+                        if (mh > budget) { stop = true; break; }
+                        gm |= 1u << h;
+                        budget -= mh;
+                        rem &= rem - 1;
+                    }
+                } else {
+                    while (rem) {
+                        const uint32_t fm = __ballot_sync(FULL, cand && (int64_t)mib <= budget) & rem;
+                        if (!fm) break;
+                        const uint32_t h = __ffs(fm) - 1;
+                        gm |= 1u << h;
+                        budget -= (int64_t)__shfl_sync(FULL, mib, h);
+                        rem &= (h == 31) ? 0u : (0xFFFFFFFFu << (h + 1));
                     }
                 }
                 const bool mine = (gm >> lane) & 1u;
                 const uint32_t below = __popc(gm & lanemask_lt());
                 if (gm) {
-                    // grant in queue order: used += nbytes, grant + alloc events,
-                    // pc past the alloc, push (now, ++counter)  (harness.py:551-558)
                     const uint32_t g = __popc(gm);
                     const uint32_t sum = __reduce_add_sync(FULL, mine ? mib : 0u);
-                    mem_point(D, now, (int64_t)sum);
-                    if constexpr (PROG) {
-                        bool inc = false;
-                        if (mine) {
-                            const int32_t h = s_held[app_l];
-                            const int32_t nh = h + (int32_t)mib;
-                            s_held[app_l] = nh;
-                            inc = h <= 0 && nh > 0;
-                            s_pc[app_l] = (uint16_t)(s_pc[app_l] + 1);
-                        }
-                        D.holders += __popc(__ballot_sync(FULL, inc));
-                    } else {
-                        D.holders += (int32_t)g;
-                        if (mine) s_pc[app_l] = 2;
+                    mem_point(now);
+                    used += sum;
+                    bool inc = false;
+                    if (mine) {
+                        TM::store(s_kt, s_kc, app_l, TM::make_key(now, counter + below + 1, app_l));
+                        if (TM::is_never(s_grant[app_l])) s_grant[app_l] = now;
+                        s_st[app_l] = (uint16_t)(s_st[app_l] + 1);
+                        const int32_t h = s_held[app_l];
+                        const int32_t nh = h + (int32_t)mib;
+                        s_held[app_l] = nh;
+                        inc = h <= 0 && nh > 0;
                     }
-                    if (mine && TM::is_never(s_grant[app_l])) s_grant[app_l] = now;
-                    D.maxh = max(D.maxh, (uint32_t)max(D.holders, 0));
-                    D.grants += g;
+                    holders += __popc(__ballot_sync(FULL, inc));
+                    counter += g;
+                    if (counter >= kCounterLimit) status |= SG_ST_COUNTER_OVERFLOW;
+                    maxh = max(maxh, (uint32_t)max(holders, 0));
+                    grants += g;
                     if (ev != nullptr) {
                         if (mine) {
                             const uint32_t pos = ev_n + 2 * below;
                             sg_event e1;
                             e1.t = TM::bits(now);
                             e1.app = (uint16_t)app_l;
-                            e1.dev = (uint8_t)d;
+                            e1.dev = 0;
                             e1.mib = mib;
                             e1.kind = SG_EV_GRANT;
                             if (pos < P.ev_cap) ev[pos] = e1;
@@ -319,18 +389,7 @@ struct TraceSim {
                         }
                         ev_n += 2 * g;
                     }
-                    const uint32_t c0 = counter;
-                    counter += g;
-                    if (counter >= kCounterLimit) status |= SG_ST_COUNTER_OVERFLOW;
-                    uint32_t rem = gm, k = 0;
-                    while (rem) {
-                        const uint32_t j = __ffs(rem) - 1;
-                        rem &= rem - 1;
-                        const uint32_t a = __shfl_sync(FULL, app_l, j);
-                        set_key(a, TM::key(now), c0 + (++k));
-                    }
                 }
-                // stable compaction of the survivors
                 const uint32_t shift = removed + below;
                 __syncwarp();
                 if (valid && !mine && shift) s_q[i - shift] = e;
@@ -338,123 +397,137 @@ struct TraceSim {
                 __syncwarp();
             }
             qlen -= removed;
-            // FIFO/MMU: a second round is provably empty (every survivor
-            // already failed against a budget >= the current one); priority
-            // policies drain the top class and may serve the next one in the
-            // same tick (fixpoint, harness.py:547-550).
             if (removed == 0 || !prio_pol || qlen == 0) return;
         }
     }
 
-    // -------------------------------------------------------------- advance
-    // harness.py:510-543: run app's steps from its pc until it blocks.
-    __device__ void advance(uint32_t app, T now, bool counted_pop) {
+    // ---------------------------------------------------- advance (T0 mode)
+    // harness.py:510-543 on the flattened program cpu/alloc/busy/free.  The
+    // cpu step only runs at the initial pop (run()); a popped app is either
+    // arriving (alloc pending), granted from the queue (busy next) or ending
+    // its busy step (free next), so the rest is straight-line code.
+    __device__ __forceinline__ void advance_t0(uint32_t app, T now) {
         const uint4 f = s_app[app];
-        uint32_t pc = s_pc[app];
-        int32_t held = 0;
-        if constexpr (PROG) held = s_held[app];
+        const uint32_t st = s_st[app];
         __syncwarp();
-        const uint32_t d = dev_of(f.w);
-        DS& D = dev(d);
-        const int64_t cap = (int64_t)P.cap[MULTI ? d : 0];
-        D.last = now;
-        if (counted_pop) D.pops += 1;
+        last = now;
+        pops += 1;
+        Key nk = TM::inf();
+        if (st & kBusyFlag) {
+            busy_point(now, -1);
+        } else {
+            if (st & kAllocPending) {
+                if (f.y <= cap - used) {  // arrival bypass (harness.py:521-531)
+                    mem_point(now);
+                    used += f.y;
+                    holders += 1;
+                    maxh = max(maxh, (uint32_t)holders);
+                    grants += 1;
+                    s_grant[app] = now;
+                } else {                   // wait (harness.py:532-536)
+                    s_q[qtail] = q_pack(app, min(f.y, kSat), f.w & 0xFFu);
+                    if (lane == (qtail >> 5)) qm_lane |= 1u << (qtail & 31);
+                    qtail += 1;
+                    qlen += 1;
+                    TM::store(s_kt, s_kc, app, nk);
+                    return;
+                }
+            }
+            if (f.z) {  // busy (harness.py:514-520)
+                busy_point(now, +1);
+                nk = push_key(TM::add(now, f.z, status), app);
+                s_st[app] = kBusyFlag;
+                TM::store(s_kt, s_kc, app, nk);
+                return;
+            }
+        }
+        if (f.y) {  // free -> grant_waiters (harness.py:537-542)
+            mem_point(now);
+            used -= f.y;
+            holders -= 1;
+            grant_waiters_t0(now);
+        }
+        s_end[app] = now;  // harness.py:543
+        s_st[app] = 0;
+        TM::store(s_kt, s_kc, app, nk);
+    }
+
+    // ------------------------------------------------- advance (programs)
+    __device__ __forceinline__ void advance_prog(uint32_t app, T now) {
+        const uint4 f = s_app[app];  // x = first step, y = step count
+        uint32_t pc = s_st[app];
+        int32_t held = s_held[app];
+        __syncwarp();
+        last = now;
+        pops += 1;
         if (pc & kBusyFlag) {
-            busy_point(D, now, -1);
+            busy_point(now, -1);
             pc &= ~kBusyFlag;
         }
+        Key nk = TM::inf();
         while (true) {
-            uint32_t op = 0, mib = 0;
-            uint64_t dur = 0;
-            bool done = false;
-            if constexpr (PROG) {
-                if (pc >= f.y) {
-                    done = true;
-                } else {
-                    const uint4 st = __ldg(reinterpret_cast<const uint4*>(P.steps) + f.x + pc);
-                    op = st.x;
-                    mib = st.y;
-                    dur = ((uint64_t)st.w << 32) | st.z;
-                }
-            } else {
-                // T0: cpu(arrival) -> alloc(mem) -> busy(busy) -> free(mem),
-                // zero fields skipped (harness.py:482-489)
-                if (pc == 0) {
-                    if (f.x) { op = SG_OP_CPU; dur = f.x; } else { pc = 1; continue; }
-                } else if (pc == 1) {
-                    if (f.y) { op = SG_OP_ALLOC; mib = f.y; } else { pc = 2; continue; }
-                } else if (pc == 2) {
-                    if (f.z) { op = SG_OP_BUSY; dur = f.z; } else { pc = 3; continue; }
-                } else if (pc == 3) {
-                    if (f.y) { op = SG_OP_FREE; mib = f.y; } else { pc = 4; continue; }
-                } else {
-                    done = true;
-                }
-            }
-            if (done) {  // harness.py:543
+            if (pc >= f.y) {  // harness.py:543
                 s_end[app] = now;
-                s_pc[app] = (uint16_t)pc;
-                emit(now, app, SG_EV_END, d, 0);
-                return;
+                emit(now, app, SG_EV_END, 0);
+                break;
             }
+            const uint4 stp = __ldg(reinterpret_cast<const uint4*>(P.steps) + f.x + pc);
+            const uint32_t op = stp.x, mib = stp.y;
+            const uint64_t dur = ((uint64_t)stp.w << 32) | stp.z;
             if (op == SG_OP_CPU || op == SG_OP_BUSY) {  // harness.py:514-520
-                bool ovf = false;
-                const T t2 = TM::add(now, dur, ovf);
-                if (ovf) status |= SG_ST_TICK_OVERFLOW;
-                if (op == SG_OP_BUSY) {
-                    busy_point(D, now, +1);
-                    emit(now, app, SG_EV_BUSY_START, d, 0);
-                    emit(t2, app, SG_EV_BUSY_END, d, 0);
-                }
+                const T t2 = TM::add(now, dur, status);
                 pc += 1;
-                s_pc[app] = (uint16_t)(pc | (op == SG_OP_BUSY ? kBusyFlag : 0u));
-                if constexpr (PROG) s_held[app] = held;
-                push(app, t2);
-                return;
+                if (op == SG_OP_BUSY) {
+                    busy_point(now, +1);
+                    emit(now, app, SG_EV_BUSY_START, 0);
+                    emit(t2, app, SG_EV_BUSY_END, 0);
+                    pc |= kBusyFlag;
+                }
+                nk = push_key(t2, app);
+                break;
             }
             if (op == SG_OP_ALLOC) {  // harness.py:521-536
-                emit(now, app, SG_EV_REQUEST, d, mib);
-                if (D.used + (int64_t)mib <= cap) {  // arrival bypass: fits => granted
-                    mem_point(D, now, (int64_t)mib);
-                    if constexpr (PROG) {
-                        if (held <= 0 && held + (int32_t)mib > 0) D.holders += 1;
-                        held += (int32_t)mib;
-                    } else {
-                        D.holders += 1;
-                    }
-                    D.maxh = max(D.maxh, (uint32_t)max(D.holders, 0));
-                    D.grants += 1;
+                emit(now, app, SG_EV_REQUEST, mib);
+                if ((int64_t)used + (int64_t)mib <= (int64_t)cap) {
+                    mem_point(now);
+                    used += mib;
+                    if (held <= 0 && held + (int32_t)mib > 0) holders += 1;
+                    held += (int32_t)mib;
+                    maxh = max(maxh, (uint32_t)max(holders, 0));
+                    grants += 1;
                     if (TM::is_never(s_grant[app])) s_grant[app] = now;
-                    emit(now, app, SG_EV_GRANT, d, mib);
-                    emit(now, app, SG_EV_ALLOC, d, mib);
+                    emit(now, app, SG_EV_GRANT, mib);
+                    emit(now, app, SG_EV_ALLOC, mib);
                     pc += 1;
                     continue;
                 }
-                s_q[qlen] = q_pack(app, min(mib, kSat), f.w & 0xFF, d);
+                s_q[qlen] = q_pack(app, min(mib, kSat), f.w & 0xFFu);
                 qlen += 1;
-                s_pc[app] = (uint16_t)pc;
-                if constexpr (PROG) s_held[app] = held;
-                return;
+                break;
             }
             // SG_OP_FREE: harness.py:537-542
-            mem_point(D, now, -(int64_t)mib);
-            if constexpr (PROG) {
-                if (held > 0 && held - (int32_t)mib <= 0) D.holders -= 1;
-                held -= (int32_t)mib;
-            } else {
-                D.holders -= 1;
-            }
+            mem_point(now);
+            used -= mib;
+            if (held > 0 && held - (int32_t)mib <= 0) holders -= 1;
+            held -= (int32_t)mib;
             pc += 1;
-            s_pc[app] = (uint16_t)pc;
-            if constexpr (PROG) s_held[app] = held;
-            emit(now, app, SG_EV_FREE, d, mib);
-            __syncwarp();
-            grant_waiters(d, now);
+            s_st[app] = (uint16_t)pc;
+            s_held[app] = held;
+            emit(now, app, SG_EV_FREE, mib);
+            grant_waiters_prog(now);
         }
+        s_st[app] = (uint16_t)pc;
+        s_held[app] = held;
+        TM::store(s_kt, s_kc, app, nk);
     }
 
-    // first step of app i is a cpu step (initial pop only pushes)?
-    __device__ __forceinline__ bool first_is_cpu(uint32_t i, uint64_t& dur) {
+    __device__ __forceinline__ void advance(uint32_t app, T now) {
+        if constexpr (PROG) advance_prog(app, now);
+        else advance_t0(app, now);
+    }
+
+    // first step of app i is cpu(dur)?  (the initial pop then only pushes)
+    __device__ __forceinline__ bool first_is_cpu(uint32_t i, uint64_t& dur) const {
         const uint4 f = s_app[i];
         if constexpr (PROG) {
             if (f.y == 0) return false;
@@ -468,60 +541,81 @@ struct TraceSim {
     }
 
     // ------------------------------------------------------------------ run
-    __device__ void run(uint32_t n_apps, uint32_t policy, sg_event* ev_slice) {
+    __device__ __forceinline__ void run(uint32_t n_apps, uint32_t policy, uint32_t cap_mib, sg_event* ev_slice) {
         n = n_apps;
+        cap = cap_mib;
         prio_pol = policy >= SG_POLICY_PFIFO;
         mmu = (policy & 1u) != 0;
-        qlen = 0;
         counter = n;  // initial pushes took counters 1..n (harness.py:560-562)
         status = 0;
+        qlen = 0;
+        qtail = 0;
+        qm_lane = 0;
+        last = mem_t = busy_prev = TM::zero();
+        I = 0;
+        B = 0;
+        used = 0;
+        busy_level = holders = 0;
+        maxh = grants = pops = 0;
         ev = ev_slice;
         ev_n = 0;
+        // Initial pops run in index order at t = 0 before anything else.  An
+        // app whose first step is cpu(d) only pushes (t = d, ++counter); when
+        // every app is like that all keys are assigned at once, otherwise runs
+        // of such apps are batched and the others advanced one by one.
+        bool all_simple = true;
 #pragma unroll
-        for (int j = 0; j < K; j++) { kt[j] = TM::INFK; kc[j] = 0xFFFFFFFFu; }
-#pragma unroll
-        for (int d = 0; d < (MULTI ? SG_MAX_DEV : 1); d++) {
-            ds[d].last = TM::zero();
-            ds[d].mem_t = TM::zero();
-            ds[d].busy_prev = TM::zero();
-            ds[d].I = 0;
-            ds[d].B = 0;
-            ds[d].used = 0;
-            ds[d].busy_level = 0;
-            ds[d].holders = 0;
-            ds[d].maxh = 0;
-            ds[d].grants = 0;
-            ds[d].pops = 0;
-        }
-        for (uint32_t i = lane; i < n; i += 32) {
-            s_pc[i] = 0;
-            s_grant[i] = TM::never();
-            s_end[i] = TM::never();
-            if constexpr (PROG) s_held[i] = 0;
-            if (ev != nullptr && i < P.ev_cap) {  // start events (harness.py:561)
-                sg_event e;
-                e.t = TM::bits(TM::zero());
-                e.app = (uint16_t)i;
-                e.kind = SG_EV_START;
-                e.dev = (uint8_t)dev_of(s_app[i].w);
-                e.mib = 0;
-                ev[i] = e;
+        for (int j = 0; j < K; j++) {
+            const uint32_t i = 32 * j + lane;
+            bool simple = true;
+            uint64_t dur = 0;
+            if (i < n) {
+                s_grant[i] = TM::never();
+                s_end[i] = TM::never();
+                if constexpr (PROG) s_held[i] = 0;
+                simple = first_is_cpu(i, dur);
+                if (simple) {
+                    const T t0 = TM::add(TM::zero(), dur, status);
+                    TM::store(s_kt, s_kc, i, TM::make_key(t0, n + i + 1, i));
+                } else {
+                    TM::store(s_kt, s_kc, i, TM::inf());
+                }
+                if constexpr (PROG) {
+                    s_st[i] = simple ? 1 : 0;
+                    if (ev != nullptr && i < P.ev_cap) {  // start events (harness.py:561)
+                        sg_event e;
+                        e.t = TM::bits(TM::zero());
+                        e.app = (uint16_t)i;
+                        e.kind = SG_EV_START;
+                        e.dev = 0;
+                        e.mib = 0;
+                        ev[i] = e;
+                    }
+                } else {
+                    s_st[i] = s_app[i].y ? kAllocPending : 0u;
+                }
+            } else {
+                TM::store(s_kt, s_kc, i, TM::inf());
             }
+            all_simple = all_simple && simple;
         }
-        if (ev != nullptr) ev_n = n;
+        status = __reduce_or_sync(FULL, status);
+        if constexpr (PROG) {
+            if (ev != nullptr) ev_n = n;
+        }
+        uint32_t next_init = n;
+        if (__all_sync(FULL, all_simple)) {
+            counter = 2 * n;
+            if (counter >= kCounterLimit) status |= SG_ST_COUNTER_OVERFLOW;
+        } else {
+            next_init = 0;
+        }
         __syncwarp();
 
-        uint32_t next_init = 0;
-        local_min();
         while (true) {
             uint32_t app;
             T now;
-            bool counted = true;
             if (next_init < n) {
-                // Initial pops run in index order at t = 0 before anything else
-                // (their counters 1..n precede every later push).  A run of apps
-                // whose first step is cpu only pushes (t = d, ++counter): do the
-                // whole run at once; any other app is advanced individually.
                 const uint32_t c = next_init >> 5;
                 const uint32_t i = (c << 5) + lane;
                 const bool valid = i < n && i >= next_init;
@@ -532,18 +626,17 @@ struct TraceSim {
                 const uint32_t nonsimple = vm & ~sm;
                 const uint32_t run = nonsimple ? (sm & ((1u << (__ffs(nonsimple) - 1)) - 1u)) : sm;
                 if (run) {
-                    const bool in = (run >> lane) & 1u;
-                    bool ovf = false;
-                    const T t2 = TM::add(TM::zero(), dur, ovf);
-                    if (__any_sync(FULL, in && ovf)) status |= SG_ST_TICK_OVERFLOW;
-                    const uint32_t cval = counter + __popc(run & lanemask_lt()) + 1;
-#pragma unroll
-                    for (int j = 0; j < K; j++)
-                        if (in && c == (uint32_t)j) { kt[j] = TM::key(t2); kc[j] = (cval << kAppBits) | i; }
-                    if (in) s_pc[i] = 1;
+                    // re-assign the pre-set keys with the live counter
+                    if ((run >> lane) & 1u) {
+                        const T t0 = TM::add(TM::zero(), dur, status);
+                        TM::store(s_kt, s_kc, i,
+                                  TM::make_key(t0, counter + __popc(run & lanemask_lt()) + 1, i));
+                    }
                     counter += __popc(run);
                     if (counter >= kCounterLimit) status |= SG_ST_COUNTER_OVERFLOW;
+                    status = __reduce_or_sync(FULL, status);
                 }
+                __syncwarp();
                 if (!nonsimple) {
                     next_init = min(n, (c + 1) << 5);
                     continue;
@@ -551,103 +644,92 @@ struct TraceSim {
                 app = (c << 5) + __ffs(nonsimple) - 1;
                 next_init = app + 1;
                 now = TM::zero();
-                counted = false;
-                __syncwarp();
+                pops -= 1;  // initial pops are counted once, in finish()
             } else {
-                local_min();
-                const Key kmin = TM::warp_min(lt);
-                if (kmin == TM::INFK) break;
-                const uint32_t cm = __reduce_min_sync(FULL, lt == kmin ? lc : 0xFFFFFFFFu);
-                app = cm & (SG_MAX_APPS - 1);
-                now = TM::time(kmin);
-                clear_key(app);
+                __syncwarp();
+                Key lm = TM::load(s_kt, s_kc, lane);
+#pragma unroll
+                for (int j = 1; j < K; j++) {
+                    const Key k = TM::load(s_kt, s_kc, 32 * j + lane);
+                    if (TM::less(k, lm)) lm = k;
+                }
+                if (!TM::argmin(lm, now, app)) break;
             }
-            __syncwarp();
-            advance(app, now, counted);
+            advance(app, now);
         }
     }
 
     // --------------------------------------------------------------- output
-    __device__ void finish(uint64_t rec_base, uint64_t app_out_base, uint32_t* ev_count_out) {
+    // rec: statistics record index; s_idx: sub-trace -> trace app index (or null)
+    __device__ __forceinline__ void finish(uint64_t rec, uint64_t app_out_base, const uint16_t* s_idx,
+                           uint32_t* ev_count_out) {
         __syncwarp();
-        const uint32_t nd = MULTI ? P.ndev : 1;
-        uint32_t napps[MULTI ? SG_MAX_DEV : 1];
-        uint32_t unf[MULTI ? SG_MAX_DEV : 1];
-#pragma unroll
-        for (int d = 0; d < (MULTI ? SG_MAX_DEV : 1); d++) { napps[d] = 0; unf[d] = 0; }
+        uint32_t unf = 0;
         for (uint32_t base = 0; base < n; base += 32) {
             const uint32_t i = base + lane;
             const bool valid = i < n;
-            T gv = TM::never(), evv = TM::never();
-            uint32_t dd = 0;
+            T evv = TM::never();
             if (valid) {
-                gv = s_grant[i];
+                const T gv = s_grant[i];
                 evv = s_end[i];
-                dd = dev_of(s_app[i].w);
-                if (P.grant) reinterpret_cast<T*>(P.grant)[app_out_base + i] = gv;
-                if (P.end) reinterpret_cast<T*>(P.end)[app_out_base + i] = evv;
+                const uint64_t o = app_out_base + (s_idx ? s_idx[i] : i);
+                if (P.grant) reinterpret_cast<T*>(P.grant)[o] = gv;
+                if (P.end) reinterpret_cast<T*>(P.end)[o] = evv;
             }
-#pragma unroll
-            for (int d = 0; d < (MULTI ? SG_MAX_DEV : 1); d++) {
-                napps[d] += __popc(__ballot_sync(FULL, valid && dd == (uint32_t)d));
-                unf[d] += __popc(__ballot_sync(FULL, valid && dd == (uint32_t)d && TM::is_never(evv)));
-            }
+            unf += __popc(__ballot_sync(FULL, valid && TM::is_never(evv)));
         }
         if (ev_count_out != nullptr && lane == 0) *ev_count_out = ev_n;
-        const double scale = ldexp(1.0, -P.tick_log2);
-#pragma unroll
-        for (int d = 0; d < (MULTI ? SG_MAX_DEV : 1); d++) {
-            if ((uint32_t)d >= nd) break;
-            if (lane != (uint32_t)d) continue;
-            DS& D = ds[d];
+        if (lane == 0) {
+            const double scale = ldexp(1.0, -P.tick_log2);
+            const double cap_bytes = (double)cap * kMiB;
+            const int64_t u = (int64_t)used;
             uint32_t st = status;
             double mem_pct, dev_pct;
-            const double cap_bytes = (double)P.cap[d] * kMiB;
             if constexpr (TM::F64) {
-                // makespan_s = max(t_end - t0, 1e-9), final integral term (harness.py:378, 425)
-                const double span = D.last >= 1e-9 ? D.last : 1e-9;
-                D.I = __dadd_rn(D.I, __dmul_rn(__ll2double_rn(D.used * 1048576LL), __dsub_rn(span, D.mem_t)));
-                mem_pct = __ddiv_rn(__dmul_rn(100.0, D.I), __dmul_rn(cap_bytes, span));
-                dev_pct = __ddiv_rn(__dmul_rn(100.0, D.B), span);
+                // makespan_s = max(t_end - t0, 1e-9); final integral term (harness.py:378, 425)
+                const double span = last >= 1e-9 ? last : 1e-9;
+                I = __dadd_rn(I, __dmul_rn(__ll2double_rn(u * 1048576LL), __dsub_rn(span, mem_t)));
+                mem_pct = __ddiv_rn(__dmul_rn(100.0, I), __dmul_rn(cap_bytes, span));
+                dev_pct = __ddiv_rn(__dmul_rn(100.0, B), span);
                 sg_trace_stats_f64 r;
-                r.makespan_s = D.last;
-                r.mem_integral = D.I;
-                r.busy_s = D.B;
-                r.grants = D.grants;
-                r.pops = D.pops + napps[d];
-                r.max_holders = (uint16_t)D.maxh;
-                r.unfinished = (uint16_t)unf[d];
+                r.makespan_s = last;
+                r.mem_integral = I;
+                r.busy_s = B;
+                r.grants = grants;
+                r.pops = pops + n;
+                r.max_holders = (uint16_t)maxh;
+                r.unfinished = (uint16_t)unf;
                 r.status = st;
-                reinterpret_cast<sg_trace_stats_f64*>(P.stats)[rec_base + d] = r;
+                reinterpret_cast<sg_trace_stats_f64*>(P.stats)[rec] = r;
             } else {
-                uint64_t I = D.I;
+                uint64_t Iv = I;
                 double integral;
-                if (D.last == 0 && D.used != 0) {
+                if (last == 0 && u != 0) {
                     // span = 1e-9 s is not on the tick grid: report the level
                     st |= SG_ST_ZERO_SPAN_LEVEL;
-                    I = (uint64_t)D.used;
-                    integral = __dmul_rn(__ll2double_rn(D.used * 1048576LL), 1e-9);
+                    Iv = (uint64_t)u;
+                    integral = __dmul_rn(__ll2double_rn(u * 1048576LL), 1e-9);
                 } else {
-                    I += (uint64_t)(D.used * (int64_t)(D.last - D.mem_t));
-                    integral = __dmul_rn((double)I, kMiB * scale);
+                    Iv += (uint64_t)(u * (int64_t)(last - mem_t));
+                    integral = __dmul_rn((double)Iv, kMiB * scale);
                 }
-                const double span = D.last > 0 ? __dmul_rn((double)D.last, scale) : 1e-9;
+                const double span = last > 0 ? __dmul_rn((double)last, scale) : 1e-9;
                 mem_pct = __ddiv_rn(__dmul_rn(100.0, integral), __dmul_rn(cap_bytes, span));
-                dev_pct = __ddiv_rn(__dmul_rn(100.0, __dmul_rn((double)D.B, scale)), span);
+                dev_pct = __ddiv_rn(__dmul_rn(100.0, __dmul_rn((double)B, scale)), span);
                 sg_trace_stats r;
-                r.makespan = D.last;
-                r.busy = (uint32_t)D.B;
-                r.mem_integral = I;
-                r.grants = D.grants;
-                r.pops = D.pops + napps[d];
-                r.max_holders = (uint16_t)D.maxh;
-                r.unfinished = (uint16_t)unf[d];
+                r.makespan = last;
+                r.busy = (uint32_t)B;
+                r.mem_integral = Iv;
+                r.grants = grants;
+                r.pops = pops + n;
+                r.max_holders = (uint16_t)maxh;
+                r.unfinished = (uint16_t)unf;
                 r.status = st;
-                reinterpret_cast<sg_trace_stats*>(P.stats)[rec_base + d] = r;
+                reinterpret_cast<sg_trace_stats*>(P.stats)[rec] = r;
             }
-            if (napps[d] == 0) { mem_pct = 0.0; dev_pct = 0.0; }  // empty event list (harness.py:374-375)
-            if (P.mem_pct) P.mem_pct[rec_base + d] = mem_pct;
-            if (P.dev_pct) P.dev_pct[rec_base + d] = dev_pct;
+            if (n == 0) { mem_pct = 0.0; dev_pct = 0.0; }  // empty event list (harness.py:374-375)
+            if (P.mem_pct) P.mem_pct[rec] = mem_pct;
+            if (P.dev_pct) P.dev_pct[rec] = dev_pct;
         }
         __syncwarp();
     }
@@ -655,19 +737,23 @@ struct TraceSim {
 
 // ------------------------------------------------------------------ kernel
 
-template <class TM, int K, bool PROG, bool MULTI>
-__global__ void __launch_bounds__(kSimWarpsPerBlock * 32)
+#ifndef SG_SIM_MIN_BLOCKS
+#define SG_SIM_MIN_BLOCKS 1
+#endif
+
+template <class TM, int K, bool PROG>
+__global__ void __launch_bounds__(kSimWarpsPerBlock * 32, SG_SIM_MIN_BLOCKS)
 trace_sim_kernel(const SimParams P) {
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
+    const uint32_t wpb = blockDim.x >> 5;
     uint8_t* ws = smem + (size_t)warp * P.warp_bytes;
-    uint4* app_buf[2] = {reinterpret_cast<uint4*>(ws + P.off_app),
-                         reinterpret_cast<uint4*>(ws + P.off_app + (size_t)P.n_pad * 16)};
     uint64_t* bar = reinterpret_cast<uint64_t*>(ws + P.off_bar);
+    const uint32_t buf_bytes = P.n_pad * 16u;
 
-    const uint64_t gw = (uint64_t)blockIdx.x * kSimWarpsPerBlock + warp;
-    const uint64_t stride = (uint64_t)gridDim.x * kSimWarpsPerBlock;
+    const uint64_t gw = (uint64_t)blockIdx.x * wpb + warp;
+    const uint64_t stride = (uint64_t)gridDim.x * wpb;
 
     auto trace_range = [&](uint64_t t, uint64_t& a0, uint32_t& na) {
         if (P.trace_offsets) {
@@ -680,14 +766,14 @@ trace_sim_kernel(const SimParams P) {
         }
     };
     // T0 mode: stage the trace's 16 B/app records with the bulk-copy engine.
-    auto stage = [&](uint64_t t, int b) {
+    auto stage = [&](uint64_t t, uint32_t b) {
         uint64_t a0;
         uint32_t na;
         trace_range(t, a0, na);
         if (lane == 0) {
             fence_proxy_async_smem();
             mbar_arrive_expect_tx(&bar[b], na * 16u);
-            if (na) bulk_g2s(app_buf[b], P.apps + a0, na * 16u, &bar[b]);
+            if (na) bulk_g2s(ws + P.off_app + b * buf_bytes, P.apps + a0, na * 16u, &bar[b]);
         }
     };
 
@@ -706,27 +792,66 @@ trace_sim_kernel(const SimParams P) {
         uint64_t a0;
         uint32_t na;
         trace_range(t, a0, na);
-        const int b = PROG ? 0 : (int)(iter & 1u);
+        const uint32_t b = PROG ? 0u : (iter & 1u);
         if constexpr (!PROG) {
             mbar_wait(&bar[b], (iter >> 1) & 1u);
             __syncwarp();
-            if (t + stride < P.n_traces) stage(t + stride, b ^ 1);
+            if (t + stride < P.n_traces) stage(t + stride, b ^ 1u);
         } else {
+            uint4* dst = reinterpret_cast<uint4*>(ws + P.off_app);
             const uint32_t s0 = P.step_offsets[0];
             for (uint32_t i = lane; i < na; i += 32) {
                 const uint32_t sb = P.step_offsets[a0 + i] - s0;
                 const uint32_t se = P.step_offsets[a0 + i + 1] - s0;
-                app_buf[0][i] = make_uint4(sb, se - sb, 0u, P.apps[a0 + i].attr);
+                dst[i] = make_uint4(sb, se - sb, 0u, P.apps[a0 + i].attr);
             }
             __syncwarp();
         }
-        for (uint32_t p = 0; p < P.npol; p++) {
-            TraceSim<TM, K, PROG, MULTI> sim(P, lane, ws, app_buf[b]);
-            const uint64_t slot = (uint64_t)p * P.n_traces + t;
-            sg_event* evs = P.events ? P.events + slot * P.ev_cap : nullptr;
-            sim.run(na, P.policies[p], evs);
-            sim.finish(slot * P.ndev, (uint64_t)p * P.n_apps_total + a0,
-                       P.event_counts ? P.event_counts + slot : nullptr);
+        const uint4* apps_smem = reinterpret_cast<const uint4*>(ws + P.off_app + b * buf_bytes);
+        for (uint32_t d = 0; d < P.ndev; d++) {
+            // (no dynamic indexing into the kernel parameters: it would force a
+            // local-memory copy of SimParams)
+            uint32_t cap_d = P.cap[0];
+#pragma unroll
+            for (uint32_t j = 1; j < SG_MAX_DEV; j++)
+                if (d == j) cap_d = P.cap[j];
+            // device d's sub-trace (all apps when ndev == 1), in index order
+            const uint4* sub = apps_smem;
+            const uint16_t* idx = nullptr;
+            uint32_t nd = na;
+            if (P.ndev > 1) {
+                uint4* s_sub = reinterpret_cast<uint4*>(ws + P.off_sub);
+                uint16_t* s_idx = reinterpret_cast<uint16_t*>(ws + P.off_idx);
+                nd = 0;
+                for (uint32_t base = 0; base < na; base += 32) {
+                    const uint32_t i = base + lane;
+                    uint4 f = make_uint4(0, 0, 0, 0);
+                    uint32_t dv = ~0u;
+                    if (i < na) {
+                        f = apps_smem[i];
+                        dv = (f.w >> 8) & 0xFFu;
+                        if (dv >= P.ndev) dv = 0;
+                    }
+                    const uint32_t m = __ballot_sync(FULL, dv == d);
+                    if (dv == d) {
+                        const uint32_t pos = nd + __popc(m & lanemask_lt());
+                        s_sub[pos] = f;
+                        s_idx[pos] = (uint16_t)i;
+                    }
+                    nd += __popc(m);
+                }
+                __syncwarp();
+                sub = s_sub;
+                idx = s_idx;
+            }
+            for (uint32_t p = 0; p < P.npol; p++) {
+                TraceSim<TM, K, PROG> sim(P, lane, ws, sub);
+                const uint64_t slot = (uint64_t)p * P.n_traces + t;
+                sg_event* evs = P.events ? P.events + slot * P.ev_cap : nullptr;
+                sim.run(nd, (P.policy_list >> (4 * p)) & 0xFu, cap_d, evs);
+                sim.finish(slot * P.ndev + d, (uint64_t)p * P.n_apps_total + a0, idx,
+                           P.event_counts ? P.event_counts + slot : nullptr);
+            }
         }
         __syncwarp();
     }
@@ -739,16 +864,25 @@ static inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 void sim_layout(SimParams& p, bool program_mode, bool f64) {
     const uint32_t N = p.n_pad;
     const uint32_t tsz = f64 ? 8u : 4u;
+    const bool multi = p.ndev > 1;
     uint32_t o = 0;
     p.off_app = o;
     o = align16(o + N * 16u * (program_mode ? 1u : 2u));
+    p.off_sub = o;
+    o = align16(o + (multi ? N * 16u : 0u));
+    p.off_idx = o;
+    o = align16(o + (multi ? N * 2u : 0u));
+    p.off_key = o;
+    o = align16(o + N * 8u);
+    p.off_kc = o;
+    o = align16(o + (f64 ? N * 4u : 0u));
     p.off_q = o;
     o = align16(o + N * 8u);
     p.off_grant = o;
     o = align16(o + N * tsz);
     p.off_end = o;
     o = align16(o + N * tsz);
-    p.off_pc = o;
+    p.off_st = o;
     o = align16(o + N * 2u);
     p.off_held = o;
     o = align16(o + (program_mode ? N * 4u : 0u));
@@ -757,49 +891,52 @@ void sim_layout(SimParams& p, bool program_mode, bool f64) {
     p.warp_bytes = o;
 }
 
-template <class TM, int K, bool PROG, bool MULTI>
+template <class TM, int K, bool PROG>
 static cudaError_t launch_t(const SimParams& p, cudaStream_t stream, int* grid_out) {
-    auto kern = trace_sim_kernel<TM, K, PROG, MULTI>;
-    const size_t smem = (size_t)p.warp_bytes * kSimWarpsPerBlock;
+    auto kern = trace_sim_kernel<TM, K, PROG>;
+    // warps per block: as many as fit (<= kSimWarpsPerBlock) in 227 KB
+    uint32_t wpb = kSimWarpsPerBlock;
+    while (wpb > 1 && (size_t)p.warp_bytes * wpb > 227u * 1024u) wpb--;
+    const size_t smem = (size_t)p.warp_bytes * wpb;
+    if (smem > 227u * 1024u) return cudaErrorInvalidConfiguration;
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSimWarpsPerBlock * 32, smem);
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, smem);
     if (err != cudaSuccess) return err;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    const uint64_t need = (p.n_traces + kSimWarpsPerBlock - 1) / kSimWarpsPerBlock;
+    const uint64_t need = (p.n_traces + wpb - 1) / wpb;
     uint64_t grid = (uint64_t)sms * per_sm;
     if (need < grid) grid = need;
     if (grid == 0) grid = 1;
     if (grid_out) *grid_out = (int)grid;
-    kern<<<(unsigned)grid, kSimWarpsPerBlock * 32, smem, stream>>>(p);
+    kern<<<(unsigned)grid, wpb * 32, smem, stream>>>(p);
     return cudaGetLastError();
 }
 
-template <class TM, bool PROG, bool MULTI>
+template <class TM, bool PROG>
 static cudaError_t launch_k(const SimParams& p, cudaStream_t s, int* g) {
-    const uint32_t k = p.n_pad / 32;
-    if (k <= 1) return launch_t<TM, 1, PROG, MULTI>(p, s, g);
-    if (k <= 2) return launch_t<TM, 2, PROG, MULTI>(p, s, g);
-    if (k <= 4) return launch_t<TM, 4, PROG, MULTI>(p, s, g);
-    if (k <= 8) return launch_t<TM, 8, PROG, MULTI>(p, s, g);
-    return launch_t<TM, 32, PROG, MULTI>(p, s, g);
+    switch (p.n_pad / 32) {
+        case 1: return launch_t<TM, 1, PROG>(p, s, g);
+        case 2: return launch_t<TM, 2, PROG>(p, s, g);
+        case 4: return launch_t<TM, 4, PROG>(p, s, g);
+        case 8: return launch_t<TM, 8, PROG>(p, s, g);
+        case 16: return launch_t<TM, 16, PROG>(p, s, g);
+        case 32: return launch_t<TM, 32, PROG>(p, s, g);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
-cudaError_t launch_sim(const SimParams& p, bool program_mode, bool f64, bool multi,
-                       cudaStream_t stream, int* grid_out) {
+cudaError_t launch_sim(const SimParams& p, bool program_mode, bool f64, cudaStream_t stream,
+                       int* grid_out) {
     if (f64) {
         if (!program_mode) return cudaErrorInvalidValue;
-        return multi ? launch_k<F64TM, true, true>(p, stream, grid_out)
-                     : launch_k<F64TM, true, false>(p, stream, grid_out);
+        return launch_k<F64TM, true>(p, stream, grid_out);
     }
-    if (program_mode)
-        return multi ? launch_k<TickTM, true, true>(p, stream, grid_out)
-                     : launch_k<TickTM, true, false>(p, stream, grid_out);
-    return multi ? launch_k<TickTM, false, true>(p, stream, grid_out)
-                 : launch_k<TickTM, false, false>(p, stream, grid_out);
+    if (program_mode) return launch_k<TickTM, true>(p, stream, grid_out);
+    return launch_k<TickTM, false>(p, stream, grid_out);
 }
 
 }  // namespace sg
