@@ -155,6 +155,7 @@ struct TraceSim {
     uint32_t counter, status;
     uint32_t qlen;            // PROG: compacted queue length; T0: waiting entries
     uint32_t qtail;           // T0: next queue position (apps enqueue at most once)
+    uint32_t qhead;           // T0 FIFO: first waiting position
     uint32_t qm_lane;         // T0: lane j holds the presence bits of queue positions 32j..32j+31
     // statistics (harness.py:373-461 integer forms)
     T last, mem_t, busy_prev;
@@ -218,9 +219,10 @@ struct TraceSim {
     // Busy point in time order: the sweep of harness.py:429-437.  Points of
     // equal time add zero, so pop order within a tick is immaterial.
     __device__ __forceinline__ void busy_point(T now, int32_t delta) {
-        if (busy_level > 0) {
-            if constexpr (TM::F64) B = __dadd_rn(B, __dsub_rn(now, busy_prev));
-            else B += (uint32_t)(now - busy_prev);
+        if constexpr (TM::F64) {
+            if (busy_level > 0) B = __dadd_rn(B, __dsub_rn(now, busy_prev));
+        } else {
+            B += busy_level > 0 ? (uint32_t)(now - busy_prev) : 0u;
         }
         busy_prev = now;
         busy_level += delta;
@@ -230,6 +232,34 @@ struct TraceSim {
     // harness.py:545-558 + policy.py:52-74 over the position-stable queue.
     __device__ __forceinline__ void grant_waiters_t0(T now) {
         if (qlen == 0) return;
+        if (!mmu && !prio_pol) {
+            // FIFO removes only from the head: the queue is the contiguous
+            // position range [qhead, qtail); grant while the head fits.
+            const uint32_t budget0 = cap - used;
+            uint32_t budget = budget0, g = 0;
+            while (qhead < qtail) {
+                const uint64_t e = s_q[qhead];
+                const uint32_t mib = (uint32_t)e;
+                if (mib > budget) break;
+                const uint32_t a = q_app(e);
+                budget -= mib;
+                g += 1;
+                TM::store(s_kt, s_kc, a, TM::make_key(now, counter + g, a));
+                s_grant[a] = now;
+                s_st[a] = 0;
+                qhead += 1;
+            }
+            if (g) {
+                mem_point(now);
+                used += budget0 - budget;
+                holders += (int32_t)g;
+                maxh = max(maxh, (uint32_t)holders);
+                grants += g;
+                counter += g;
+                qlen -= g;
+            }
+            return;
+        }
         while (true) {
             uint32_t budget = cap - used;
             const uint32_t budget0 = budget;
@@ -299,7 +329,6 @@ struct TraceSim {
                 maxh = max(maxh, (uint32_t)holders);
                 grants += granted;
                 qlen -= granted;
-                if (counter >= kCounterLimit) status |= SG_ST_COUNTER_OVERFLOW;
             }
             // FIFO/MMU: a second round is provably empty; priority policies
             // drain the top class and may serve the next one (harness.py:547-550)
@@ -411,7 +440,6 @@ struct TraceSim {
         const uint32_t st = s_st[app];
         __syncwarp();
         last = now;
-        pops += 1;
         Key nk = TM::inf();
         if (st & kBusyFlag) {
             busy_point(now, -1);
@@ -434,8 +462,11 @@ struct TraceSim {
                 }
             }
             if (f.z) {  // busy (harness.py:514-520)
+                // no overflow checks: run() verified max arrival + sum(busy) < 2^32 - 1
+                // ticks (a bound on every event time) and counters stay < 4n
                 busy_point(now, +1);
-                nk = push_key(TM::add(now, f.z, status), app);
+                counter += 1;
+                nk = TM::make_key(now + f.z, counter, app);
                 s_st[app] = kBusyFlag;
                 TM::store(s_kt, s_kc, app, nk);
                 return;
@@ -448,7 +479,6 @@ struct TraceSim {
             grant_waiters_t0(now);
         }
         s_end[app] = now;  // harness.py:543
-        s_st[app] = 0;
         TM::store(s_kt, s_kc, app, nk);
     }
 
@@ -459,7 +489,6 @@ struct TraceSim {
         int32_t held = s_held[app];
         __syncwarp();
         last = now;
-        pops += 1;
         if (pc & kBusyFlag) {
             busy_point(now, -1);
             pc &= ~kBusyFlag;
@@ -550,6 +579,7 @@ struct TraceSim {
         status = 0;
         qlen = 0;
         qtail = 0;
+        qhead = 0;
         qm_lane = 0;
         last = mem_t = busy_prev = TM::zero();
         I = 0;
@@ -564,12 +594,14 @@ struct TraceSim {
         // every app is like that all keys are assigned at once, otherwise runs
         // of such apps are batched and the others advanced one by one.
         bool all_simple = true;
+        bool big = false;  // T0: an app whose fields could push times past 2^32 - 1
 #pragma unroll
         for (int j = 0; j < K; j++) {
             const uint32_t i = 32 * j + lane;
             bool simple = true;
             uint64_t dur = 0;
             if (i < n) {
+                if constexpr (!PROG) big = big || s_app[i].x >= (1u << 31) || s_app[i].z >= (1u << 21);
                 s_grant[i] = TM::never();
                 s_end[i] = TM::never();
                 if constexpr (PROG) s_held[i] = 0;
@@ -600,6 +632,24 @@ struct TraceSim {
             all_simple = all_simple && simple;
         }
         status = __reduce_or_sync(FULL, status);
+        if constexpr (!PROG) {
+            // every event time is <= max arrival + sum(busy) (after the last
+            // arrival the clock only advances while some app is busy); with
+            // arrival < 2^31 and busy < 2^21 (n <= 1024) it fits in 32 bits
+            if (__any_sync(FULL, big)) {
+                uint64_t bsum = 0, amax = 0;
+                for (uint32_t i = lane; i < n; i += 32) {
+                    bsum += s_app[i].z;
+                    amax = max(amax, (uint64_t)s_app[i].x);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    bsum += __shfl_xor_sync(FULL, bsum, o);
+                    amax = max(amax, __shfl_xor_sync(FULL, amax, o));
+                }
+                if (amax + bsum > 0xFFFFFFFEull) status |= SG_ST_TICK_OVERFLOW;
+            }
+        }
         if constexpr (PROG) {
             if (ev != nullptr) ev_n = n;
         }
@@ -643,8 +693,7 @@ struct TraceSim {
                 }
                 app = (c << 5) + __ffs(nonsimple) - 1;
                 next_init = app + 1;
-                now = TM::zero();
-                pops -= 1;  // initial pops are counted once, in finish()
+                now = TM::zero();  // (initial pops are counted in finish())
             } else {
                 __syncwarp();
                 Key lm = TM::load(s_kt, s_kc, lane);
@@ -654,6 +703,7 @@ struct TraceSim {
                     if (TM::less(k, lm)) lm = k;
                 }
                 if (!TM::argmin(lm, now, app)) break;
+                pops += 1;
             }
             advance(app, now);
         }
@@ -737,13 +787,16 @@ struct TraceSim {
 
 // ------------------------------------------------------------------ kernel
 
-#ifndef SG_SIM_MIN_BLOCKS
-#define SG_SIM_MIN_BLOCKS 1
+// SG_SIM_MIN_BLOCKS (build-time A/B knob): minimum resident blocks per SM
+// requested from ptxas, i.e. a register cap of 64K / (128 * min_blocks).
+#ifdef SG_SIM_MIN_BLOCKS
+#define SG_SIM_BOUNDS __launch_bounds__(kSimWarpsPerBlock * 32, SG_SIM_MIN_BLOCKS)
+#else
+#define SG_SIM_BOUNDS __launch_bounds__(kSimWarpsPerBlock * 32)
 #endif
 
 template <class TM, int K, bool PROG>
-__global__ void __launch_bounds__(kSimWarpsPerBlock * 32, SG_SIM_MIN_BLOCKS)
-trace_sim_kernel(const SimParams P) {
+__global__ void SG_SIM_BOUNDS trace_sim_kernel(const SimParams P) {
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
