@@ -2,6 +2,7 @@
 // argument validation, kernel dispatch, and the host-buffer pipeline.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -118,8 +119,21 @@ static int simulate_device(const sg_batch* in, const sg_out* out, cudaStream_t s
     sg::sim_layout(p, s.program, s.f64);
     if (p.warp_bytes > 227u * 1024u)
         return fail(E_RANGE, "shared memory per warp exceeds 227 KB (n_pad=%u)", s.n_pad);
-    cudaError_t e = sg::launch_sim(p, s.program, s.f64, stream, nullptr);
-    if (e != cudaSuccess) return cuda_fail(e, "trace_sim launch");
+    // K1 engine: the lane kernel (v4) where eligible, else the warp kernel
+    // (v3).  SGPU_K1=warp|lane overrides (A/B runs and parity tests).
+    const char* eng = getenv("SGPU_K1");
+    const bool want_warp = eng && strcmp(eng, "warp") == 0;
+    const bool want_lane = eng && strcmp(eng, "lane") == 0;
+    const bool lane_ok = sg::lane_eligible(p, s.program, s.f64);
+    if (want_lane && !lane_ok) return fail(E_ARG, "SGPU_K1=lane: batch not eligible for the lane kernel");
+    cudaError_t e;
+    if (lane_ok && !want_warp) {
+        e = sg::launch_sim_lane(p, stream, nullptr);
+        if (e != cudaSuccess) return cuda_fail(e, "trace_sim_lane launch");
+    } else {
+        e = sg::launch_sim(p, s.program, s.f64, stream, nullptr);
+        if (e != cudaSuccess) return cuda_fail(e, "trace_sim launch");
+    }
     return 0;
 }
 

@@ -44,6 +44,11 @@ void sim_layout(SimParams& p, bool program_mode, bool f64);
 cudaError_t launch_sim(const SimParams& p, bool program_mode, bool f64, cudaStream_t stream,
                        int* grid_out);
 
+// K1 v4: lane-per-(trace, device, policy) kernel for T0 tick-mode batches
+// (sgpu_lane.cu), with an in-kernel exact fallback to TraceSim.
+bool lane_eligible(const SimParams& p, bool program_mode, bool f64);
+cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_out);
+
 cudaError_t launch_reduce(const sg_trace_stats* stats, uint64_t count, sg_aggr* out,
                           cudaStream_t stream);
 cudaError_t launch_generate(const sg_gen_params& p, uint64_t trace_begin, uint64_t n_traces,

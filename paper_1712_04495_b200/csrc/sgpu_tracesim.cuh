@@ -1,0 +1,809 @@
+// sgpu_tracesim.cuh — the warp-per-trace simulator (K1 v3 core): time models,
+// TraceSim (one warp simulates one (sub-)trace under one policy).  Shared by
+// trace_sim_kernel (sgpu_sim.cu) and the lane kernel's exact fallback path
+// (sgpu_lane.cu).  Semantics: see the header of sgpu_sim.cu.
+#pragma once
+
+#include <cmath>
+#include <type_traits>
+
+#include "sgpu_common.cuh"
+#include "sgpu_internal.h"
+
+namespace sg {
+
+constexpr uint32_t kBusyFlag = 0x8000u;   // s_st bit: the pending pop ends a busy step
+constexpr uint32_t kAllocPending = 0x2u;  // s_st bit (T0): the alloc step has not run
+constexpr uint32_t kSat = 0x7FFFFFFFu;    // MiB saturation for FIFO prefix sums
+constexpr uint32_t kAppBits = 10;         // SG_MAX_APPS == 1 << kAppBits
+constexpr uint32_t kAppMask = (1u << kAppBits) - 1;
+constexpr uint32_t kCounterLimit = 1u << (32 - kAppBits);
+constexpr double kMiB = 1048576.0;
+
+// ------------------------------------------------------------ time models
+
+// Integer ticks.  Heap key = t << 32 | counter << 10 | app (one u64).
+struct TickTM {
+    using T = uint32_t;
+    using Acc = uint64_t;
+    using Key = uint64_t;
+    static constexpr bool F64 = false;
+    static __device__ __forceinline__ Key inf() { return ~0ull; }
+    static __device__ __forceinline__ Key make_key(T t, uint32_t c, uint32_t app) {
+        return ((uint64_t)t << 32) | (c << kAppBits) | app;
+    }
+    static __device__ __forceinline__ bool less(Key a, Key b) { return a < b; }
+    static __device__ __forceinline__ Key load(const uint64_t* kt, const uint32_t*, uint32_t i) {
+        return kt[i];
+    }
+    static __device__ __forceinline__ void store(uint64_t* kt, uint32_t*, uint32_t i, Key k) {
+        kt[i] = k;
+    }
+    // heapq order: min time, then min counter; false when the heap is empty
+    static __device__ __forceinline__ bool argmin(Key lk, T& now, uint32_t& app) {
+        const uint32_t hi = __reduce_min_sync(FULL, (uint32_t)(lk >> 32));
+        const uint32_t lo = __reduce_min_sync(FULL, (uint32_t)(lk >> 32) == hi ? (uint32_t)lk : ~0u);
+        now = hi;
+        app = lo & kAppMask;
+        return hi != ~0u;
+    }
+    static __device__ __forceinline__ T zero() { return 0u; }
+    static __device__ __forceinline__ T never() { return SG_NEVER; }
+    static __device__ __forceinline__ bool is_never(T t) { return t == SG_NEVER; }
+    static __device__ __forceinline__ T add(T now, uint64_t dur, uint32_t& status) {
+        const uint64_t s = (uint64_t)now + dur;
+        if (s > 0xFFFFFFFEull) { status |= SG_ST_TICK_OVERFLOW; return 0xFFFFFFFEu; }
+        return (T)s;
+    }
+    static __device__ __forceinline__ uint64_t bits(T t) { return t; }
+};
+
+// float64 seconds (reference arithmetic).  Heap key = (t bits, counter/app).
+struct F64TM {
+    using T = double;
+    using Acc = double;
+    struct Key {
+        uint64_t t;
+        uint32_t c;
+    };
+    static constexpr bool F64 = true;
+    static __device__ __forceinline__ Key inf() { return Key{~0ull, ~0u}; }
+    // event times are non-negative doubles: their bit patterns order like values
+    static __device__ __forceinline__ Key make_key(T t, uint32_t c, uint32_t app) {
+        return Key{(uint64_t)__double_as_longlong(t), (c << kAppBits) | app};
+    }
+    static __device__ __forceinline__ bool less(Key a, Key b) {
+        return a.t < b.t || (a.t == b.t && a.c < b.c);
+    }
+    static __device__ __forceinline__ Key load(const uint64_t* kt, const uint32_t* kc, uint32_t i) {
+        return Key{kt[i], kc[i]};
+    }
+    static __device__ __forceinline__ void store(uint64_t* kt, uint32_t* kc, uint32_t i, Key k) {
+        kt[i] = k.t;
+        kc[i] = k.c;
+    }
+    static __device__ __forceinline__ bool argmin(Key lk, T& now, uint32_t& app) {
+        const uint64_t t = warp_min_u64(lk.t);
+        const uint32_t c = __reduce_min_sync(FULL, lk.t == t ? lk.c : ~0u);
+        now = __longlong_as_double((long long)t);
+        app = c & kAppMask;
+        return t != ~0ull;
+    }
+    static __device__ __forceinline__ T zero() { return 0.0; }
+    static __device__ __forceinline__ T never() { return __longlong_as_double(-1LL); }  // NaN
+    static __device__ __forceinline__ bool is_never(T t) { return isnan(t); }
+    static __device__ __forceinline__ T add(T now, uint64_t dur, uint32_t&) {
+        return __dadd_rn(now, __longlong_as_double((long long)dur));  // harness.py:517,519
+    }
+    static __device__ __forceinline__ uint64_t bits(T t) { return (uint64_t)__double_as_longlong(t); }
+};
+
+__device__ __forceinline__ uint32_t q_app(uint64_t e) { return (uint32_t)(e >> 32) & 0xFFFFu; }
+__device__ __forceinline__ uint32_t q_prio(uint64_t e) { return (uint32_t)(e >> 48) & 0xFFu; }
+__device__ __forceinline__ uint64_t q_pack(uint32_t app, uint32_t mib, uint32_t prio) {
+    return ((uint64_t)(prio & 0xFF) << 48) | ((uint64_t)app << 32) | mib;
+}
+
+// Tick-mode statistics record + utilisation percentages of one (policy,
+// trace, device).  The percentages follow the reference's float operation
+// order (harness.py:376-378, 414-437): integral = I * MiB * 2^-tick_log2,
+// span = max(T * 2^-tick_log2, 1e-9), mem% = (100 * integral) / (cap_bytes *
+// span), dev% = (100 * B * 2^-tick_log2) / span; an empty event list reports
+// 0 / 0 (harness.py:374-375).  Shared by both K1 kernels so their records are
+// identical by construction.
+__device__ __forceinline__ void store_tick_record(const SimParams& P, uint64_t rec, uint32_t n,
+                                                  uint32_t cap, uint32_t last, uint32_t mem_t,
+                                                  uint64_t I, uint32_t B, int64_t u, uint32_t grants,
+                                                  uint32_t pops, uint32_t maxh, uint32_t unf,
+                                                  uint32_t st) {
+    const double scale = ldexp(1.0, -P.tick_log2);
+    const double cap_bytes = (double)cap * kMiB;
+    uint64_t Iv = I;
+    double integral;
+    if (last == 0 && u != 0) {
+        // span = 1e-9 s is not on the tick grid: report the level
+        st |= SG_ST_ZERO_SPAN_LEVEL;
+        Iv = (uint64_t)u;
+        integral = __dmul_rn(__ll2double_rn(u * 1048576LL), 1e-9);
+    } else {
+        Iv += (uint64_t)(u * (int64_t)(last - mem_t));
+        integral = __dmul_rn((double)Iv, kMiB * scale);
+    }
+    const double span = last > 0 ? __dmul_rn((double)last, scale) : 1e-9;
+    double mem_pct = __ddiv_rn(__dmul_rn(100.0, integral), __dmul_rn(cap_bytes, span));
+    double dev_pct = __ddiv_rn(__dmul_rn(100.0, __dmul_rn((double)B, scale)), span);
+    sg_trace_stats r;
+    r.makespan = last;
+    r.busy = B;
+    r.mem_integral = Iv;
+    r.grants = grants;
+    r.pops = pops;
+    r.max_holders = (uint16_t)maxh;
+    r.unfinished = (uint16_t)unf;
+    r.status = st;
+    reinterpret_cast<sg_trace_stats*>(P.stats)[rec] = r;
+    if (n == 0) { mem_pct = 0.0; dev_pct = 0.0; }
+    if (P.mem_pct) P.mem_pct[rec] = mem_pct;
+    if (P.dev_pct) P.dev_pct[rec] = dev_pct;
+}
+
+// Device d's sub-trace (apps whose device field is d; out-of-range devices
+// count as device 0), in index order, with its trace app indices.  Returns
+// its length.  Warp-collective.
+__device__ __forceinline__ uint32_t build_subtrace(const uint4* apps, uint32_t na, uint32_t d,
+                                                   uint32_t ndev, uint4* s_sub, uint16_t* s_idx,
+                                                   uint32_t lane) {
+    uint32_t nd = 0;
+    for (uint32_t base = 0; base < na; base += 32) {
+        const uint32_t i = base + lane;
+        uint4 f = make_uint4(0, 0, 0, 0);
+        uint32_t dv = ~0u;
+        if (i < na) {
+            f = apps[i];
+            dv = (f.w >> 8) & 0xFFu;
+            if (dv >= ndev) dv = 0;
+        }
+        const uint32_t m = __ballot_sync(FULL, dv == d);
+        if (dv == d) {
+            const uint32_t pos = nd + __popc(m & lanemask_lt());
+            s_sub[pos] = f;
+            s_idx[pos] = (uint16_t)i;
+        }
+        nd += __popc(m);
+    }
+    __syncwarp();
+    return nd;
+}
+
+// One (sub-)trace of n apps on one simulated device under one policy.
+template <class TM, int K, bool PROG>
+struct TraceSim {
+    using T = typename TM::T;
+    using Key = typename TM::Key;
+    using Used = typename std::conditional<PROG, int64_t, uint32_t>::type;
+
+    const SimParams& P;
+    const uint32_t lane;
+    // per-warp shared memory
+    const uint4* s_app;
+    uint64_t* s_q;
+    uint64_t* s_kt;
+    uint32_t* s_kc;
+    T* s_grant;
+    T* s_end;
+    uint16_t* s_st;
+    int32_t* s_held;
+    // trace / policy
+    uint32_t n, cap;
+    bool prio_pol, mmu;
+    // warp-uniform simulation state
+    uint32_t counter, status;
+    uint32_t qlen;            // PROG: compacted queue length; T0: waiting entries
+    uint32_t qtail;           // T0: next queue position (apps enqueue at most once)
+    uint32_t qhead;           // T0 FIFO: first waiting position
+    uint32_t qm_lane;         // T0: lane j holds the presence bits of queue positions 32j..32j+31
+    // statistics (harness.py:373-461 integer forms)
+    T last, mem_t, busy_prev;
+    typename TM::Acc I, B;
+    Used used;
+    int32_t busy_level, holders;
+    uint32_t maxh, grants, pops;
+    sg_event* ev;
+    uint32_t ev_n;
+
+    __device__ __forceinline__ TraceSim(const SimParams& p, uint32_t lane_, uint8_t* ws,
+                                        const uint4* apps_smem)
+        : P(p), lane(lane_) {
+        s_app = apps_smem;
+        s_q = reinterpret_cast<uint64_t*>(ws + p.off_q);
+        s_kt = reinterpret_cast<uint64_t*>(ws + p.off_key);
+        s_kc = reinterpret_cast<uint32_t*>(ws + p.off_kc);
+        s_grant = reinterpret_cast<T*>(ws + p.off_grant);
+        s_end = reinterpret_cast<T*>(ws + p.off_end);
+        s_st = reinterpret_cast<uint16_t*>(ws + p.off_st);
+        s_held = reinterpret_cast<int32_t*>(ws + p.off_held);
+    }
+
+    // harness.py:505-508: a push takes the next counter value
+    __device__ __forceinline__ Key push_key(T t, uint32_t app) {
+        counter += 1;
+        if (counter >= kCounterLimit) status |= SG_ST_COUNTER_OVERFLOW;
+        return TM::make_key(t, counter, app);
+    }
+
+    // -------------------------------------------------------------- events
+    __device__ __forceinline__ void emit(T t, uint32_t app, uint32_t kind, uint32_t mib) {
+        if constexpr (PROG) {
+            if (ev != nullptr) {
+                if (lane == 0 && ev_n < P.ev_cap) {
+                    sg_event e;
+                    e.t = TM::bits(t);
+                    e.app = (uint16_t)app;
+                    e.kind = (uint8_t)kind;
+                    e.dev = 0;
+                    e.mib = mib;
+                    ev[ev_n] = e;
+                }
+                ev_n++;
+            }
+        }
+    }
+
+    // ---------------------------------------------------------- statistics
+    // Memory point: total += level * (t - prev) (harness.py:414-426).
+    __device__ __forceinline__ void mem_point(T now) {
+        if constexpr (TM::F64) {
+            I = __dadd_rn(I, __dmul_rn(__ll2double_rn((int64_t)used * 1048576LL), __dsub_rn(now, mem_t)));
+        } else if constexpr (PROG) {
+            I += (uint64_t)(used * (int64_t)(now - mem_t));
+        } else {
+            I += (uint64_t)used * (uint32_t)(now - mem_t);
+        }
+        mem_t = now;
+    }
+    // Busy point in time order: the sweep of harness.py:429-437.  Points of
+    // equal time add zero, so pop order within a tick is immaterial.
+    __device__ __forceinline__ void busy_point(T now, int32_t delta) {
+        if constexpr (TM::F64) {
+            if (busy_level > 0) B = __dadd_rn(B, __dsub_rn(now, busy_prev));
+        } else {
+            B += busy_level > 0 ? (uint32_t)(now - busy_prev) : 0u;
+        }
+        busy_prev = now;
+        busy_level += delta;
+    }
+
+    // ------------------------------------------- grant_waiters (T0 traces)
+    // harness.py:545-558 + policy.py:52-74 over the position-stable queue.
+    __device__ __forceinline__ void grant_waiters_t0(T now) {
+        if (qlen == 0) return;
+        if (!mmu && !prio_pol) {
+            // FIFO removes only from the head: the queue is the contiguous
+            // position range [qhead, qtail); grant while the head fits.
+            const uint32_t budget0 = cap - used;
+            uint32_t budget = budget0, g = 0;
+            while (qhead < qtail) {
+                const uint64_t e = s_q[qhead];
+                const uint32_t mib = (uint32_t)e;
+                if (mib > budget) break;
+                const uint32_t a = q_app(e);
+                budget -= mib;
+                g += 1;
+                TM::store(s_kt, s_kc, a, TM::make_key(now, counter + g, a));
+                s_grant[a] = now;
+                s_st[a] = 0;
+                qhead += 1;
+            }
+            if (g) {
+                mem_point(now);
+                used += budget0 - budget;
+                holders += (int32_t)g;
+                maxh = max(maxh, (uint32_t)holders);
+                grants += g;
+                counter += g;
+                qlen -= g;
+            }
+            return;
+        }
+        while (true) {
+            uint32_t budget = cap - used;
+            const uint32_t budget0 = budget;
+            uint32_t top = 0;
+            const uint32_t active = __ballot_sync(FULL, qm_lane != 0);  // chunks with waiters
+            if (prio_pol) {
+                // top = max waiting priority (policy.py:58-63)
+                uint32_t best = 0;
+                for (uint32_t a = active; a; a &= a - 1) {
+                    const uint32_t j = __ffs(a) - 1;
+                    const uint32_t m = __shfl_sync(FULL, qm_lane, j);
+                    const uint64_t e = s_q[32 * j + lane];
+                    if ((m >> lane) & 1u) best = max(best, q_prio(e) + 1);
+                }
+                top = __reduce_max_sync(FULL, best) - 1;
+            }
+            uint32_t granted = 0;
+            bool stop = false;
+            for (uint32_t a = active; a && !stop; a &= a - 1) {
+                const uint32_t j = __ffs(a) - 1;
+                uint32_t rem = __shfl_sync(FULL, qm_lane, j);
+                const uint64_t e = s_q[32 * j + lane];
+                const uint32_t mib = (uint32_t)e;
+                const uint32_t app_l = q_app(e);
+                if (prio_pol) rem &= __ballot_sync(FULL, q_prio(e) == top);
+                const bool cand = (rem >> lane) & 1u;
+                uint32_t gm = 0;
+                if (!mmu) {
+                    // FIFO: grant from the head while it fits; a misfit blocks.
+                    while (rem) {
+                        const uint32_t h = __ffs(rem) - 1;
+                        const uint32_t mh = __shfl_sync(FULL, mib, h);
+                        if (mh > budget) { stop = true; break; }
+                        gm |= 1u << h;
+                        budget -= mh;
+                        rem &= rem - 1;
+                    }
+                } else {
+                    // MMU: first fit with a shrinking budget, skip misfits.
+                    while (rem) {
+                        const uint32_t fm = __ballot_sync(FULL, cand && mib <= budget) & rem;
+                        if (!fm) break;
+                        const uint32_t h = __ffs(fm) - 1;
+                        gm |= 1u << h;
+                        budget -= __shfl_sync(FULL, mib, h);
+                        rem &= (h == 31) ? 0u : (0xFFFFFFFFu << (h + 1));
+                    }
+                }
+                if (gm) {
+                    // grants in queue order: pc past the alloc, push (now, ++counter)
+                    if ((gm >> lane) & 1u) {
+                        TM::store(s_kt, s_kc, app_l,
+                                  TM::make_key(now, counter + __popc(gm & lanemask_lt()) + 1, app_l));
+                        s_grant[app_l] = now;
+                        s_st[app_l] = 0;
+                    }
+                    const uint32_t g = __popc(gm);
+                    counter += g;
+                    granted += g;
+                    if (lane == j) qm_lane &= ~gm;
+                }
+            }
+            if (granted) {
+                mem_point(now);
+                used += budget0 - budget;
+                holders += (int32_t)granted;
+                maxh = max(maxh, (uint32_t)holders);
+                grants += granted;
+                qlen -= granted;
+            }
+            // FIFO/MMU: a second round is provably empty; priority policies
+            // drain the top class and may serve the next one (harness.py:547-550)
+            if (granted == 0 || !prio_pol || qlen == 0) return;
+        }
+    }
+
+    // ----------------------------------------- grant_waiters (step programs)
+    // Apps may wait several times: the queue is compacted after each round.
+    __device__ __forceinline__ void grant_waiters_prog(T now) {
+        if (qlen == 0) return;
+        while (true) {
+            int64_t budget = (int64_t)cap - (int64_t)used;
+            uint32_t top = 0;
+            if (prio_pol) {
+                uint32_t best = 0;
+                for (uint32_t base = 0; base < qlen; base += 32) {
+                    const uint32_t i = base + lane;
+                    if (i < qlen) best = max(best, q_prio(s_q[i]) + 1);
+                }
+                top = __reduce_max_sync(FULL, best) - 1;
+            }
+            uint32_t removed = 0;
+            bool stop = false;
+            for (uint32_t base = 0; base < qlen; base += 32) {
+                const uint32_t i = base + lane;
+                const bool valid = i < qlen;
+                const uint64_t e = valid ? s_q[i] : 0ull;
+                const uint32_t mib = (uint32_t)e;
+                const uint32_t app_l = q_app(e);
+                const bool cand = valid && !stop && (!prio_pol || q_prio(e) == top);
+                uint32_t rem = __ballot_sync(FULL, cand);
+                uint32_t gm = 0;
+                if (!mmu) {
+                    while (rem) {
+                        const uint32_t h = __ffs(rem) - 1;
+                        const int64_t mh = __shfl_sync(FULL, mib, h);
+                        if (mh > budget) { stop = true; break; }
+                        gm |= 1u << h;
+                        budget -= mh;
+                        rem &= rem - 1;
+                    }
+                } else {
+                    while (rem) {
+                        const uint32_t fm = __ballot_sync(FULL, cand && (int64_t)mib <= budget) & rem;
+                        if (!fm) break;
+                        const uint32_t h = __ffs(fm) - 1;
+                        gm |= 1u << h;
+                        budget -= (int64_t)__shfl_sync(FULL, mib, h);
+                        rem &= (h == 31) ? 0u : (0xFFFFFFFFu << (h + 1));
+                    }
+                }
+                const bool mine = (gm >> lane) & 1u;
+                const uint32_t below = __popc(gm & lanemask_lt());
+                if (gm) {
+                    const uint32_t g = __popc(gm);
+                    const uint32_t sum = __reduce_add_sync(FULL, mine ? mib : 0u);
+                    mem_point(now);
+                    used += sum;
+                    bool inc = false;
+                    if (mine) {
+                        TM::store(s_kt, s_kc, app_l, TM::make_key(now, counter + below + 1, app_l));
+                        if (TM::is_never(s_grant[app_l])) s_grant[app_l] = now;
+                        s_st[app_l] = (uint16_t)(s_st[app_l] + 1);
+                        const int32_t h = s_held[app_l];
+                        const int32_t nh = h + (int32_t)mib;
+                        s_held[app_l] = nh;
+                        inc = h <= 0 && nh > 0;
+                    }
+                    holders += __popc(__ballot_sync(FULL, inc));
+                    counter += g;
+                    if (counter >= kCounterLimit) status |= SG_ST_COUNTER_OVERFLOW;
+                    maxh = max(maxh, (uint32_t)max(holders, 0));
+                    grants += g;
+                    if (ev != nullptr) {
+                        if (mine) {
+                            const uint32_t pos = ev_n + 2 * below;
+                            sg_event e1;
+                            e1.t = TM::bits(now);
+                            e1.app = (uint16_t)app_l;
+                            e1.dev = 0;
+                            e1.mib = mib;
+                            e1.kind = SG_EV_GRANT;
+                            if (pos < P.ev_cap) ev[pos] = e1;
+                            e1.kind = SG_EV_ALLOC;
+                            if (pos + 1 < P.ev_cap) ev[pos + 1] = e1;
+                        }
+                        ev_n += 2 * g;
+                    }
+                }
+                const uint32_t shift = removed + below;
+                __syncwarp();
+                if (valid && !mine && shift) s_q[i - shift] = e;
+                removed += __popc(gm);
+                __syncwarp();
+            }
+            qlen -= removed;
+            if (removed == 0 || !prio_pol || qlen == 0) return;
+        }
+    }
+
+    // ---------------------------------------------------- advance (T0 mode)
+    // harness.py:510-543 on the flattened program cpu/alloc/busy/free.  The
+    // cpu step only runs at the initial pop (run()); a popped app is either
+    // arriving (alloc pending), granted from the queue (busy next) or ending
+    // its busy step (free next), so the rest is straight-line code.
+    __device__ __forceinline__ void advance_t0(uint32_t app, T now) {
+        const uint4 f = s_app[app];
+        const uint32_t st = s_st[app];
+        __syncwarp();
+        last = now;
+        Key nk = TM::inf();
+        if (st & kBusyFlag) {
+            busy_point(now, -1);
+        } else {
+            if (st & kAllocPending) {
+                if (f.y <= cap - used) {  // arrival bypass (harness.py:521-531)
+                    mem_point(now);
+                    used += f.y;
+                    holders += 1;
+                    maxh = max(maxh, (uint32_t)holders);
+                    grants += 1;
+                    s_grant[app] = now;
+                } else {                   // wait (harness.py:532-536)
+                    s_q[qtail] = q_pack(app, min(f.y, kSat), f.w & 0xFFu);
+                    if (lane == (qtail >> 5)) qm_lane |= 1u << (qtail & 31);
+                    qtail += 1;
+                    qlen += 1;
+                    TM::store(s_kt, s_kc, app, nk);
+                    return;
+                }
+            }
+            if (f.z) {  // busy (harness.py:514-520)
+                // no overflow checks: run() verified max arrival + sum(busy) < 2^32 - 1
+                // ticks (a bound on every event time) and counters stay < 4n
+                busy_point(now, +1);
+                counter += 1;
+                nk = TM::make_key(now + f.z, counter, app);
+                s_st[app] = kBusyFlag;
+                TM::store(s_kt, s_kc, app, nk);
+                return;
+            }
+        }
+        if (f.y) {  // free -> grant_waiters (harness.py:537-542)
+            mem_point(now);
+            used -= f.y;
+            holders -= 1;
+            grant_waiters_t0(now);
+        }
+        s_end[app] = now;  // harness.py:543
+        TM::store(s_kt, s_kc, app, nk);
+    }
+
+    // ------------------------------------------------- advance (programs)
+    __device__ __forceinline__ void advance_prog(uint32_t app, T now) {
+        const uint4 f = s_app[app];  // x = first step, y = step count
+        uint32_t pc = s_st[app];
+        int32_t held = s_held[app];
+        __syncwarp();
+        last = now;
+        if (pc & kBusyFlag) {
+            busy_point(now, -1);
+            pc &= ~kBusyFlag;
+        }
+        Key nk = TM::inf();
+        while (true) {
+            if (pc >= f.y) {  // harness.py:543
+                s_end[app] = now;
+                emit(now, app, SG_EV_END, 0);
+                break;
+            }
+            const uint4 stp = __ldg(reinterpret_cast<const uint4*>(P.steps) + f.x + pc);
+            const uint32_t op = stp.x, mib = stp.y;
+            const uint64_t dur = ((uint64_t)stp.w << 32) | stp.z;
+            if (op == SG_OP_CPU || op == SG_OP_BUSY) {  // harness.py:514-520
+                const T t2 = TM::add(now, dur, status);
+                pc += 1;
+                if (op == SG_OP_BUSY) {
+                    busy_point(now, +1);
+                    emit(now, app, SG_EV_BUSY_START, 0);
+                    emit(t2, app, SG_EV_BUSY_END, 0);
+                    pc |= kBusyFlag;
+                }
+                nk = push_key(t2, app);
+                break;
+            }
+            if (op == SG_OP_ALLOC) {  // harness.py:521-536
+                emit(now, app, SG_EV_REQUEST, mib);
+                if ((int64_t)used + (int64_t)mib <= (int64_t)cap) {
+                    mem_point(now);
+                    used += mib;
+                    if (held <= 0 && held + (int32_t)mib > 0) holders += 1;
+                    held += (int32_t)mib;
+                    maxh = max(maxh, (uint32_t)max(holders, 0));
+                    grants += 1;
+                    if (TM::is_never(s_grant[app])) s_grant[app] = now;
+                    emit(now, app, SG_EV_GRANT, mib);
+                    emit(now, app, SG_EV_ALLOC, mib);
+                    pc += 1;
+                    continue;
+                }
+                s_q[qlen] = q_pack(app, min(mib, kSat), f.w & 0xFFu);
+                qlen += 1;
+                break;
+            }
+            // SG_OP_FREE: harness.py:537-542
+            mem_point(now);
+            used -= mib;
+            if (held > 0 && held - (int32_t)mib <= 0) holders -= 1;
+            held -= (int32_t)mib;
+            pc += 1;
+            s_st[app] = (uint16_t)pc;
+            s_held[app] = held;
+            emit(now, app, SG_EV_FREE, mib);
+            grant_waiters_prog(now);
+        }
+        s_st[app] = (uint16_t)pc;
+        s_held[app] = held;
+        TM::store(s_kt, s_kc, app, nk);
+    }
+
+    __device__ __forceinline__ void advance(uint32_t app, T now) {
+        if constexpr (PROG) advance_prog(app, now);
+        else advance_t0(app, now);
+    }
+
+    // first step of app i is cpu(dur)?  (the initial pop then only pushes)
+    __device__ __forceinline__ bool first_is_cpu(uint32_t i, uint64_t& dur) const {
+        const uint4 f = s_app[i];
+        if constexpr (PROG) {
+            if (f.y == 0) return false;
+            const uint4 st = __ldg(reinterpret_cast<const uint4*>(P.steps) + f.x);
+            dur = ((uint64_t)st.w << 32) | st.z;
+            return st.x == SG_OP_CPU;
+        } else {
+            dur = f.x;
+            return f.x != 0;
+        }
+    }
+
+    // ------------------------------------------------------------------ run
+    __device__ __forceinline__ void run(uint32_t n_apps, uint32_t policy, uint32_t cap_mib, sg_event* ev_slice) {
+        n = n_apps;
+        cap = cap_mib;
+        prio_pol = policy >= SG_POLICY_PFIFO;
+        mmu = (policy & 1u) != 0;
+        counter = n;  // initial pushes took counters 1..n (harness.py:560-562)
+        status = 0;
+        qlen = 0;
+        qtail = 0;
+        qhead = 0;
+        qm_lane = 0;
+        last = mem_t = busy_prev = TM::zero();
+        I = 0;
+        B = 0;
+        used = 0;
+        busy_level = holders = 0;
+        maxh = grants = pops = 0;
+        ev = ev_slice;
+        ev_n = 0;
+        // Initial pops run in index order at t = 0 before anything else.  An
+        // app whose first step is cpu(d) only pushes (t = d, ++counter); when
+        // every app is like that all keys are assigned at once, otherwise runs
+        // of such apps are batched and the others advanced one by one.
+        bool all_simple = true;
+        bool big = false;  // T0: an app whose fields could push times past 2^32 - 1
+#pragma unroll
+        for (int j = 0; j < K; j++) {
+            const uint32_t i = 32 * j + lane;
+            bool simple = true;
+            uint64_t dur = 0;
+            if (i < n) {
+                if constexpr (!PROG) big = big || s_app[i].x >= (1u << 31) || s_app[i].z >= (1u << 21);
+                s_grant[i] = TM::never();
+                s_end[i] = TM::never();
+                if constexpr (PROG) s_held[i] = 0;
+                simple = first_is_cpu(i, dur);
+                if (simple) {
+                    const T t0 = TM::add(TM::zero(), dur, status);
+                    TM::store(s_kt, s_kc, i, TM::make_key(t0, n + i + 1, i));
+                } else {
+                    TM::store(s_kt, s_kc, i, TM::inf());
+                }
+                if constexpr (PROG) {
+                    s_st[i] = simple ? 1 : 0;
+                    if (ev != nullptr && i < P.ev_cap) {  // start events (harness.py:561)
+                        sg_event e;
+                        e.t = TM::bits(TM::zero());
+                        e.app = (uint16_t)i;
+                        e.kind = SG_EV_START;
+                        e.dev = 0;
+                        e.mib = 0;
+                        ev[i] = e;
+                    }
+                } else {
+                    s_st[i] = s_app[i].y ? kAllocPending : 0u;
+                }
+            } else {
+                TM::store(s_kt, s_kc, i, TM::inf());
+            }
+            all_simple = all_simple && simple;
+        }
+        status = __reduce_or_sync(FULL, status);
+        if constexpr (!PROG) {
+            // every event time is <= max arrival + sum(busy) (after the last
+            // arrival the clock only advances while some app is busy); with
+            // arrival < 2^31 and busy < 2^21 (n <= 1024) it fits in 32 bits
+            if (__any_sync(FULL, big)) {
+                uint64_t bsum = 0, amax = 0;
+                for (uint32_t i = lane; i < n; i += 32) {
+                    bsum += s_app[i].z;
+                    amax = max(amax, (uint64_t)s_app[i].x);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    bsum += __shfl_xor_sync(FULL, bsum, o);
+                    amax = max(amax, __shfl_xor_sync(FULL, amax, o));
+                }
+                if (amax + bsum > 0xFFFFFFFEull) status |= SG_ST_TICK_OVERFLOW;
+            }
+        }
+        if constexpr (PROG) {
+            if (ev != nullptr) ev_n = n;
+        }
+        uint32_t next_init = n;
+        if (__all_sync(FULL, all_simple)) {
+            counter = 2 * n;
+            if (counter >= kCounterLimit) status |= SG_ST_COUNTER_OVERFLOW;
+        } else {
+            next_init = 0;
+        }
+        __syncwarp();
+
+        while (true) {
+            uint32_t app;
+            T now;
+            if (next_init < n) {
+                const uint32_t c = next_init >> 5;
+                const uint32_t i = (c << 5) + lane;
+                const bool valid = i < n && i >= next_init;
+                uint64_t dur = 0;
+                const bool simple = valid && first_is_cpu(i, dur);
+                const uint32_t vm = __ballot_sync(FULL, valid);
+                const uint32_t sm = __ballot_sync(FULL, simple);
+                const uint32_t nonsimple = vm & ~sm;
+                const uint32_t run = nonsimple ? (sm & ((1u << (__ffs(nonsimple) - 1)) - 1u)) : sm;
+                if (run) {
+                    // re-assign the pre-set keys with the live counter
+                    if ((run >> lane) & 1u) {
+                        const T t0 = TM::add(TM::zero(), dur, status);
+                        TM::store(s_kt, s_kc, i,
+                                  TM::make_key(t0, counter + __popc(run & lanemask_lt()) + 1, i));
+                    }
+                    counter += __popc(run);
+                    if (counter >= kCounterLimit) status |= SG_ST_COUNTER_OVERFLOW;
+                    status = __reduce_or_sync(FULL, status);
+                }
+                __syncwarp();
+                if (!nonsimple) {
+                    next_init = min(n, (c + 1) << 5);
+                    continue;
+                }
+                app = (c << 5) + __ffs(nonsimple) - 1;
+                next_init = app + 1;
+                now = TM::zero();  // (initial pops are counted in finish())
+            } else {
+                __syncwarp();
+                Key lm = TM::load(s_kt, s_kc, lane);
+#pragma unroll
+                for (int j = 1; j < K; j++) {
+                    const Key k = TM::load(s_kt, s_kc, 32 * j + lane);
+                    if (TM::less(k, lm)) lm = k;
+                }
+                if (!TM::argmin(lm, now, app)) break;
+                pops += 1;
+            }
+            advance(app, now);
+        }
+    }
+
+    // --------------------------------------------------------------- output
+    // rec: statistics record index; s_idx: sub-trace -> trace app index (or null)
+    __device__ __forceinline__ void finish(uint64_t rec, uint64_t app_out_base, const uint16_t* s_idx,
+                           uint32_t* ev_count_out) {
+        __syncwarp();
+        uint32_t unf = 0;
+        for (uint32_t base = 0; base < n; base += 32) {
+            const uint32_t i = base + lane;
+            const bool valid = i < n;
+            T evv = TM::never();
+            if (valid) {
+                const T gv = s_grant[i];
+                evv = s_end[i];
+                const uint64_t o = app_out_base + (s_idx ? s_idx[i] : i);
+                if (P.grant) reinterpret_cast<T*>(P.grant)[o] = gv;
+                if (P.end) reinterpret_cast<T*>(P.end)[o] = evv;
+            }
+            unf += __popc(__ballot_sync(FULL, valid && TM::is_never(evv)));
+        }
+        if (ev_count_out != nullptr && lane == 0) *ev_count_out = ev_n;
+        if (lane == 0) {
+            const int64_t u = (int64_t)used;
+            uint32_t st = status;
+            if constexpr (TM::F64) {
+                const double cap_bytes = (double)cap * kMiB;
+                // makespan_s = max(t_end - t0, 1e-9); final integral term (harness.py:378, 425)
+                const double span = last >= 1e-9 ? last : 1e-9;
+                I = __dadd_rn(I, __dmul_rn(__ll2double_rn(u * 1048576LL), __dsub_rn(span, mem_t)));
+                double mem_pct = __ddiv_rn(__dmul_rn(100.0, I), __dmul_rn(cap_bytes, span));
+                double dev_pct = __ddiv_rn(__dmul_rn(100.0, B), span);
+                sg_trace_stats_f64 r;
+                r.makespan_s = last;
+                r.mem_integral = I;
+                r.busy_s = B;
+                r.grants = grants;
+                r.pops = pops + n;
+                r.max_holders = (uint16_t)maxh;
+                r.unfinished = (uint16_t)unf;
+                r.status = st;
+                reinterpret_cast<sg_trace_stats_f64*>(P.stats)[rec] = r;
+                if (n == 0) { mem_pct = 0.0; dev_pct = 0.0; }  // empty event list (harness.py:374-375)
+                if (P.mem_pct) P.mem_pct[rec] = mem_pct;
+                if (P.dev_pct) P.dev_pct[rec] = dev_pct;
+            } else {
+                store_tick_record(P, rec, n, cap, (uint32_t)last, (uint32_t)mem_t, (uint64_t)I,
+                                  (uint32_t)B, u, grants, pops + n, maxh, unf, st);
+            }
+        }
+        __syncwarp();
+    }
+};
+
+}  // namespace sg

@@ -17,6 +17,18 @@ from util import NEVER, POLICIES, floats_equal, golden
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["auto", "warp"], autouse=True)
+def engine(request, monkeypatch):
+    """Every parity test runs on both K1 engines: `auto` takes the lane kernel
+    (v4) wherever the batch is eligible (T0, <= 256 apps), `warp` forces the
+    warp-per-trace kernel (v3)."""
+    if request.param == "warp":
+        monkeypatch.setenv("SGPU_K1", "warp")
+    else:
+        monkeypatch.delenv("SGPU_K1", raising=False)
+    return request.param
+
+
 def to_dev(apps_u32, dev):
     a = np.ascontiguousarray(apps_u32, dtype=np.uint32)
     return torch.from_numpy(a.view(np.int32)).to(dev)
@@ -150,6 +162,34 @@ def test_edge_cases(cuda):
     z = np.zeros((3, 5, 4), dtype=np.uint32)
     res = check_against_oracle(z, (10,), cuda)
     assert (res.ticks("end") == 0).all() and (res.ticks("grant") == NEVER).all()
+
+
+def test_lane_fallback_heap_overflow(cuda):
+    """More than 32 apps busy at once (no-alloc apps with long busy steps)
+    overflow a lane's heap; those lanes are re-simulated exactly in-kernel."""
+    rng = np.random.default_rng(5)
+    n, nt = 64, 96
+    apps = np.zeros((nt, n, 4), dtype=np.uint32)
+    apps[:, :, 0] = rng.integers(0, 40, (nt, n))
+    apps[:, :, 1] = np.where(rng.random((nt, n)) < 0.7, 0, rng.integers(1, 300, (nt, n)))
+    apps[:, :, 2] = rng.integers(500, 900, (nt, n))
+    apps[:, :, 3] = rng.integers(0, 4, (nt, n))
+    apps[::2, :, 1] = rng.integers(1, 20, (nt // 2, n))      # mixed: some lanes stay on the fast path
+    check_against_oracle(apps, (1000,), cuda)
+
+
+def test_lane_fallback_tick_range(cuda):
+    """Traces with arrivals >= 2^31 or busy steps >= 2^21 ticks (whose times
+    could approach the 32-bit tick range) take the exact fallback."""
+    rng = np.random.default_rng(8)
+    n, nt = 40, 64
+    apps = np.zeros((nt, n, 4), dtype=np.uint32)
+    apps[:, :, 0] = rng.integers(0, 1000, (nt, n))
+    apps[:, :, 1] = rng.integers(1, 600, (nt, n))
+    apps[:, :, 2] = rng.integers(1, 50, (nt, n))
+    apps[:8, 0, 0] = np.uint32(0xF0000000)                  # arrival >= 2^31
+    apps[8:16, 1, 2] = np.uint32(1 << 22)                    # busy >= 2^21, still in range
+    check_against_oracle(apps, (1000,), cuda)
 
 
 def test_ragged_offsets(cuda):
