@@ -3,7 +3,7 @@
 //
 // Same semantics as trace_sim_kernel (sgpu_sim.cu),
 // restated for a single thread.  The T0 shape (cpu(arrival) -> alloc ->
-// busy -> free, memshare/harness.py:478-490) makes three reductions exact:
+// busy -> free, memshare/harness.py:478-490) makes these reductions exact:
 //
 //  * Arrival stream.  The initial pops run in index order at t = 0
 //    (harness.py:560-562); an app with arrival a > 0 only pushes (a, c), with
@@ -11,49 +11,79 @@
 //    per-trace sort, shared by every lane of the trace, replaces those heap
 //    entries.  Heap counters are restated as order-preserving virtual
 //    counters: the initial pop of app i owns the counter block [i << LOGN,
-//    (i + 1) << LOGN) (its arrival push, or the pushes its inline run at t = 0
-//    makes), and every later push counts up from n << LOGN.  Comparing
+//    (i + 1) << LOGN) (its arrival push, or the pushes its inline run at
+//    t = 0 makes), and every later push counts up from n << LOGN.  Comparing
 //    (t, virtual counter) is therefore the reference's (t, counter) order
 //    (harness.py:505-508, 563-565).
-//  * Wait queue.  An app enqueues at most once, at its arrival pop, so its
-//    queue position is its rank in the arrival order (FIFO/MMU), or its rank
-//    in (priority desc, arrival order) for the priority policies (the class
-//    order of policy.py:58-63).  The queue is a presence bitmask over those
-//    static positions, in registers; select_grants (policy.py:52-74) is a
-//    scan over set bits: FIFO stops at the first misfit, MMU skips it, the
-//    priority kinds scan only the top class [first waiting position, class
-//    end) and loop to the next class when it drained (harness.py:545-558).
-//  * Heap.  Only busy-end and wake-up entries remain: a per-lane binary heap
-//    in shared memory, laid out [slot][lane] so every access of a warp is
-//    bank-conflict free whatever slot each lane touches.
+//  * Wake-ups.  grant_waiters pushes each granted waiter at (now, ++counter)
+//    (harness.py:558): later than every pending entry of time `now`, earlier
+//    than any entry of a later time.  They are a per-lane FIFO, drained once
+//    no arrival / busy end of time `now` remains.  The heap keeps busy ends
+//    only: per-lane binary heap in shared memory, laid out [slot][lane] so a
+//    warp's accesses are bank-conflict free whatever slot each lane touches.
+//  * Wait queue.  An app enqueues at most once, at its arrival pop, so the
+//    queue (harness.py:532-536) is a presence bitmask over arrival positions,
+//    in registers; queue order is position order.  select_grants
+//    (policy.py:52-74) works on masks: the priority kinds restrict to the
+//    top class (per-trace class masks, policy.py:58-63), FIFO grants the
+//    head while it fits, MMU takes first fits with a shrinking budget.  For
+//    traces of <= 64 apps MMU is O(1) per grant: a per-trace table T[r] of
+//    the positions whose request is among the r smallest gives the set that
+//    fits `budget` as T[#requests <= budget] (one binary search), and the
+//    next first fit is the lowest bit of mask & class & T & above(last).
 //
-// Lanes that cannot take this path (heap capacity exceeded, or a trace
-// whose times could leave the 32-bit tick range) are re-simulated by the
-// whole warp with the exact warp-per-trace TraceSim (sgpu_tracesim.cuh)
-// right after, in the same kernel: no host round trip, no extra buffers.
+// Lanes that cannot take this path (heap or FIFO capacity exceeded, too many
+// priority classes, or a trace whose times could leave the 32-bit tick
+// range) are re-simulated by the whole warp with the exact warp-per-trace
+// TraceSim (sgpu_tracesim.cuh) right after, in the same kernel: no host
+// round trip, no extra buffers.
 #include "sgpu_tracesim.cuh"
 
 namespace sg {
 
-constexpr uint32_t kLaneHeap = 32;          // heap slots per lane
-constexpr uint32_t kKindWake = 0, kKindBusyEnd = 1, kKindArrival = 2;
+constexpr uint32_t kLaneHeap = 24;          // busy-end heap slots per lane
+constexpr uint32_t kLaneFifoWords = 8;      // wake FIFO: 4 app positions per u32 word
+constexpr uint32_t kLaneFifo = 4 * kLaneFifoWords;
+constexpr uint32_t kLaneClassMasks = 64;    // class masks per warp, split over its trace slots
+constexpr int kLaneWarpsPerBlock = 1;
 constexpr uint64_t kInf = ~0ull;
+constexpr uint32_t kBusyBits = 21;          // busy < 2^21 on this path; app index above it
 
 struct LaneParams {
     SimParams sp;          // inputs/outputs + the fallback TraceSim layout (off_* relative to off_fb)
-    uint32_t G;            // traces per block group (32 / ndev)
-    uint32_t need_cls;     // some policy is priority-aware: build the class order
-    uint32_t off_rec, off_cls, off_meta;  // block-shared staging (G trace slots)
-    uint32_t off_fb, fb_bytes;            // per-warp region: heap / scratch / fallback
-    uint32_t block_bytes;
+    uint32_t G;            // traces per warp (32 / lpt)
+    uint32_t lpt;          // lanes per trace = npol * ndev
+    uint32_t need_cls;     // a priority policy is requested: build class masks
+    uint32_t need_tbl;     // an MMU-type policy on <= 64-app traces: build the fit table
+    uint32_t cm_per_trace; // class-mask capacity of one trace slot
+    // per-warp shared-memory layout (bytes)
+    uint32_t off_a, off_mem, off_bw, off_smem, off_fen, off_tbl, off_cm, off_meta, off_fifo, off_fb,
+        warp_bytes;
 };
 
-// meta per trace slot (u16): [0] n, [1] big, [2..10] device bounds, [11..18] a==0 counts
+// Per-trace-slot strides (in elements) of the shared arrays, skewed so the
+// slots of a warp start on different banks: 16-byte loads of the 8 slots of
+// a warp (fence / block / table reads) hit disjoint bank groups.
+template <uint32_t N> struct SlotStride {
+    static constexpr uint32_t S32 = N + 4;          // u32 record arrays
+    static constexpr uint32_t SRT = N + 8 + 4;      // sorted requests (+8: rank-search pad block)
+    static constexpr uint32_t FEN = N / 8 + 4;      // fences: every 8th sorted request
+    static constexpr uint32_t T64 = N + 2;          // fit table (N + 1 entries)
+};
+
+// meta per trace slot (u16): [0] n, [1] fail (big times / too many classes),
+// [2..10] device bounds in arrival order, [11..18] apps arriving at t = 0 per
+// device, [19..27] class-mask index bounds per device
 constexpr uint32_t kMetaU16 = 32;
 
 __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
     const uint32_t lo = __shfl_xor_sync(FULL, (uint32_t)v, m);
     const uint32_t hi = __shfl_xor_sync(FULL, (uint32_t)(v >> 32), m);
+    return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t shfl_up_u64(uint64_t v, int m) {
+    const uint32_t lo = __shfl_up_sync(FULL, (uint32_t)v, m);
+    const uint32_t hi = __shfl_up_sync(FULL, (uint32_t)(v >> 32), m);
     return ((uint64_t)hi << 32) | lo;
 }
 __device__ __forceinline__ uint32_t shfl_xor_key(uint32_t v, int m) { return __shfl_xor_sync(FULL, v, m); }
@@ -97,22 +127,34 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+__device__ __forceinline__ uint32_t ffs64(uint64_t x) { return (uint32_t)__ffsll((long long)x) - 1u; }
+
 template <int K>
 struct LaneSim {
     static constexpr uint32_t N = 32u * K;
     static constexpr uint32_t NW = (N + 63u) / 64u;  // queue mask words
     static constexpr uint32_t LOGN = K == 1 ? 5 : K == 2 ? 6 : K == 4 ? 7 : 8;
+    static constexpr bool TBL = K <= 2;              // fit table (one mask word)
 
     const SimParams& P;
-    const uint4* rec;      // trace slot records, arrival order
-    const uint32_t* cls;   // class position -> apos | class_end << 16
-    uint64_t* heap;        // this lane's column: heap[h * 32]
-    uint64_t out_base;     // grant/end index of app 0 of the trace under this policy
+    // trace slot (shared by the trace's lanes), arrival-position order
+    const uint32_t* s_a;     // arrival tick
+    const uint32_t* s_mem;   // request MiB
+    const uint32_t* s_bw;    // busy | app << kBusyBits
+    const uint32_t* s_smem;  // requests sorted ascending (padded with ~0 to N + 8)
+    const uint32_t* s_fen;   // s_fen[i] = s_smem[8i + 7]
+    const uint64_t* s_tbl;   // T[r]: positions of the r smallest requests
+    const uint64_t* s_cm;    // class masks of this lane's device, top class first
+    uint32_t ncls;
+    // this lane's columns
+    uint64_t* heap;          // heap[h * 32]
+    uint32_t* fifo;          // fifo[w * 32]
+    uint64_t out_base;       // grant/end index of app 0 of the trace under this policy
     uint32_t cap, used;
     bool prio_pol, mmu, fail;
     uint64_t mask[NW];
-    uint32_t hs;
-    uint64_t kh;           // heap top (kInf when empty)
+    uint32_t hs, fhead, ftail;
+    uint64_t kh;             // heap top (kInf when empty)
     uint32_t counter;
     // statistics (harness.py:373-461 integer forms)
     uint32_t last, mem_t, busy_prev, B;
@@ -132,10 +174,10 @@ struct LaneSim {
         busy_level += delta;
     }
 
-    // ------------------------------------------------------------ heap
-    __device__ __forceinline__ void push(uint32_t t, uint32_t kind, uint32_t q) {
+    // ------------------------------------------------- busy-end heap
+    __device__ __forceinline__ void push(uint32_t t, uint32_t q) {
         if (hs >= kLaneHeap) { fail = true; return; }
-        const uint64_t key = ((uint64_t)t << 32) | (counter << 10) | (kind << 8) | q;
+        const uint64_t key = ((uint64_t)t << 32) | (counter << 8) | q;
         counter += 1;
         uint32_t i = hs++;
         while (i > 0) {
@@ -154,7 +196,6 @@ struct LaneSim {
         const uint64_t lastk = heap[hs * 32];
         uint32_t i = 0;
         uint64_t top = lastk;
-        bool first = true;
         while (true) {
             uint32_t c = 2 * i + 1;
             if (c >= hs) break;
@@ -165,104 +206,168 @@ struct LaneSim {
             }
             if (lastk < ck) break;
             heap[i * 32] = ck;
-            if (first) top = ck;
-            first = false;
+            if (i == 0) top = ck;
             i = c;
         }
         heap[i * 32] = lastk;
         kh = top;
     }
 
-    // ------------------------------------------------------- wait queue
+    // ------------------------------------------------- wake FIFO
+    __device__ __forceinline__ void wake(uint32_t q) {
+        if (ftail - fhead >= kLaneFifo) { fail = true; return; }
+        const uint32_t slot = ftail % kLaneFifo;
+        uint32_t* w = fifo + (slot >> 2) * 32;
+        const uint32_t sh = (slot & 3u) * 8u;
+        *w = (*w & ~(0xFFu << sh)) | (q << sh);
+        ftail += 1;
+    }
+    __device__ __forceinline__ uint32_t unwake() {
+        const uint32_t slot = fhead % kLaneFifo;
+        fhead += 1;
+        return (fifo[(slot >> 2) * 32] >> ((slot & 3u) * 8u)) & 0xFFu;
+    }
+
+    // ------------------------------------------------- wait queue
     __device__ __forceinline__ void enqueue(uint32_t q) {
 #pragma unroll
         for (uint32_t w = 0; w < NW; w++)
             if (w == (q >> 6)) mask[w] |= 1ull << (q & 63u);
     }
-    __device__ __forceinline__ uint32_t q_apos(uint32_t q) const {
-        return prio_pol ? (cls[q] & 0xFFFFu) : q;
+    // number of requests <= budget in the trace: two 8-ary levels of 16-byte
+    // loads (fences, then one block of 8 sorted requests)
+    __device__ __forceinline__ uint32_t fit_rank(uint32_t budget) const {
+        uint32_t j = 0;
+#pragma unroll
+        for (uint32_t i = 0; i < N / 32; i++) {
+            const uint4 f = reinterpret_cast<const uint4*>(s_fen)[i];
+            j += (f.x <= budget) + (f.y <= budget) + (f.z <= budget) + (f.w <= budget);
+        }
+        const uint4* blk = reinterpret_cast<const uint4*>(s_smem + 8 * j);
+        const uint4 u0 = blk[0], u1 = blk[1];
+        return 8 * j + (u0.x <= budget) + (u0.y <= budget) + (u0.z <= budget) + (u0.w <= budget) +
+               (u1.x <= budget) + (u1.y <= budget) + (u1.z <= budget) + (u1.w <= budget);
+    }
+    __device__ __forceinline__ void grant_one(uint32_t q, uint32_t m, uint32_t& budget, uint32_t& g) {
+#pragma unroll
+        for (uint32_t w = 0; w < NW; w++)
+            if (w == (q >> 6)) mask[w] &= ~(1ull << (q & 63u));
+        budget -= m;
+        g += 1;
+        wake(q);
     }
 
     // grant_waiters (harness.py:545-558) + select_grants (policy.py:52-74)
-    __device__ __forceinline__ void grant_waiters(uint32_t now) {
+    __device__ __forceinline__ void grant_waiters() {
+        uint32_t c = 0;  // current class (priority kinds)
         while (true) {
-            // first waiting position
-            uint32_t q0 = N;
+            // candidate set: the waiting entries of the top class (policy.py:58-63)
+            uint64_t cand[NW];
+            bool any = false;
+            if (prio_pol) {
+                while (c < ncls) {
 #pragma unroll
-            for (int w = NW - 1; w >= 0; w--)
-                if (mask[w]) q0 = 64u * w + (__ffsll((long long)mask[w]) - 1);
-            if (q0 == N) return;
-            const uint32_t qend = prio_pol ? (cls[q0] >> 16) : N;
+                    for (uint32_t w = 0; w < NW; w++) {
+                        cand[w] = mask[w] & s_cm[c * NW + w];
+                        any = any || cand[w] != 0;
+                    }
+                    if (any) break;
+                    c += 1;
+                }
+            } else {
+#pragma unroll
+                for (uint32_t w = 0; w < NW; w++) {
+                    cand[w] = mask[w];
+                    any = any || cand[w] != 0;
+                }
+            }
+            if (!any) return;
             const uint32_t budget0 = cap - used;
             uint32_t budget = budget0, g = 0;
-            bool left = false, stop = false;
+            if (mmu && TBL) {
+                // first fit with a shrinking budget: lowest waiting position
+                // among the requests that fit
+                uint64_t fit = cand[0] & s_tbl[fit_rank(budget)];
+                while (fit) {
+                    const uint32_t q = ffs64(fit);
+                    const uint32_t m = s_mem[q];
+                    grant_one(q, m, budget, g);
+                    if (fail) return;
+                    cand[0] &= ~(1ull << q);
+                    fit = budget ? (cand[0] & s_tbl[fit_rank(budget)] & ~((2ull << q) - 1ull)) : 0ull;
+                }
+            } else {
+                // FIFO: grant the head while it fits; MMU (long traces): skip misfits
+                bool stop = false;
 #pragma unroll
-            for (uint32_t w = 0; w < NW; w++) {
-                uint64_t bits = mask[w];
-                while (bits && !stop) {
-                    const uint32_t q = 64u * w + (__ffsll((long long)bits) - 1);
-                    bits &= bits - 1;
-                    if (q >= qend) { stop = true; break; }
-                    const uint32_t apos = q_apos(q);
-                    const uint32_t m = rec[apos].y;
-                    if (m <= budget) {
-                        budget -= m;
-                        g += 1;
-                        mask[w] &= ~(1ull << (q & 63u));
-                        push(now, kKindWake, apos);
-                        if (fail) return;
-                    } else {
-                        left = true;
-                        if (!mmu) stop = true;
+                for (uint32_t w = 0; w < NW; w++) {
+                    uint64_t bits = cand[w];
+                    while (bits && !stop) {
+                        const uint32_t q = 64u * w + ffs64(bits);
+                        bits &= bits - 1;
+                        const uint32_t m = s_mem[q];
+                        if (m <= budget) {
+                            grant_one(q, m, budget, g);
+                            if (fail) return;
+                        } else if (!mmu) {
+                            stop = true;
+                        }
                     }
                 }
             }
             if (g) {
-                mem_point(now);
+                mem_point(last);
                 used += budget0 - budget;
                 holders += (int32_t)g;
                 maxh = max(maxh, (uint32_t)holders);
                 grants += g;
             }
-            if (!prio_pol || g == 0 || left) return;
+            if (!prio_pol || g == 0) return;
+            // the top class continues only if it drained (harness.py:547-550)
+            bool left = false;
+#pragma unroll
+            for (uint32_t w = 0; w < NW; w++) left = left || (mask[w] & s_cm[c * NW + w]) != 0;
+            if (left) return;
         }
     }
 
     // --------------------------------------------------------- advance
-    __device__ __forceinline__ void end_app(const uint4& r, uint32_t now) {
-        if (r.y) {  // free -> grant_waiters (harness.py:537-542)
+    __device__ __forceinline__ void end_app(uint32_t m, uint32_t bw, uint32_t now) {
+        if (m) {  // free -> grant_waiters (harness.py:537-542)
             mem_point(now);
-            used -= r.y;
+            used -= m;
             holders -= 1;
-            grant_waiters(now);
+            grant_waiters();
         }
-        const uint64_t o = out_base + (r.w & kAppMask);  // end (harness.py:543)
+        const uint64_t o = out_base + (bw >> kBusyBits);  // end (harness.py:543)
         if (P.end) reinterpret_cast<uint32_t*>(P.end)[o] = now;
         // the grant is the busy start: busy runs [grant, grant + busy]
-        if (P.grant) reinterpret_cast<uint32_t*>(P.grant)[o] = r.y ? now - r.z : SG_NEVER;
+        if (P.grant)
+            reinterpret_cast<uint32_t*>(P.grant)[o] = m ? now - (bw & ((1u << kBusyBits) - 1u)) : SG_NEVER;
     }
-    __device__ __forceinline__ void run_from_busy(uint32_t q, const uint4& r, uint32_t now) {
-        if (r.z) {  // busy (harness.py:514-520)
+    __device__ __forceinline__ void run_from_busy(uint32_t q, uint32_t m, uint32_t bw, uint32_t now) {
+        const uint32_t b = bw & ((1u << kBusyBits) - 1u);
+        if (b) {  // busy (harness.py:514-520)
             busy_point(now, +1);
-            push(now + r.z, kKindBusyEnd, q);
+            push(now + b, q);
             return;
         }
-        end_app(r, now);
+        end_app(m, bw, now);
     }
-    __device__ __forceinline__ void arrive(uint32_t q, const uint4& r, uint32_t now) {
-        if (r.y) {
-            if (r.y <= cap - used) {  // arrival bypass (harness.py:521-531)
+    __device__ __forceinline__ void arrive(uint32_t q, uint32_t m, uint32_t bw, uint32_t now) {
+        if (m) {
+            if (m <= cap - used) {  // arrival bypass (harness.py:521-531)
                 mem_point(now);
-                used += r.y;
+                used += m;
                 holders += 1;
                 maxh = max(maxh, (uint32_t)holders);
                 grants += 1;
-            } else {                  // wait (harness.py:532-536)
-                enqueue(prio_pol ? ((r.w >> 10) & 0x3FFu) : q);
+            } else {                // wait (harness.py:532-536)
+                enqueue(q);
                 return;
             }
         }
-        run_from_busy(q, r, now);
+        run_from_busy(q, m, bw, now);
     }
 
     // Simulate device range [s, e) of the slot's arrival order (z apps arrive
@@ -276,7 +381,7 @@ struct LaneSim {
         fail = false;
 #pragma unroll
         for (uint32_t w = 0; w < NW; w++) mask[w] = 0;
-        hs = 0;
+        hs = fhead = ftail = 0;
         kh = kInf;
         last = mem_t = busy_prev = B = 0;
         I = 0;
@@ -285,48 +390,49 @@ struct LaneSim {
         // initial pops at t = 0: apps without a cpu step run inline, in index
         // order, each in its own virtual counter block
         for (uint32_t q = s; q < s + z; q++) {
-            const uint4 r = rec[q];
-            counter = (r.w & kAppMask) << LOGN;
-            arrive(q, r, 0u);
+            const uint32_t bw = s_bw[q];
+            counter = (bw >> kBusyBits) << LOGN;
+            arrive(q, s_mem[q], bw, 0u);
             if (fail) return false;
         }
         counter = n_trace << LOGN;
         uint32_t ap = s + z;
-        uint4 ra = make_uint4(0, 0, 0, 0);
         uint64_t ka = kInf;
+        uint32_t bwa = 0;
         if (ap < e) {
-            ra = rec[ap];
-            ka = ((uint64_t)ra.x << 32) | (((ra.w & kAppMask) << LOGN) << 10) | (kKindArrival << 8) | ap;
+            bwa = s_bw[ap];
+            ka = ((uint64_t)s_a[ap] << 32) | (((bwa >> kBusyBits) << LOGN) << 8) | ap;
         }
         while (true) {
-            if (ka < kh) {
+            const uint64_t kmin = ka < kh ? ka : kh;
+            if (fhead != ftail && (kmin >> 32) > last) {
+                // granted waiters resume after every other entry of their tick
+                const uint32_t q = unwake();
+                pops += 1;
+                run_from_busy(q, s_mem[q], s_bw[q], last);
+            } else if (ka < kh) {
                 const uint32_t q = ap;
-                const uint4 r = ra;
-                const uint32_t now = ra.x;
+                const uint32_t now = (uint32_t)(ka >> 32);
+                const uint32_t bw = bwa;
                 ap += 1;
                 if (ap < e) {
-                    ra = rec[ap];
-                    ka = ((uint64_t)ra.x << 32) | (((ra.w & kAppMask) << LOGN) << 10) | (kKindArrival << 8) | ap;
+                    bwa = s_bw[ap];
+                    ka = ((uint64_t)s_a[ap] << 32) | (((bwa >> kBusyBits) << LOGN) << 8) | ap;
                 } else {
                     ka = kInf;
                 }
                 pops += 1;
                 last = now;
-                arrive(q, r, now);
+                arrive(q, s_mem[q], bw, now);
             } else if (kh != kInf) {
                 const uint64_t key = kh;
                 pop();
                 const uint32_t q = (uint32_t)key & 0xFFu;
                 const uint32_t now = (uint32_t)(key >> 32);
-                const uint4 r = rec[q];
                 pops += 1;
                 last = now;
-                if (((uint32_t)key >> 8) & 1u) {  // busy end
-                    busy_point(now, -1);
-                    end_app(r, now);
-                } else {                          // granted waiter resumes
-                    run_from_busy(q, r, now);
-                }
+                busy_point(now, -1);
+                end_app(s_mem[q], s_bw[q], now);
             } else {
                 break;
             }
@@ -340,8 +446,8 @@ struct LaneSim {
 #pragma unroll
         for (uint32_t w = 0; w < NW; w++) {
             for (uint64_t bits = mask[w]; bits; bits &= bits - 1) {
-                const uint32_t q = 64u * w + (__ffsll((long long)bits) - 1);
-                const uint64_t o = out_base + (rec[q_apos(q)].w & kAppMask);
+                const uint32_t q = 64u * w + ffs64(bits);
+                const uint64_t o = out_base + (s_bw[q] >> kBusyBits);
                 if (P.grant) reinterpret_cast<uint32_t*>(P.grant)[o] = SG_NEVER;
                 if (P.end) reinterpret_cast<uint32_t*>(P.end)[o] = SG_NEVER;
                 unf += 1;
@@ -364,20 +470,33 @@ __device__ __forceinline__ void lane_trace_range(const SimParams& P, uint64_t t,
     }
 }
 
-// Stage trace t into slot g (scratch: the calling warp's fb region): records in (device, arrival, index) order, the
-// class order for the priority policies, device bounds.  Warp-collective.
+// Exclusive prefix over lanes 0..7 of a per-device count held by lane d.
+__device__ __forceinline__ uint32_t dev_scan_incl(uint32_t v, uint32_t lane) {
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(FULL, v, o);
+        if (lane >= (uint32_t)o) v += u;
+    }
+    return v;
+}
+
+// Stage trace t into slot g (scratch: the warp's fb region): SoA records in
+// (device, arrival, index) order, class masks of each device's priority
+// classes (highest first), the fit table.  Warp-collective.
 template <int K>
-__device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, uint8_t* fb, uint32_t g,
-                                            uint64_t t, uint32_t lane) {
+__device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, uint32_t g, uint64_t t,
+                                            uint32_t lane) {
     const SimParams& P = L.sp;
     constexpr uint32_t N = 32u * K;
+    constexpr uint32_t NW = (N + 63u) / 64u;
     uint64_t a0;
     uint32_t na;
     lane_trace_range(P, t, a0, na);
-    uint4* raw = reinterpret_cast<uint4*>(fb);
-    uint16_t* cpos = reinterpret_cast<uint16_t*>(fb + N * 16u);
-    uint4* rec = reinterpret_cast<uint4*>(ws + L.off_rec) + g * N;
-    uint32_t* cls = reinterpret_cast<uint32_t*>(ws + L.off_cls) + g * N;
+    uint4* raw = reinterpret_cast<uint4*>(ws + L.off_fb);
+    using SS = SlotStride<N>;
+    uint32_t* s_a = reinterpret_cast<uint32_t*>(ws + L.off_a) + g * SS::S32;
+    uint32_t* s_mem = reinterpret_cast<uint32_t*>(ws + L.off_mem) + g * SS::S32;
+    uint32_t* s_bw = reinterpret_cast<uint32_t*>(ws + L.off_bw) + g * SS::S32;
     uint16_t* meta = reinterpret_cast<uint16_t*>(ws + L.off_meta) + g * kMetaU16;
     const uint32_t ndev = P.ndev;
 
@@ -393,14 +512,31 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
             uint32_t dv = ndev > 1 ? (f.w >> 8) & 0xFFu : 0u;
             if (dv >= ndev) dv = 0;
             key[k] = ((uint64_t)dv << 42) | ((uint64_t)f.x << 10) | i;
-            big = big || f.x >= (1u << 31) || f.z >= (1u << 21);
+            big = big || f.x >= (1u << 31) || f.z >= (1u << kBusyBits);
         }
     }
-    big = __any_sync(FULL, big);
+    uint32_t fail = __any_sync(FULL, big) ? 1u : 0u;
     warp_bitonic_sort<K>(key, lane);
     __syncwarp();
-    // device bounds and arrivals at t = 0, per device
-    uint32_t cnt_d = 0, z_d = 0;  // lane d < ndev holds device d's counts
+    // SoA records in arrival order
+    uint32_t memk[K], prk[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        const uint32_t e = (uint32_t)k * 32u + lane;
+        memk[k] = ~0u;
+        prk[k] = 0;
+        if (key[k] != kInf) {
+            const uint32_t i = (uint32_t)key[k] & kAppMask;
+            const uint4 f = raw[i];
+            s_a[e] = f.x;
+            s_mem[e] = f.y;
+            s_bw[e] = (f.z & ((1u << kBusyBits) - 1u)) | (i << kBusyBits);
+            memk[k] = f.y;
+            prk[k] = f.w & 0xFFu;
+        }
+    }
+    // device bounds and arrivals at t = 0, per device (lane d holds device d)
+    uint32_t cnt_d = 0, z_d = 0;
     for (uint32_t d = 0; d < ndev; d++) {
         uint32_t c = 0, zc = 0;
 #pragma unroll
@@ -411,121 +547,144 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
         }
         if (lane == d) { cnt_d = c; z_d = zc; }
     }
+    const uint32_t dincl = dev_scan_incl(cnt_d, lane);
     if (L.need_cls) {
-        // class order: (device, priority desc, arrival position)
+        // classes = (device, priority) groups, highest priority first
+        // (policy.py:58-63); one mask of arrival positions per class
+        uint64_t* cm = reinterpret_cast<uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW + 1);
         uint32_t ck[K];
 #pragma unroll
         for (int k = 0; k < K; k++) {
             const uint32_t e = (uint32_t)k * 32u + lane;
-            ck[k] = ~0u;
-            if (key[k] != kInf) {
-                const uint32_t i = (uint32_t)key[k] & kAppMask;
-                const uint32_t prio = raw[i].w & 0xFFu;
-                ck[k] = ((uint32_t)(key[k] >> 42) << 18) | ((255u - prio) << 10) | e;
-            }
+            ck[k] = key[k] != kInf ? (((uint32_t)(key[k] >> 42) << 18) | ((255u - prk[k]) << 10) | e) : ~0u;
         }
         warp_bitonic_sort<K>(ck, lane);
-        // class boundaries as a bitmask over positions
-        uint32_t bw[K];
+        uint32_t bnd[K];
+        uint32_t ncls_total = 0;
 #pragma unroll
         for (int k = 0; k < K; k++) {
             uint32_t prev = __shfl_up_sync(FULL, ck[k], 1);
-            const uint32_t pk = k > 0 ? __shfl_sync(FULL, ck[k > 0 ? k - 1 : 0], 31) : ~0u;
-            if (lane == 0) prev = pk;
+            const uint32_t pk = __shfl_sync(FULL, ck[k > 0 ? k - 1 : 0], 31);
+            if (lane == 0) prev = k > 0 ? pk : ~0u;
             const bool valid = ck[k] != ~0u;
-            bw[k] = __ballot_sync(FULL, valid && (prev == ~0u || (prev >> 10) != (ck[k] >> 10)));
+            bnd[k] = __ballot_sync(FULL, valid && (prev == ~0u || (prev >> 10) != (ck[k] >> 10)));
+            ncls_total += __popc(bnd[k]);
         }
+        if (ncls_total > L.cm_per_trace) {
+            fail = 1;
+        } else {
+            for (uint32_t i = lane; i < ncls_total * NW; i += 32) cm[i] = 0ull;
+            __syncwarp();
+            uint32_t before = 0;  // classes starting before word k
+#pragma unroll
+            for (int k = 0; k < K; k++) {
+                if (ck[k] != ~0u) {
+                    const uint32_t ci = before + __popc(bnd[k] & ((2u << lane) - 1u)) - 1u;
+                    const uint32_t apos = ck[k] & 0x3FFu;
+                    atomicOr(reinterpret_cast<unsigned long long*>(&cm[ci * NW + (apos >> 6)]),
+                             1ull << (apos & 63u));
+                }
+                before += __popc(bnd[k]);
+            }
+            // class-index bounds per device
+            uint32_t nc_d = 0;
+            for (uint32_t d = 0; d < ndev; d++) {
+                uint32_t c = 0;
+#pragma unroll
+                for (int k = 0; k < K; k++)
+                    c += __popc(bnd[k] & __ballot_sync(FULL, ck[k] != ~0u && (ck[k] >> 18) == d));
+                if (lane == d) nc_d = c;
+            }
+            const uint32_t cincl = dev_scan_incl(nc_d, lane);
+            if (lane < ndev) meta[20 + lane] = (uint16_t)cincl;
+        }
+    }
+    if (L.need_tbl) {
+        // fit table: requests ascending; T[r] = positions of the r smallest
+        uint32_t* s_smem = reinterpret_cast<uint32_t*>(ws + L.off_smem) + g * SS::SRT;
+        uint32_t* s_fen = reinterpret_cast<uint32_t*>(ws + L.off_fen) + g * SS::FEN;
+        uint64_t* s_tbl = reinterpret_cast<uint64_t*>(ws + L.off_tbl) + g * SS::T64;
+        uint64_t mk[K];
 #pragma unroll
         for (int k = 0; k < K; k++) {
-            if (ck[k] != ~0u) {
-                const uint32_t c = (uint32_t)k * 32u + lane;
-                uint32_t cend = na;
-                bool found = false;
-                const uint32_t above = lane == 31 ? 0u : (bw[k] & ~((2u << lane) - 1u));
-                if (above) { cend = (uint32_t)k * 32u + __ffs(above) - 1; found = true; }
+            const uint32_t e = (uint32_t)k * 32u + lane;
+            mk[k] = memk[k] != ~0u ? (((uint64_t)memk[k] << 8) | e) : kInf;
+        }
+        warp_bitonic_sort<K>(mk, lane);
+        uint64_t carry = 0;
 #pragma unroll
-                for (int k2 = k + 1; k2 < K; k2++)
-                    if (!found && bw[k2]) { cend = (uint32_t)k2 * 32u + __ffs(bw[k2]) - 1; found = true; }
-                const uint32_t apos = ck[k] & 0x3FFu;
-                cls[c] = apos | (cend << 16);
-                cpos[apos] = (uint16_t)c;
+        for (int k = 0; k < K; k++) {
+            const uint32_t r = (uint32_t)k * 32u + lane;
+            const uint32_t sm = mk[k] != kInf ? (uint32_t)(mk[k] >> 8) : ~0u;
+            s_smem[r] = sm;
+            if ((r & 7u) == 7u) s_fen[r >> 3] = sm;
+            if (r < 8) s_smem[N + r] = ~0u;
+            uint64_t v = mk[k] != kInf ? (1ull << ((uint32_t)mk[k] & 63u)) : 0ull;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t u = shfl_up_u64(v, o);
+                if (lane >= (uint32_t)o) v |= u;
             }
+            v |= carry;
+            s_tbl[r + 1] = v;
+            carry = __shfl_sync(FULL, (uint32_t)v, 31) | ((uint64_t)__shfl_sync(FULL, (uint32_t)(v >> 32), 31) << 32);
         }
-        __syncwarp();
-    }
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-        const uint32_t e = (uint32_t)k * 32u + lane;
-        if (key[k] != kInf) {
-            const uint32_t i = (uint32_t)key[k] & kAppMask;
-            const uint4 f = raw[i];
-            const uint32_t cp = L.need_cls ? cpos[e] : 0u;
-            rec[e] = make_uint4(f.x, f.y, f.z, i | (cp << 10) | ((f.w & 0xFFu) << 20));
-        }
-    }
-    // meta: exclusive scan of the device counts
-    uint32_t incl = cnt_d;
-#pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(FULL, incl, o);
-        if (lane >= (uint32_t)o) incl += v;
+        if (lane == 0) s_tbl[0] = 0ull;
     }
     if (lane < ndev) {
-        meta[3 + lane] = (uint16_t)incl;
+        meta[3 + lane] = (uint16_t)dincl;
         meta[11 + lane] = (uint16_t)z_d;
     }
     if (lane == 0) {
         meta[0] = (uint16_t)na;
-        meta[1] = big ? 1 : 0;
+        meta[1] = (uint16_t)fail;
         meta[2] = 0;
+        meta[19] = 0;
     }
     __syncwarp();
 }
 
-// Block = one warp per requested policy; the block stages G = 32 / ndev
-// traces at a time into shared memory (the warps split the traces), then
-// warp w simulates policy w of all of them, lane = (trace slot, device).
-// Every lane of a warp runs the same policy, so their control flow differs
-// only by the trace data.
 template <int K>
-__global__ void __launch_bounds__(128) trace_sim_lane_kernel(const LaneParams L) {
+__global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel(const LaneParams L) {
     const SimParams& P = L.sp;
     constexpr uint32_t N = 32u * K;
+    constexpr uint32_t NW = (N + 63u) / 64u;
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
-    const uint32_t npol = P.npol;
-    const uint32_t ndev = P.ndev;
-    uint8_t* fb = smem + L.off_fb + (size_t)warp * L.fb_bytes;
+    uint8_t* ws = smem + (size_t)warp * L.warp_bytes;
     const uint64_t n_groups = (P.n_traces + L.G - 1) / L.G;
+    const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    const uint32_t ndev = P.ndev;
 
-    // lane -> (slot, device); warp -> policy slot
-    const uint32_t g = lane / ndev;
-    const uint32_t d = lane - g * ndev;
-    const uint32_t pslot = warp;
+    // lane -> (slot, device, policy slot)
+    const uint32_t g = lane / L.lpt;
+    const uint32_t rem = lane - g * L.lpt;
+    const uint32_t d = rem / P.npol;
+    const uint32_t pslot = rem - d * P.npol;
     const uint32_t policy = (P.policy_list >> (4 * pslot)) & 0xFu;
     uint32_t cap_d = P.cap[0];
 #pragma unroll
     for (uint32_t j = 1; j < SG_MAX_DEV; j++)
         if (d == j) cap_d = P.cap[j];
 
-    for (uint64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+    for (uint64_t grp = gw; grp < n_groups; grp += stride) {
         const uint64_t t0 = grp * L.G;
         const uint32_t gcount = (uint32_t)min((uint64_t)L.G, P.n_traces - t0);
-        for (uint32_t s = warp; s < gcount; s += npol) stage_trace<K>(L, smem, fb, s, t0 + s, lane);
+        for (uint32_t s = 0; s < gcount; s++) stage_trace<K>(L, ws, s, t0 + s, lane);
         // warm L2 with the next group's records while this one simulates
-        if (warp == 0 && grp + gridDim.x < n_groups && !P.trace_offsets) {
-            const uint64_t nt0 = (grp + gridDim.x) * L.G;
+        if (grp + stride < n_groups && !P.trace_offsets) {
+            const uint64_t nt0 = (grp + stride) * L.G;
             const uint64_t nb = min((uint64_t)L.G, P.n_traces - nt0) * P.apps_per_trace * 16u;
             const uint8_t* base = reinterpret_cast<const uint8_t*>(P.apps + nt0 * P.apps_per_trace);
             for (uint64_t off = (uint64_t)lane * 128u; off < nb; off += 32u * 128u) prefetch_l2(base + off);
         }
-        __syncthreads();
 
         bool fail = false;
         if (g < gcount) {
             const uint64_t t = t0 + g;
-            const uint16_t* meta = reinterpret_cast<const uint16_t*>(smem + L.off_meta) + g * kMetaU16;
+            const uint16_t* meta = reinterpret_cast<const uint16_t*>(ws + L.off_meta) + g * kMetaU16;
             const uint32_t na = meta[0];
             if (meta[1]) {
                 fail = true;
@@ -535,9 +694,19 @@ __global__ void __launch_bounds__(128) trace_sim_lane_kernel(const LaneParams L)
                 uint32_t na_unused;
                 lane_trace_range(P, t, a0, na_unused);
                 LaneSim<K> sim(P);
-                sim.rec = reinterpret_cast<const uint4*>(smem + L.off_rec) + g * N;
-                sim.cls = reinterpret_cast<const uint32_t*>(smem + L.off_cls) + g * N;
-                sim.heap = reinterpret_cast<uint64_t*>(fb) + lane;
+                using SS = SlotStride<N>;
+                sim.s_a = reinterpret_cast<const uint32_t*>(ws + L.off_a) + g * SS::S32;
+                sim.s_mem = reinterpret_cast<const uint32_t*>(ws + L.off_mem) + g * SS::S32;
+                sim.s_bw = reinterpret_cast<const uint32_t*>(ws + L.off_bw) + g * SS::S32;
+                sim.s_smem = reinterpret_cast<const uint32_t*>(ws + L.off_smem) + g * SS::SRT;
+                sim.s_fen = reinterpret_cast<const uint32_t*>(ws + L.off_fen) + g * SS::FEN;
+                sim.s_tbl = reinterpret_cast<const uint64_t*>(ws + L.off_tbl) + g * SS::T64;
+                uint32_t c0 = 0, c1 = 0;
+                if (L.need_cls) { c0 = meta[19 + d]; c1 = meta[20 + d]; }
+                sim.s_cm = reinterpret_cast<const uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW + 1) + c0 * NW;
+                sim.ncls = c1 - c0;
+                sim.heap = reinterpret_cast<uint64_t*>(ws + L.off_fb) + lane;
+                sim.fifo = reinterpret_cast<uint32_t*>(ws + L.off_fifo) + lane;
                 sim.out_base = (uint64_t)pslot * P.n_apps_total + a0;
                 if (sim.run(na, s0, s1, z, policy, cap_d))
                     sim.finish(((uint64_t)pslot * P.n_traces + t) * ndev + d, s1 - s0);
@@ -549,12 +718,15 @@ __global__ void __launch_bounds__(128) trace_sim_lane_kernel(const LaneParams L)
         // exact fallback: the whole warp re-simulates each failed lane
         for (uint32_t fm = __ballot_sync(FULL, fail); fm; fm &= fm - 1) {
             const uint32_t fl = __ffs(fm) - 1;
-            const uint32_t fg = fl / ndev;
-            const uint32_t fd = fl - fg * ndev;
+            const uint32_t fg = fl / L.lpt;
+            const uint32_t frem = fl - fg * L.lpt;
+            const uint32_t fd = frem / P.npol;
+            const uint32_t fp = frem - fd * P.npol;
             const uint64_t t = t0 + fg;
             uint64_t a0;
             uint32_t na;
             lane_trace_range(P, t, a0, na);
+            uint8_t* fb = ws + L.off_fb;
             uint4* apps_s = reinterpret_cast<uint4*>(fb + P.off_app);
             for (uint32_t i = lane; i < na; i += 32)
                 apps_s[i] = __ldg(reinterpret_cast<const uint4*>(P.apps + a0) + i);
@@ -574,11 +746,11 @@ __global__ void __launch_bounds__(128) trace_sim_lane_kernel(const LaneParams L)
             for (uint32_t j = 1; j < SG_MAX_DEV; j++)
                 if (fd == j) fcap = P.cap[j];
             TraceSim<TickTM, K, false> sim(P, lane, fb, sub);
-            sim.run(nd, policy, fcap, nullptr);
-            sim.finish(((uint64_t)pslot * P.n_traces + t) * ndev + fd,
-                       (uint64_t)pslot * P.n_apps_total + a0, idx, nullptr);
+            sim.run(nd, (P.policy_list >> (4 * fp)) & 0xFu, fcap, nullptr);
+            sim.finish(((uint64_t)fp * P.n_traces + t) * ndev + fd, (uint64_t)fp * P.n_apps_total + a0,
+                       idx, nullptr);
         }
-        __syncthreads();
+        __syncwarp();
     }
 }
 
@@ -586,30 +758,31 @@ static inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
 // Lane path eligibility: T0 ticks mode, no event log, <= 256 apps per trace.
 bool lane_eligible(const SimParams& p, bool program_mode, bool f64) {
-    return !program_mode && !f64 && p.events == nullptr && p.n_pad <= 256 && p.npol <= 4 &&
-           p.ndev <= 32;
+    return !program_mode && !f64 && p.events == nullptr && p.n_pad <= 256 &&
+           p.npol * p.ndev <= 32;
 }
 
 template <int K>
 static cudaError_t launch_lane_t(LaneParams& L, cudaStream_t stream, int* grid_out) {
     auto kern = trace_sim_lane_kernel<K>;
-    const uint32_t threads = 32u * L.sp.npol;
-    const size_t smem = L.block_bytes;
+    const uint32_t wpb = kLaneWarpsPerBlock;
+    const size_t smem = (size_t)L.warp_bytes * wpb;
     if (smem > 227u * 1024u) return cudaErrorInvalidConfiguration;
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, smem);
     if (err != cudaSuccess) return err;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const uint64_t groups = (L.sp.n_traces + L.G - 1) / L.G;
+    const uint64_t need = (groups + wpb - 1) / wpb;
     uint64_t grid = (uint64_t)sms * per_sm;
-    if (groups < grid) grid = groups;
+    if (need < grid) grid = need;
     if (grid == 0) grid = 1;
     if (grid_out) *grid_out = (int)grid;
-    kern<<<(unsigned)grid, threads, smem, stream>>>(L);
+    kern<<<(unsigned)grid, wpb * 32, smem, stream>>>(L);
     return cudaGetLastError();
 }
 
@@ -617,26 +790,46 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
     LaneParams L;
     L.sp = p;
     const uint32_t N = p.n_pad;
-    L.G = 32u / p.ndev;
+    const uint32_t NW = (N + 63u) / 64u;
+    L.lpt = p.npol * p.ndev;
+    L.G = 32u / L.lpt;
     L.need_cls = 0;
-    for (uint32_t i = 0; i < p.npol; i++)
-        if (((p.policy_list >> (4 * i)) & 0xFu) >= SG_POLICY_PFIFO) L.need_cls = 1;
-    // per-warp region: heap / staging scratch / fallback TraceSim layout (relative to it)
+    bool any_mmu = false;
+    for (uint32_t i = 0; i < p.npol; i++) {
+        const uint32_t pol = (p.policy_list >> (4 * i)) & 0xFu;
+        if (pol >= SG_POLICY_PFIFO) L.need_cls = 1;
+        if (pol & 1u) any_mmu = true;
+    }
+    L.need_tbl = (any_mmu && N <= 64) ? 1u : 0u;
+    L.cm_per_trace = max(kLaneClassMasks / L.G, 8u);
+    // per-warp region: busy-end heap / staging scratch / fallback TraceSim
     sim_layout(L.sp, false, false);
     uint32_t fb = L.sp.warp_bytes;
     fb = max(fb, kLaneHeap * 32u * 8u);
-    fb = max(fb, N * 16u + N * 2u);
-    L.fb_bytes = align16(fb);
+    fb = max(fb, N * 16u);
+    const uint32_t S32 = N + 4, SRT = N + 12, FEN = N / 8 + 4, T64 = N + 2;  // SlotStride<N>
     uint32_t o = 0;
-    L.off_rec = o;
-    o = align16(o + L.G * N * 16u);
-    L.off_cls = o;
-    o = align16(o + (L.need_cls ? L.G * N * 4u : 0u));
+    L.off_a = o;
+    o = align16(o + L.G * S32 * 4u);
+    L.off_mem = o;
+    o = align16(o + L.G * S32 * 4u);
+    L.off_bw = o;
+    o = align16(o + L.G * S32 * 4u);
+    L.off_smem = o;
+    o = align16(o + (L.need_tbl ? L.G * SRT * 4u : 0u));
+    L.off_fen = o;
+    o = align16(o + (L.need_tbl ? L.G * FEN * 4u : 0u));
+    L.off_tbl = o;
+    o = align16(o + (L.need_tbl ? L.G * T64 * 8u : 0u));
+    L.off_cm = o;
+    o = align16(o + (L.need_cls ? L.G * (L.cm_per_trace * NW + 1) * 8u : 0u));
     L.off_meta = o;
     o = align16(o + L.G * kMetaU16 * 2u);
+    L.off_fifo = o;
+    o = align16(o + kLaneFifoWords * 32u * 4u);
     L.off_fb = o;
-    o += L.fb_bytes * p.npol;
-    L.block_bytes = o;
+    o = align16(o + fb);
+    L.warp_bytes = o;
     switch (N / 32) {
         case 1: return launch_lane_t<1>(L, stream, grid_out);
         case 2: return launch_lane_t<2>(L, stream, grid_out);
