@@ -259,6 +259,54 @@ struct LaneSim {
 
     // grant_waiters (harness.py:545-558) + select_grants (policy.py:52-74)
     __device__ __forceinline__ void grant_waiters() {
+        if constexpr (TBL) grant_waiters_tbl();
+        else grant_waiters_scan();
+    }
+
+    // <= 64 apps: one code path for all four kinds, so the lanes of a warp
+    // (mixed policies) stay converged.  Per round: the top class (all
+    // waiting entries for FIFO/MMU); per grant: fit = class & T[#requests <=
+    // budget]; FIFO takes the head iff it fits, MMU the lowest fit; both
+    // continue above the granted position.
+    __device__ __forceinline__ void grant_waiters_tbl() {
+        const uint32_t nc = prio_pol ? ncls : 1u;
+        uint32_t c = 0;
+        while (true) {
+            uint64_t cm = ~0ull, cand = 0;
+            while (c < nc) {
+                cm = prio_pol ? s_cm[c] : ~0ull;
+                cand = mask[0] & cm;
+                if (cand) break;
+                c += 1;
+            }
+            if (!cand) return;
+            const uint32_t budget0 = cap - used;
+            uint32_t budget = budget0, g = 0;
+            while (cand) {
+                const uint64_t fit = cand & s_tbl[fit_rank(budget)];
+                const uint64_t head = cand & (0ull - cand);
+                const uint64_t pick = mmu ? fit : (fit & head);
+                if (!pick) break;
+                const uint32_t q = ffs64(pick);
+                grant_one(q, s_mem[q], budget, g);
+                if (fail) return;
+                cand &= ~((2ull << q) - 1ull);
+            }
+            if (g) {
+                mem_point(last);
+                used += budget0 - budget;
+                holders += (int32_t)g;
+                maxh = max(maxh, (uint32_t)holders);
+                grants += g;
+            }
+            // the top class continues only if it drained (harness.py:547-550)
+            if (!prio_pol || g == 0 || (mask[0] & cm) != 0) return;
+            c += 1;
+        }
+    }
+
+    // longer traces: scan the candidates in queue order
+    __device__ __forceinline__ void grant_waiters_scan() {
         uint32_t c = 0;  // current class (priority kinds)
         while (true) {
             // candidate set: the waiting entries of the top class (policy.py:58-63)
@@ -284,34 +332,20 @@ struct LaneSim {
             if (!any) return;
             const uint32_t budget0 = cap - used;
             uint32_t budget = budget0, g = 0;
-            if (mmu && TBL) {
-                // first fit with a shrinking budget: lowest waiting position
-                // among the requests that fit
-                uint64_t fit = cand[0] & s_tbl[fit_rank(budget)];
-                while (fit) {
-                    const uint32_t q = ffs64(fit);
-                    const uint32_t m = s_mem[q];
-                    grant_one(q, m, budget, g);
-                    if (fail) return;
-                    cand[0] &= ~(1ull << q);
-                    fit = budget ? (cand[0] & s_tbl[fit_rank(budget)] & ~((2ull << q) - 1ull)) : 0ull;
-                }
-            } else {
-                // FIFO: grant the head while it fits; MMU (long traces): skip misfits
-                bool stop = false;
+            // FIFO: grant the head while it fits; MMU: skip misfits
+            bool stop = false;
 #pragma unroll
-                for (uint32_t w = 0; w < NW; w++) {
-                    uint64_t bits = cand[w];
-                    while (bits && !stop) {
-                        const uint32_t q = 64u * w + ffs64(bits);
-                        bits &= bits - 1;
-                        const uint32_t m = s_mem[q];
-                        if (m <= budget) {
-                            grant_one(q, m, budget, g);
-                            if (fail) return;
-                        } else if (!mmu) {
-                            stop = true;
-                        }
+            for (uint32_t w = 0; w < NW; w++) {
+                uint64_t bits = cand[w];
+                while (bits && !stop) {
+                    const uint32_t q = 64u * w + ffs64(bits);
+                    bits &= bits - 1;
+                    const uint32_t m = s_mem[q];
+                    if (m <= budget) {
+                        grant_one(q, m, budget, g);
+                        if (fail) return;
+                    } else if (!mmu) {
+                        stop = true;
                     }
                 }
             }
@@ -323,11 +357,11 @@ struct LaneSim {
                 grants += g;
             }
             if (!prio_pol || g == 0) return;
-            // the top class continues only if it drained (harness.py:547-550)
             bool left = false;
 #pragma unroll
             for (uint32_t w = 0; w < NW; w++) left = left || (mask[w] & s_cm[c * NW + w]) != 0;
             if (left) return;
+            c += 1;
         }
     }
 
@@ -404,16 +438,20 @@ struct LaneSim {
             ka = ((uint64_t)s_a[ap] << 32) | (((bwa >> kBusyBits) << LOGN) << 8) | ap;
         }
         while (true) {
+            // next event: a granted waiter resumes after every other entry of
+            // its tick; otherwise the smaller of the arrival / busy-end keys
             const uint64_t kmin = ka < kh ? ka : kh;
-            if (fhead != ftail && (kmin >> 32) > last) {
-                // granted waiters resume after every other entry of their tick
-                const uint32_t q = unwake();
-                pops += 1;
-                run_from_busy(q, s_mem[q], s_bw[q], last);
-            } else if (ka < kh) {
-                const uint32_t q = ap;
-                const uint32_t now = (uint32_t)(ka >> 32);
-                const uint32_t bw = bwa;
+            const bool is_wake = fhead != ftail && (kmin >> 32) > last;
+            if (!is_wake && kmin == kInf) break;
+            const bool is_arr = !is_wake && ka < kh;
+            const bool is_end = !is_wake && !is_arr;
+            const uint32_t fslot = fhead % kLaneFifo;
+            const uint32_t fq = (fifo[(fslot >> 2) * 32] >> ((fslot & 3u) * 8u)) & 0xFFu;
+            const uint32_t q = is_wake ? fq : (uint32_t)kmin & 0xFFu;
+            const uint32_t now = is_wake ? last : (uint32_t)(kmin >> 32);
+            if (is_end) pop();
+            if (is_wake) fhead += 1;
+            if (is_arr) {
                 ap += 1;
                 if (ap < e) {
                     bwa = s_bw[ap];
@@ -421,21 +459,30 @@ struct LaneSim {
                 } else {
                     ka = kInf;
                 }
-                pops += 1;
-                last = now;
-                arrive(q, s_mem[q], bw, now);
-            } else if (kh != kInf) {
-                const uint64_t key = kh;
-                pop();
-                const uint32_t q = (uint32_t)key & 0xFFu;
-                const uint32_t now = (uint32_t)(key >> 32);
-                pops += 1;
-                last = now;
-                busy_point(now, -1);
-                end_app(s_mem[q], s_bw[q], now);
-            } else {
-                break;
             }
+            const uint32_t m = s_mem[q];
+            const uint32_t bw = s_bw[q];
+            const uint32_t b = bw & ((1u << kBusyBits) - 1u);
+            pops += 1;
+            last = now;
+            // arrival: memory-fit admission with bypass, else wait (harness.py:521-536)
+            const bool alloc = is_arr && m != 0;
+            const bool fits = m <= cap - used;
+            const bool enq = alloc && !fits;
+            if (enq) enqueue(q);
+            mem_point(now);
+            if (alloc && fits) {
+                used += m;
+                holders += 1;
+                maxh = max(maxh, (uint32_t)holders);
+                grants += 1;
+            }
+            // busy (harness.py:514-520) or its end
+            const bool to_busy = !is_end && !enq;
+            const bool start = to_busy && b != 0;
+            busy_point(now, start ? 1 : (is_end ? -1 : 0));
+            if (start) push(now + b, q);
+            if ((to_busy && b == 0) || is_end) end_app(m, bw, now);
             if (fail) return false;
         }
         return true;
@@ -794,13 +841,11 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
     L.lpt = p.npol * p.ndev;
     L.G = 32u / L.lpt;
     L.need_cls = 0;
-    bool any_mmu = false;
     for (uint32_t i = 0; i < p.npol; i++) {
         const uint32_t pol = (p.policy_list >> (4 * i)) & 0xFu;
         if (pol >= SG_POLICY_PFIFO) L.need_cls = 1;
-        if (pol & 1u) any_mmu = true;
     }
-    L.need_tbl = (any_mmu && N <= 64) ? 1u : 0u;
+    L.need_tbl = N <= 64 ? 1u : 0u;  // all kinds use the fit table on short traces
     L.cm_per_trace = max(kLaneClassMasks / L.G, 8u);
     // per-warp region: busy-end heap / staging scratch / fallback TraceSim
     sim_layout(L.sp, false, false);
