@@ -399,7 +399,7 @@ def main():
             "aggregate": aggd,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                         "kernel": "trace_sim_kernel", "alg_bytes_per_launch": alg_bytes,
+                         "kernel": os.environ.get("SGPU_K1_NAME", "trace_sim_lane_kernel"), "alg_bytes_per_launch": alg_bytes,
                          "mean_launch_ms": mean_k * 1000.0},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }

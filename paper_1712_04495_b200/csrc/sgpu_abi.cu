@@ -124,7 +124,7 @@ static int simulate_device(const sg_batch* in, const sg_out* out, cudaStream_t s
     const char* eng = getenv("SGPU_K1");
     const bool want_warp = eng && strcmp(eng, "warp") == 0;
     const bool want_lane = eng && strcmp(eng, "lane") == 0;
-    const bool lane_ok = sg::lane_eligible(p, s.program, s.f64);
+    const bool lane_ok = sg::lane_eligible(p, s.program, s.f64, want_lane);
     if (want_lane && !lane_ok) return fail(E_ARG, "SGPU_K1=lane: batch not eligible for the lane kernel");
     cudaError_t e;
     if (lane_ok && !want_warp) {

@@ -46,7 +46,7 @@ cudaError_t launch_sim(const SimParams& p, bool program_mode, bool f64, cudaStre
 
 // K1 v4: lane-per-(trace, device, policy) kernel for T0 tick-mode batches
 // (sgpu_lane.cu), with an in-kernel exact fallback to TraceSim.
-bool lane_eligible(const SimParams& p, bool program_mode, bool f64);
+bool lane_eligible(const SimParams& p, bool program_mode, bool f64, bool forced);
 cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_out);
 
 cudaError_t launch_reduce(const sg_trace_stats* stats, uint64_t count, sg_aggr* out,

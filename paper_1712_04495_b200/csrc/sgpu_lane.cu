@@ -57,7 +57,7 @@ struct LaneParams {
     uint32_t need_tbl;     // an MMU-type policy on <= 64-app traces: build the fit table
     uint32_t cm_per_trace; // class-mask capacity of one trace slot
     // per-warp shared-memory layout (bytes)
-    uint32_t off_a, off_mem, off_bw, off_smem, off_fen, off_tbl, off_cm, off_meta, off_fifo, off_fb,
+    uint32_t off_a, off_mem, off_bw, off_smem, off_lt, off_tbl, off_cm, off_meta, off_fifo, off_fb,
         warp_bytes;
 };
 
@@ -67,13 +67,13 @@ struct LaneParams {
 template <uint32_t N> struct SlotStride {
     static constexpr uint32_t S32 = N + 4;          // u32 record arrays
     static constexpr uint32_t SRT = N + 8 + 4;      // sorted requests (+8: rank-search pad block)
-    static constexpr uint32_t FEN = N / 8 + 4;      // fences: every 8th sorted request
+    static constexpr uint32_t LTB = 80;             // rank lookup: 64 u8 buckets (+16 B skew)
     static constexpr uint32_t T64 = N + 2;          // fit table (N + 1 entries)
 };
 
 // meta per trace slot (u16): [0] n, [1] fail (big times / too many classes),
 // [2..10] device bounds in arrival order, [11..18] apps arriving at t = 0 per
-// device, [19..27] class-mask index bounds per device
+// device, [19..27] class-mask index bounds per device, [28] rank-lookup shift
 constexpr uint32_t kMetaU16 = 32;
 
 __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
@@ -142,7 +142,8 @@ struct LaneSim {
     const uint32_t* s_mem;   // request MiB
     const uint32_t* s_bw;    // busy | app << kBusyBits
     const uint32_t* s_smem;  // requests sorted ascending (padded with ~0 to N + 8)
-    const uint32_t* s_fen;   // s_fen[i] = s_smem[8i + 7]
+    const uint8_t* s_lt;     // s_lt[j] = #requests < j << lt_shift (64 buckets)
+    uint32_t lt_shift;
     const uint64_t* s_tbl;   // T[r]: positions of the r smallest requests
     const uint64_t* s_cm;    // class masks of this lane's device, top class first
     uint32_t ncls;
@@ -234,19 +235,15 @@ struct LaneSim {
         for (uint32_t w = 0; w < NW; w++)
             if (w == (q >> 6)) mask[w] |= 1ull << (q & 63u);
     }
-    // number of requests <= budget in the trace: two 8-ary levels of 16-byte
-    // loads (fences, then one block of 8 sorted requests)
+    // number of requests <= budget in the trace: bucket lookup (64 power-of-2
+    // buckets spanning the trace's largest request), then a short forward
+    // scan of the sorted requests inside the bucket
     __device__ __forceinline__ uint32_t fit_rank(uint32_t budget) const {
-        uint32_t j = 0;
-#pragma unroll
-        for (uint32_t i = 0; i < N / 32; i++) {
-            const uint4 f = reinterpret_cast<const uint4*>(s_fen)[i];
-            j += (f.x <= budget) + (f.y <= budget) + (f.z <= budget) + (f.w <= budget);
-        }
-        const uint4* blk = reinterpret_cast<const uint4*>(s_smem + 8 * j);
-        const uint4 u0 = blk[0], u1 = blk[1];
-        return 8 * j + (u0.x <= budget) + (u0.y <= budget) + (u0.z <= budget) + (u0.w <= budget) +
-               (u1.x <= budget) + (u1.y <= budget) + (u1.z <= budget) + (u1.w <= budget);
+        const uint32_t bi = budget >> lt_shift;
+        if (bi >= 64u) return N;
+        uint32_t r = s_lt[bi];
+        while (s_smem[r] <= budget) r += 1;
+        return r;
     }
     __device__ __forceinline__ void grant_one(uint32_t q, uint32_t m, uint32_t& budget, uint32_t& g) {
 #pragma unroll
@@ -554,7 +551,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
         const uint32_t i = (uint32_t)k * 32u + lane;
         key[k] = kInf;
         if (i < na) {
-            const uint4 f = __ldg(reinterpret_cast<const uint4*>(P.apps + a0) + i);
+            const uint4 f = ldg_stream(reinterpret_cast<const uint4*>(P.apps + a0) + i, l2_policy_evict_first());
             raw[i] = f;
             uint32_t dv = ndev > 1 ? (f.w >> 8) & 0xFFu : 0u;
             if (dv >= ndev) dv = 0;
@@ -649,7 +646,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
     if (L.need_tbl) {
         // fit table: requests ascending; T[r] = positions of the r smallest
         uint32_t* s_smem = reinterpret_cast<uint32_t*>(ws + L.off_smem) + g * SS::SRT;
-        uint32_t* s_fen = reinterpret_cast<uint32_t*>(ws + L.off_fen) + g * SS::FEN;
+        uint8_t* s_lt = ws + L.off_lt + g * SS::LTB;
         uint64_t* s_tbl = reinterpret_cast<uint64_t*>(ws + L.off_tbl) + g * SS::T64;
         uint64_t mk[K];
 #pragma unroll
@@ -664,7 +661,6 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
             const uint32_t r = (uint32_t)k * 32u + lane;
             const uint32_t sm = mk[k] != kInf ? (uint32_t)(mk[k] >> 8) : ~0u;
             s_smem[r] = sm;
-            if ((r & 7u) == 7u) s_fen[r >> 3] = sm;
             if (r < 8) s_smem[N + r] = ~0u;
             uint64_t v = mk[k] != kInf ? (1ull << ((uint32_t)mk[k] & 63u)) : 0ull;
 #pragma unroll
@@ -677,6 +673,26 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
             carry = __shfl_sync(FULL, (uint32_t)v, 31) | ((uint64_t)__shfl_sync(FULL, (uint32_t)(v >> 32), 31) << 32);
         }
         if (lane == 0) s_tbl[0] = 0ull;
+        // rank lookup buckets: j << shift for j < 64 covers [0, largest request]
+        uint32_t mx = 0;
+#pragma unroll
+        for (int k = 0; k < K; k++) mx = max(mx, memk[k] != ~0u ? memk[k] : 0u);
+        mx = __reduce_max_sync(FULL, mx);
+        const uint32_t bits = 32u - __clz(mx);
+        const uint32_t shift = bits > 6u ? bits - 6u : 0u;
+        __syncwarp();
+#pragma unroll
+        for (uint32_t h = 0; h < 2; h++) {
+            const uint32_t j = h * 32u + lane;
+            const uint32_t x = j << shift;
+            uint32_t r = 0;  // #requests < x
+#pragma unroll
+            for (uint32_t step = N / 2; step > 0; step >>= 1)
+                if (s_smem[r + step - 1] < x) r += step;
+            r += s_smem[r] < x ? 1u : 0u;
+            s_lt[j] = (uint8_t)r;
+        }
+        if (lane == 0) meta[28] = (uint16_t)shift;
     }
     if (lane < ndev) {
         meta[3 + lane] = (uint16_t)dincl;
@@ -746,7 +762,8 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel
                 sim.s_mem = reinterpret_cast<const uint32_t*>(ws + L.off_mem) + g * SS::S32;
                 sim.s_bw = reinterpret_cast<const uint32_t*>(ws + L.off_bw) + g * SS::S32;
                 sim.s_smem = reinterpret_cast<const uint32_t*>(ws + L.off_smem) + g * SS::SRT;
-                sim.s_fen = reinterpret_cast<const uint32_t*>(ws + L.off_fen) + g * SS::FEN;
+                sim.s_lt = ws + L.off_lt + g * SS::LTB;
+                sim.lt_shift = meta[28];
                 sim.s_tbl = reinterpret_cast<const uint64_t*>(ws + L.off_tbl) + g * SS::T64;
                 uint32_t c0 = 0, c1 = 0;
                 if (L.need_cls) { c0 = meta[19 + d]; c1 = meta[20 + d]; }
@@ -804,8 +821,10 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel
 static inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
 // Lane path eligibility: T0 ticks mode, no event log, <= 256 apps per trace.
-bool lane_eligible(const SimParams& p, bool program_mode, bool f64) {
-    return !program_mode && !f64 && p.events == nullptr && p.n_pad <= 256 &&
+// By default only traces of <= 64 apps take it (the fit-table path); longer
+// ones are faster on the warp kernel unless `forced`.
+bool lane_eligible(const SimParams& p, bool program_mode, bool f64, bool forced) {
+    return !program_mode && !f64 && p.events == nullptr && p.n_pad <= (forced ? 256u : 64u) &&
            p.npol * p.ndev <= 32;
 }
 
@@ -852,7 +871,7 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
     uint32_t fb = L.sp.warp_bytes;
     fb = max(fb, kLaneHeap * 32u * 8u);
     fb = max(fb, N * 16u);
-    const uint32_t S32 = N + 4, SRT = N + 12, FEN = N / 8 + 4, T64 = N + 2;  // SlotStride<N>
+    const uint32_t S32 = N + 4, SRT = N + 12, LTB = 80, T64 = N + 2;  // SlotStride<N>
     uint32_t o = 0;
     L.off_a = o;
     o = align16(o + L.G * S32 * 4u);
@@ -862,8 +881,8 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
     o = align16(o + L.G * S32 * 4u);
     L.off_smem = o;
     o = align16(o + (L.need_tbl ? L.G * SRT * 4u : 0u));
-    L.off_fen = o;
-    o = align16(o + (L.need_tbl ? L.G * FEN * 4u : 0u));
+    L.off_lt = o;
+    o = align16(o + (L.need_tbl ? L.G * LTB : 0u));
     L.off_tbl = o;
     o = align16(o + (L.need_tbl ? L.G * T64 * 8u : 0u));
     L.off_cm = o;

@@ -144,6 +144,15 @@ def test_apps_per_trace_shapes(n, cuda):
     check_against_oracle(apps, (184_320,), cuda)
 
 
+@pytest.mark.parametrize("n", [65, 100, 128, 200, 256])
+def test_lane_kernel_long_traces_forced(n, cuda, monkeypatch):
+    """The lane kernel's scan path (65..256 apps; taken only when forced)."""
+    monkeypatch.setenv("SGPU_K1", "lane")
+    g = GenParams(seed=n, apps_per_trace=n, arr_hi=3 * n, mem_lo=1, mem_hi=60_000, prio_levels=5)
+    apps = as_u32x4(generate(g, 0, 64))
+    check_against_oracle(apps, (184_320,), cuda)
+
+
 def test_edge_cases(cuda):
     """Zero fields, stuck oversize requests, simultaneous arrivals, exact fits."""
     rng = np.random.default_rng(3)
