@@ -129,6 +129,11 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 
 __device__ __forceinline__ uint32_t ffs64(uint64_t x) { return (uint32_t)__ffsll((long long)x) - 1u; }
 
+// Rank-lookup bucket of a request d = mem - lo >= 0: monotone in d, 0..63.
+__device__ __forceinline__ uint32_t lt_bucket(uint32_t d, uint32_t scale) {
+    return min((uint32_t)(((uint64_t)d * scale) >> 32), 63u);
+}
+
 template <int K>
 struct LaneSim {
     static constexpr uint32_t N = 32u * K;
@@ -142,8 +147,8 @@ struct LaneSim {
     const uint32_t* s_mem;   // request MiB
     const uint32_t* s_bw;    // busy | app << kBusyBits
     const uint32_t* s_smem;  // requests sorted ascending (padded with ~0 to N + 8)
-    const uint8_t* s_lt;     // s_lt[j] = #requests < j << lt_shift (64 buckets)
-    uint32_t lt_shift;
+    const uint8_t* s_lt;     // s_lt[j] = #requests in buckets < j (64 buckets)
+    uint32_t lt_lo, lt_hi, lt_scale;
     const uint64_t* s_tbl;   // T[r]: positions of the r smallest requests
     const uint64_t* s_cm;    // class masks of this lane's device, top class first
     uint32_t ncls;
@@ -176,13 +181,15 @@ struct LaneSim {
     }
 
     // ------------------------------------------------- busy-end heap
+    // 4-ary min-heap: half the levels of a binary heap, and the four child
+    // loads of a level are independent
     __device__ __forceinline__ void push(uint32_t t, uint32_t q) {
         if (hs >= kLaneHeap) { fail = true; return; }
         const uint64_t key = ((uint64_t)t << 32) | (counter << 8) | q;
         counter += 1;
         uint32_t i = hs++;
         while (i > 0) {
-            const uint32_t par = (i - 1) >> 1;
+            const uint32_t par = (i - 1) >> 2;
             const uint64_t pk = heap[par * 32];
             if (pk < key) break;
             heap[i * 32] = pk;
@@ -198,17 +205,26 @@ struct LaneSim {
         uint32_t i = 0;
         uint64_t top = lastk;
         while (true) {
-            uint32_t c = 2 * i + 1;
+            const uint32_t c = 4 * i + 1;
             if (c >= hs) break;
-            uint64_t ck = heap[c * 32];
-            if (c + 1 < hs) {
-                const uint64_t c2 = heap[(c + 1) * 32];
-                if (c2 < ck) { ck = c2; c += 1; }
-            }
-            if (lastk < ck) break;
-            heap[i * 32] = ck;
-            if (i == 0) top = ck;
-            i = c;
+            uint64_t k0 = heap[c * 32];
+            const uint64_t k1 = c + 1 < hs ? heap[(c + 1) * 32] : kInf;
+            const uint64_t k2 = c + 2 < hs ? heap[(c + 2) * 32] : kInf;
+            const uint64_t k3 = c + 3 < hs ? heap[(c + 3) * 32] : kInf;
+            uint32_t m = c;
+            const bool s01 = k1 < k0;
+            const uint64_t a = s01 ? k1 : k0;
+            const uint32_t ia = s01 ? c + 1 : c;
+            const bool s23 = k3 < k2;
+            const uint64_t b = s23 ? k3 : k2;
+            const uint32_t ib = s23 ? c + 3 : c + 2;
+            const bool sab = b < a;
+            k0 = sab ? b : a;
+            m = sab ? ib : ia;
+            if (lastk < k0) break;
+            heap[i * 32] = k0;
+            if (i == 0) top = k0;
+            i = m;
         }
         heap[i * 32] = lastk;
         kh = top;
@@ -235,12 +251,12 @@ struct LaneSim {
         for (uint32_t w = 0; w < NW; w++)
             if (w == (q >> 6)) mask[w] |= 1ull << (q & 63u);
     }
-    // number of requests <= budget in the trace: bucket lookup (64 power-of-2
-    // buckets spanning the trace's largest request), then a short forward
-    // scan of the sorted requests inside the bucket
+    // number of requests <= budget in the trace: bucket lookup (64 buckets
+    // spread linearly over [smallest, largest] request), then a short
+    // forward scan of the sorted requests inside the bucket
     __device__ __forceinline__ uint32_t fit_rank(uint32_t budget) const {
-        const uint32_t bi = budget >> lt_shift;
-        if (bi >= 64u) return N;
+        if (budget > lt_hi) return N;
+        const uint32_t bi = budget < lt_lo ? 0u : lt_bucket(budget - lt_lo, lt_scale);
         uint32_t r = s_lt[bi];
         while (s_smem[r] <= budget) r += 1;
         return r;
@@ -266,6 +282,7 @@ struct LaneSim {
     // budget]; FIFO takes the head iff it fits, MMU the lowest fit; both
     // continue above the granted position.
     __device__ __forceinline__ void grant_waiters_tbl() {
+        if (!mask[0]) return;
         const uint32_t nc = prio_pol ? ncls : 1u;
         uint32_t c = 0;
         while (true) {
@@ -673,26 +690,38 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
             carry = __shfl_sync(FULL, (uint32_t)v, 31) | ((uint64_t)__shfl_sync(FULL, (uint32_t)(v >> 32), 31) << 32);
         }
         if (lane == 0) s_tbl[0] = 0ull;
-        // rank lookup buckets: j << shift for j < 64 covers [0, largest request]
-        uint32_t mx = 0;
+        // rank lookup: 64 buckets spread linearly over [lo, hi]
+        uint32_t mx = 0, mn = ~0u;
 #pragma unroll
-        for (int k = 0; k < K; k++) mx = max(mx, memk[k] != ~0u ? memk[k] : 0u);
+        for (int k = 0; k < K; k++) {
+            mx = max(mx, memk[k] != ~0u ? memk[k] : 0u);
+            mn = min(mn, memk[k]);
+        }
         mx = __reduce_max_sync(FULL, mx);
-        const uint32_t bits = 32u - __clz(mx);
-        const uint32_t shift = bits > 6u ? bits - 6u : 0u;
+        mn = __reduce_min_sync(FULL, mn);
+        if (mn > mx) mn = mx;  // empty trace
+        const uint64_t sc = (64ull << 32) / ((uint64_t)(mx - mn) + 1ull);
+        const uint32_t scale = sc > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)sc;
         __syncwarp();
 #pragma unroll
         for (uint32_t h = 0; h < 2; h++) {
             const uint32_t j = h * 32u + lane;
-            const uint32_t x = j << shift;
-            uint32_t r = 0;  // #requests < x
+            uint32_t r = 0;  // #requests whose bucket is < j
 #pragma unroll
-            for (uint32_t step = N / 2; step > 0; step >>= 1)
-                if (s_smem[r + step - 1] < x) r += step;
-            r += s_smem[r] < x ? 1u : 0u;
+            for (uint32_t step = N / 2; step > 0; step >>= 1) {
+                const uint32_t v = s_smem[r + step - 1];
+                if (v <= mx && lt_bucket(v - mn, scale) < j) r += step;
+            }
+            const uint32_t v = s_smem[r];
+            r += (v <= mx && lt_bucket(v - mn, scale) < j) ? 1u : 0u;
             s_lt[j] = (uint8_t)r;
         }
-        if (lane == 0) meta[28] = (uint16_t)shift;
+        if (lane == 0) {
+            uint32_t* prm = reinterpret_cast<uint32_t*>(s_lt + 64);
+            prm[0] = mn;
+            prm[1] = mx;
+            prm[2] = scale;
+        }
     }
     if (lane < ndev) {
         meta[3 + lane] = (uint16_t)dincl;
@@ -763,7 +792,9 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel
                 sim.s_bw = reinterpret_cast<const uint32_t*>(ws + L.off_bw) + g * SS::S32;
                 sim.s_smem = reinterpret_cast<const uint32_t*>(ws + L.off_smem) + g * SS::SRT;
                 sim.s_lt = ws + L.off_lt + g * SS::LTB;
-                sim.lt_shift = meta[28];
+                sim.lt_lo = reinterpret_cast<const uint32_t*>(sim.s_lt + 64)[0];
+                sim.lt_hi = reinterpret_cast<const uint32_t*>(sim.s_lt + 64)[1];
+                sim.lt_scale = reinterpret_cast<const uint32_t*>(sim.s_lt + 64)[2];
                 sim.s_tbl = reinterpret_cast<const uint64_t*>(ws + L.off_tbl) + g * SS::T64;
                 uint32_t c0 = 0, c1 = 0;
                 if (L.need_cls) { c0 = meta[19 + d]; c1 = meta[20 + d]; }
