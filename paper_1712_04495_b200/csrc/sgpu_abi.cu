@@ -189,22 +189,35 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
         sg_trace_stats* stats = nullptr;
         double *mem = nullptr, *dev = nullptr;
     } B[NBUF];
+    // Pipeline buffers come from the device's stream-ordered memory pool
+    // (cudaMallocAsync), kept cached between calls: repeated calls pay no
+    // cudaMalloc/cudaFree or implicit device synchronisation.
+    static bool pool_tuned[64] = {false};
+    if (cuda_device >= 0 && cuda_device < 64 && !pool_tuned[cuda_device]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, cuda_device) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        pool_tuned[cuda_device] = true;
+    }
     auto cleanup = [&]() {
         for (auto& b : B) {
-            if (b.st) cudaStreamSynchronize(b.st);
-            cudaFree(b.apps); cudaFree(b.grant); cudaFree(b.end); cudaFree(b.stats);
-            cudaFree(b.mem); cudaFree(b.dev);
-            if (b.st) cudaStreamDestroy(b.st);
+            if (!b.st) continue;
+            cudaFreeAsync(b.apps, b.st); cudaFreeAsync(b.grant, b.st); cudaFreeAsync(b.end, b.st);
+            cudaFreeAsync(b.stats, b.st); cudaFreeAsync(b.mem, b.st); cudaFreeAsync(b.dev, b.st);
+            cudaStreamSynchronize(b.st);
+            cudaStreamDestroy(b.st);
         }
     };
     for (auto& b : B) {
         e = cudaStreamCreateWithFlags(&b.st, cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaMalloc(&b.apps, app_b);
-        if (e == cudaSuccess && out->grant) e = cudaMalloc(&b.grant, tick_b);
-        if (e == cudaSuccess && out->end) e = cudaMalloc(&b.end, tick_b);
-        if (e == cudaSuccess) e = cudaMalloc(&b.stats, st_b);
-        if (e == cudaSuccess && want_pct) e = cudaMalloc(&b.mem, pct_b);
-        if (e == cudaSuccess && want_pct) e = cudaMalloc(&b.dev, pct_b);
+        if (e == cudaSuccess) e = cudaMallocAsync(&b.apps, app_b, b.st);
+        if (e == cudaSuccess && out->grant) e = cudaMallocAsync(&b.grant, tick_b, b.st);
+        if (e == cudaSuccess && out->end) e = cudaMallocAsync(&b.end, tick_b, b.st);
+        if (e == cudaSuccess) e = cudaMallocAsync(&b.stats, st_b, b.st);
+        if (e == cudaSuccess && want_pct) e = cudaMallocAsync(&b.mem, pct_b, b.st);
+        if (e == cudaSuccess && want_pct) e = cudaMallocAsync(&b.dev, pct_b, b.st);
         if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "allocating pipeline buffers"); }
     }
     const uint64_t n_apps_total = N * napps;
