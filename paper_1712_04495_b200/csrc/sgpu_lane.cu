@@ -57,7 +57,7 @@ struct LaneParams {
     uint32_t need_tbl;     // an MMU-type policy on <= 64-app traces: build the fit table
     uint32_t cm_per_trace; // class-mask capacity of one trace slot
     // per-warp shared-memory layout (bytes)
-    uint32_t off_a, off_mem, off_bw, off_smem, off_lt, off_tbl, off_cm, off_meta, off_fifo, off_fb,
+    uint32_t off_a, off_mem, off_bw, off_por, off_lt, off_tbl, off_cm, off_meta, off_fifo, off_fb,
         warp_bytes;
 };
 
@@ -66,9 +66,9 @@ struct LaneParams {
 // a warp (fence / block / table reads) hit disjoint bank groups.
 template <uint32_t N> struct SlotStride {
     static constexpr uint32_t S32 = N + 4;          // u32 record arrays
-    static constexpr uint32_t SRT = N + 8 + 4;      // sorted requests (+8: rank-search pad block)
+    static constexpr uint32_t POR = 80;             // rank -> position (u8, padded)
     static constexpr uint32_t LTB = 80;             // rank lookup: 64 u8 buckets (+16 B skew)
-    static constexpr uint32_t T64 = N + 2;          // fit table (N + 1 entries)
+    static constexpr uint32_t T4 = N / 4 + 2;       // fit table at every 4th rank (N/4 + 1 entries)
 };
 
 // meta per trace slot (u16): [0] n, [1] fail (big times / too many classes),
@@ -146,10 +146,10 @@ struct LaneSim {
     const uint32_t* s_a;     // arrival tick
     const uint32_t* s_mem;   // request MiB
     const uint32_t* s_bw;    // busy | app << kBusyBits
-    const uint32_t* s_smem;  // requests sorted ascending (padded with ~0 to N + 8)
+    const uint8_t* s_por;    // position of the r-th smallest request (N past the end)
     const uint8_t* s_lt;     // s_lt[j] = #requests in buckets < j (64 buckets)
     uint32_t lt_lo, lt_hi, lt_scale;
-    const uint64_t* s_tbl;   // T[r]: positions of the r smallest requests
+    const uint64_t* s_t4;    // T[4j]: positions of the 4j smallest requests
     const uint64_t* s_cm;    // class masks of this lane's device, top class first
     uint32_t ncls;
     // this lane's columns
@@ -258,8 +258,18 @@ struct LaneSim {
         if (budget > lt_hi) return N;
         const uint32_t bi = budget < lt_lo ? 0u : lt_bucket(budget - lt_lo, lt_scale);
         uint32_t r = s_lt[bi];
-        while (s_smem[r] <= budget) r += 1;
+        while (s_mem[s_por[r]] <= budget) r += 1;  // s_mem[N] = ~0 ends the scan
         return r;
+    }
+    // T[r]: positions of the r smallest requests = T[4 floor(r/4)] + up to 3
+    __device__ __forceinline__ uint64_t fit_set(uint32_t r) const {
+        uint64_t t = s_t4[r >> 2];
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(s_por + (r & ~3u));
+        const uint32_t k = r & 3u;
+        if (k > 0) t |= 1ull << (w & 0xFFu);
+        if (k > 1) t |= 1ull << ((w >> 8) & 0xFFu);
+        if (k > 2) t |= 1ull << ((w >> 16) & 0xFFu);
+        return t;
     }
     __device__ __forceinline__ void grant_one(uint32_t q, uint32_t m, uint32_t& budget, uint32_t& g) {
 #pragma unroll
@@ -297,7 +307,7 @@ struct LaneSim {
             const uint32_t budget0 = cap - used;
             uint32_t budget = budget0, g = 0;
             while (cand) {
-                const uint64_t fit = cand & s_tbl[fit_rank(budget)];
+                const uint64_t fit = cand & fit_set(fit_rank(budget));
                 const uint64_t head = cand & (0ull - cand);
                 const uint64_t pick = mmu ? fit : (fit & head);
                 if (!pick) break;
@@ -661,10 +671,11 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
         }
     }
     if (L.need_tbl) {
-        // fit table: requests ascending; T[r] = positions of the r smallest
-        uint32_t* s_smem = reinterpret_cast<uint32_t*>(ws + L.off_smem) + g * SS::SRT;
+        // fit table: requests ascending; T[r] = positions of the r smallest,
+        // kept at every 4th rank plus the rank -> position list
+        uint8_t* s_por = ws + L.off_por + g * SS::POR;
         uint8_t* s_lt = ws + L.off_lt + g * SS::LTB;
-        uint64_t* s_tbl = reinterpret_cast<uint64_t*>(ws + L.off_tbl) + g * SS::T64;
+        uint64_t* s_t4 = reinterpret_cast<uint64_t*>(ws + L.off_tbl) + g * SS::T4;
         uint64_t mk[K];
 #pragma unroll
         for (int k = 0; k < K; k++) {
@@ -672,24 +683,6 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
             mk[k] = memk[k] != ~0u ? (((uint64_t)memk[k] << 8) | e) : kInf;
         }
         warp_bitonic_sort<K>(mk, lane);
-        uint64_t carry = 0;
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-            const uint32_t r = (uint32_t)k * 32u + lane;
-            const uint32_t sm = mk[k] != kInf ? (uint32_t)(mk[k] >> 8) : ~0u;
-            s_smem[r] = sm;
-            if (r < 8) s_smem[N + r] = ~0u;
-            uint64_t v = mk[k] != kInf ? (1ull << ((uint32_t)mk[k] & 63u)) : 0ull;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint64_t u = shfl_up_u64(v, o);
-                if (lane >= (uint32_t)o) v |= u;
-            }
-            v |= carry;
-            s_tbl[r + 1] = v;
-            carry = __shfl_sync(FULL, (uint32_t)v, 31) | ((uint64_t)__shfl_sync(FULL, (uint32_t)(v >> 32), 31) << 32);
-        }
-        if (lane == 0) s_tbl[0] = 0ull;
         // rank lookup: 64 buckets spread linearly over [lo, hi]
         uint32_t mx = 0, mn = ~0u;
 #pragma unroll
@@ -702,26 +695,42 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
         if (mn > mx) mn = mx;  // empty trace
         const uint64_t sc = (64ull << 32) / ((uint64_t)(mx - mn) + 1ull);
         const uint32_t scale = sc > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)sc;
-        __syncwarp();
+        uint64_t carry = 0;
+        uint32_t bcarry = 0;  // bucket of the last rank of the previous row (+1)
 #pragma unroll
-        for (uint32_t h = 0; h < 2; h++) {
-            const uint32_t j = h * 32u + lane;
-            uint32_t r = 0;  // #requests whose bucket is < j
+        for (int k = 0; k < K; k++) {
+            const uint32_t r = (uint32_t)k * 32u + lane;
+            const bool valid = mk[k] != kInf;
+            s_por[r] = valid ? (uint8_t)(mk[k] & 0xFFu) : (uint8_t)N;
+            // prefix OR over ranks: v = T[r + 1]
+            uint64_t v = valid ? (1ull << ((uint32_t)mk[k] & 63u)) : 0ull;
 #pragma unroll
-            for (uint32_t step = N / 2; step > 0; step >>= 1) {
-                const uint32_t v = s_smem[r + step - 1];
-                if (v <= mx && lt_bucket(v - mn, scale) < j) r += step;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t u = shfl_up_u64(v, o);
+                if (lane >= (uint32_t)o) v |= u;
             }
-            const uint32_t v = s_smem[r];
-            r += (v <= mx && lt_bucket(v - mn, scale) < j) ? 1u : 0u;
-            s_lt[j] = (uint8_t)r;
+            v |= carry;
+            if ((r & 3u) == 3u) s_t4[(r + 1) >> 2] = v;
+            carry = __shfl_sync(FULL, (uint32_t)v, 31) | ((uint64_t)__shfl_sync(FULL, (uint32_t)(v >> 32), 31) << 32);
+            // LT[j] = first rank whose bucket is >= j: rank r owns (b[r-1], b[r]]
+            const uint32_t b = valid ? lt_bucket((uint32_t)(mk[k] >> 8) - mn, scale) + 1u : 65u;
+            uint32_t bp = __shfl_up_sync(FULL, b, 1);
+            if (lane == 0) bp = bcarry;
+            for (uint32_t j = bp; j < min(b, 65u); j++)
+                if (j < 64u) s_lt[j] = (uint8_t)r;
+            bcarry = __shfl_sync(FULL, b, 31);
         }
+        // buckets above the largest request (all ranks valid) -> N
+        for (uint32_t j = bcarry + lane; j < 64u; j += 32u) s_lt[j] = (uint8_t)N;
         if (lane == 0) {
+            s_t4[0] = 0ull;
             uint32_t* prm = reinterpret_cast<uint32_t*>(s_lt + 64);
             prm[0] = mn;
             prm[1] = mx;
             prm[2] = scale;
+            s_mem[N] = ~0u;
         }
+        if (lane < 4) s_por[N + lane] = (uint8_t)N;
     }
     if (lane < ndev) {
         meta[3 + lane] = (uint16_t)dincl;
@@ -790,12 +799,12 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel
                 sim.s_a = reinterpret_cast<const uint32_t*>(ws + L.off_a) + g * SS::S32;
                 sim.s_mem = reinterpret_cast<const uint32_t*>(ws + L.off_mem) + g * SS::S32;
                 sim.s_bw = reinterpret_cast<const uint32_t*>(ws + L.off_bw) + g * SS::S32;
-                sim.s_smem = reinterpret_cast<const uint32_t*>(ws + L.off_smem) + g * SS::SRT;
+                sim.s_por = ws + L.off_por + g * SS::POR;
                 sim.s_lt = ws + L.off_lt + g * SS::LTB;
                 sim.lt_lo = reinterpret_cast<const uint32_t*>(sim.s_lt + 64)[0];
                 sim.lt_hi = reinterpret_cast<const uint32_t*>(sim.s_lt + 64)[1];
                 sim.lt_scale = reinterpret_cast<const uint32_t*>(sim.s_lt + 64)[2];
-                sim.s_tbl = reinterpret_cast<const uint64_t*>(ws + L.off_tbl) + g * SS::T64;
+                sim.s_t4 = reinterpret_cast<const uint64_t*>(ws + L.off_tbl) + g * SS::T4;
                 uint32_t c0 = 0, c1 = 0;
                 if (L.need_cls) { c0 = meta[19 + d]; c1 = meta[20 + d]; }
                 sim.s_cm = reinterpret_cast<const uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW + 1) + c0 * NW;
@@ -902,7 +911,7 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
     uint32_t fb = L.sp.warp_bytes;
     fb = max(fb, kLaneHeap * 32u * 8u);
     fb = max(fb, N * 16u);
-    const uint32_t S32 = N + 4, SRT = N + 12, LTB = 80, T64 = N + 2;  // SlotStride<N>
+    const uint32_t S32 = N + 4, POR = 80, LTB = 80, T4 = N / 4 + 2;  // SlotStride<N>
     uint32_t o = 0;
     L.off_a = o;
     o = align16(o + L.G * S32 * 4u);
@@ -910,12 +919,12 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
     o = align16(o + L.G * S32 * 4u);
     L.off_bw = o;
     o = align16(o + L.G * S32 * 4u);
-    L.off_smem = o;
-    o = align16(o + (L.need_tbl ? L.G * SRT * 4u : 0u));
+    L.off_por = o;
+    o = align16(o + (L.need_tbl ? L.G * POR : 0u));
     L.off_lt = o;
     o = align16(o + (L.need_tbl ? L.G * LTB : 0u));
     L.off_tbl = o;
-    o = align16(o + (L.need_tbl ? L.G * T64 * 8u : 0u));
+    o = align16(o + (L.need_tbl ? L.G * T4 * 8u : 0u));
     L.off_cm = o;
     o = align16(o + (L.need_cls ? L.G * (L.cm_per_trace * NW + 1) * 8u : 0u));
     L.off_meta = o;
