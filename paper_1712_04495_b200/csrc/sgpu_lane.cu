@@ -123,6 +123,22 @@ __device__ __forceinline__ void warp_bitonic_sort(KeyT (&v)[K], uint32_t lane) {
     }
 }
 
+// Sort 64-bit keys (kInf = padding) with 32-bit compare-exchanges when every
+// real key is below 2^32 - 1 (warp-uniform `narrow`): half the shuffles.
+template <int K>
+__device__ __forceinline__ void warp_sort_keys(uint64_t (&v)[K], bool narrow, uint32_t lane) {
+    if (narrow) {
+        uint32_t w[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) w[k] = v[k] == kInf ? ~0u : (uint32_t)v[k];
+        warp_bitonic_sort<K>(w, lane);
+#pragma unroll
+        for (int k = 0; k < K; k++) v[k] = w[k] == ~0u ? kInf : (uint64_t)w[k];
+    } else {
+        warp_bitonic_sort<K>(v, lane);
+    }
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -587,7 +603,11 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
         }
     }
     uint32_t fail = __any_sync(FULL, big) ? 1u : 0u;
-    warp_bitonic_sort<K>(key, lane);
+    uint32_t amax = 0;
+#pragma unroll
+    for (int k = 0; k < K; k++) amax = max(amax, key[k] != kInf ? (uint32_t)(key[k] >> 10) : 0u);
+    amax = __reduce_max_sync(FULL, amax);
+    warp_sort_keys<K>(key, ndev == 1 && amax < (1u << 22), lane);  // device bits sit above bit 41
     __syncwarp();
     // SoA records in arrival order
     uint32_t memk[K], prk[K];
@@ -682,7 +702,10 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
             const uint32_t e = (uint32_t)k * 32u + lane;
             mk[k] = memk[k] != ~0u ? (((uint64_t)memk[k] << 8) | e) : kInf;
         }
-        warp_bitonic_sort<K>(mk, lane);
+        uint32_t mmax = 0;
+#pragma unroll
+        for (int k = 0; k < K; k++) mmax = max(mmax, memk[k] != ~0u ? memk[k] : 0u);
+        warp_sort_keys<K>(mk, __reduce_max_sync(FULL, mmax) < (1u << 24), lane);
         // rank lookup: 64 buckets spread linearly over [lo, hi]
         uint32_t mx = 0, mn = ~0u;
 #pragma unroll

@@ -201,6 +201,20 @@ def test_lane_fallback_tick_range(cuda):
     check_against_oracle(apps, (1000,), cuda)
 
 
+def test_wide_sort_keys(cuda):
+    """Arrivals >= 2^22 and requests >= 2^24 MiB take the 64-bit key sorts of
+    the lane kernel's staging (narrow 32-bit sorts otherwise)."""
+    rng = np.random.default_rng(12)
+    n, nt = 64, 128
+    apps = np.zeros((nt, n, 4), dtype=np.uint32)
+    apps[:, :, 0] = rng.integers(0, 1 << 30, (nt, n))
+    apps[:, :, 1] = rng.integers(1 << 20, 1 << 26, (nt, n))
+    apps[:, :, 2] = rng.integers(1, 1 << 20, (nt, n))
+    apps[:, :, 3] = rng.integers(0, 3, (nt, n))
+    apps[::3, :, 0] = rng.integers(0, 50_000, (len(apps[::3]), n))  # some traces narrow
+    check_against_oracle(apps, (1 << 27,), cuda)
+
+
 def test_ragged_offsets(cuda):
     rng = np.random.default_rng(9)
     lens = rng.integers(0, 90, 300)
