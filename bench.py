@@ -181,6 +181,24 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "k1_traffic.json")
+TRAFFIC_SOURCE = "dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full launch (profiles/k1_traffic.json)"
+
+
+def measured_traffic(config, traces_per_gpu):
+    """DRAM bytes per K1 launch from the committed ncu capture, when it was
+    taken on this configuration and batch size (else None)."""
+    try:
+        with open(TRAFFIC_FILE) as f:
+            t = json.load(f)
+    except (OSError, ValueError):
+        return None
+    from paper_1712_04495_b200.tracegen import CONFIGS
+    if t.get("config") != config or traces_per_gpu != CONFIGS[config].n_traces:
+        return None
+    return int(t["dram_bytes_read"]) + int(t["dram_bytes_write"])
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -341,6 +359,7 @@ def main():
     mean_k = statistics.mean(kern_ms) / 1000.0
     peak, peak_src = hbm_peak()
     achieved = alg_bytes / mean_k / 1e9
+    traffic = measured_traffic(args.config, n)
 
     # e2e through the C ABI host-buffer pipeline
     e2e = None
@@ -398,7 +417,8 @@ def main():
             "events_per_s": aggd["sum_pops"] / (ms_per_step / 1000.0),
             "aggregate": aggd,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch",
+                         "traffic_source": TRAFFIC_SOURCE if traffic else None, "peak_source": peak_src,
                          "kernel": os.environ.get("SGPU_K1_NAME", "trace_sim_lane_kernel"), "alg_bytes_per_launch": alg_bytes,
                          "mean_launch_ms": mean_k * 1000.0},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
