@@ -383,7 +383,8 @@ def main():
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e = {"value": units_per_step * e2e_steps / float(dt[0]), "unit": "traces/s",
                "h2d_bytes_per_step": int(host_apps.nbytes), "d2h_bytes_per_step": int(outb.d2h_bytes()),
-               "api": "sg_simulate_batch_host (C ABI, pinned host buffers, 3-stream pipeline)",
+               "api": "sg_simulate_batch_host (C ABI, pinned host buffers, 3-stream pipeline; "
+                      "grant ticks derived on host threads from end ticks and inputs)",
                "steps": e2e_steps}
 
     cpu = None

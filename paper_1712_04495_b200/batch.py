@@ -212,8 +212,12 @@ class HostBuffers:
         self.dev_pct = alloc((npol, n_traces, ndev), torch.float64) if want_pct else None
 
     def d2h_bytes(self) -> int:
+        """Bytes the host pipeline copies device -> host per call.  With both
+        tick arrays requested the grants are derived on the host from the
+        end ticks and the inputs (grant = end - busy), so they cross no bus."""
+        derived = self.grant if (self.grant is not None and self.end is not None) else None
         return sum(a.nbytes for a in (self.grant, self.end, self.stats, self.mem_pct, self.dev_pct)
-                   if a is not None)
+                   if a is not None and a is not derived)
 
 
 def pinned_apps(n_traces: int, n_apps: int) -> np.ndarray:

@@ -4,6 +4,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
+#include <immintrin.h>
 #include <vector>
 
 #include "sgpu_common.cuh"
@@ -157,6 +159,83 @@ int sg_simulate_batch(const sg_batch* in, const sg_out* out, void* stream) {
 // Host-buffer pipeline: chunks of traces cycle through NBUF device buffer
 // sets on NBUF streams; each chunk is H2D -> trace_sim -> D2H on its stream,
 // so the copies of one chunk overlap the simulation of the next.
+//
+// The per-app grant ticks are not copied back: for T0 traces the grant is
+// the start of the busy step, so grant = end - busy for apps that request
+// memory and end, NEVER otherwise (memshare/harness.py:514-531) — host
+// threads derive it from the end ticks and the caller's own input records
+// while later chunks are still on the GPU.  That removes a third of the
+// device->host bytes (the pipeline is PCIe-bound).  Traces whose record
+// reports a tick overflow (where that identity does not hold) are
+// re-simulated with device grants afterwards.
+namespace {
+
+struct HostChunk {
+    uint64_t t0, nt;
+    cudaEvent_t done;
+};
+
+// One (trace, policy) row: g = (mem != 0 && end != NEVER) ? end - busy : NEVER.
+// AVX2 with streaming stores when the row is 32-byte aligned (the grant
+// array is write-only here: no read-for-ownership traffic).
+__attribute__((target("avx2"))) void grant_row_avx2(const uint32_t* mem, const uint32_t* busy,
+                                                    const uint32_t* e, uint32_t* g, uint32_t n) {
+    const __m256i never = _mm256_set1_epi32((int)SG_NEVER);
+    const __m256i zero = _mm256_setzero_si256();
+    uint32_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+        const __m256i ev = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(e + i));
+        const __m256i mv = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(mem + i));
+        const __m256i bv = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(busy + i));
+        const __m256i no = _mm256_or_si256(_mm256_cmpeq_epi32(mv, zero), _mm256_cmpeq_epi32(ev, never));
+        const __m256i gv = _mm256_blendv_epi8(_mm256_sub_epi32(ev, bv), never, no);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(g + i), gv);
+    }
+    for (; i < n; i++) g[i] = (mem[i] != 0 && e[i] != SG_NEVER) ? e[i] - busy[i] : SG_NEVER;
+}
+
+void grant_row_scalar(const uint32_t* mem, const uint32_t* busy, const uint32_t* e, uint32_t* g,
+                      uint32_t n) {
+    for (uint32_t i = 0; i < n; i++) g[i] = (mem[i] != 0 && e[i] != SG_NEVER) ? e[i] - busy[i] : SG_NEVER;
+}
+
+// grant[p][a] for traces [t_lo, t_hi) of the batch; overflowing (trace,
+// policy) pairs are skipped and reported.
+void derive_grants(const sg_batch* in, const sg_out* out, uint32_t npol, uint64_t t_lo, uint64_t t_hi,
+                   std::vector<uint64_t>& overflow, bool avx2) {
+    const uint64_t N = in->n_traces;
+    const uint32_t napps = in->apps_per_trace, ndev = in->ndev;
+    const uint64_t total = N * napps;
+    const sg_trace_stats* st = static_cast<const sg_trace_stats*>(out->stats);
+    const uint32_t* end = static_cast<const uint32_t*>(out->end);
+    uint32_t* grant = static_cast<uint32_t*>(out->grant);
+    std::vector<uint32_t> mem(napps), busy(napps);
+    const bool vec = avx2 && (napps % 8 == 0) &&
+                     (reinterpret_cast<uintptr_t>(grant) & 31u) == 0 && ((total * 4) & 31u) == 0;
+    for (uint64_t t = t_lo; t < t_hi; t++) {
+        const sg_app* ap = in->apps + t * napps;
+        for (uint32_t i = 0; i < napps; i++) {
+            mem[i] = ap[i].mem_mib;
+            busy[i] = ap[i].busy;
+        }
+        bool ov_any = false;
+        for (uint32_t p = 0; p < npol; p++) {
+            bool ov = false;
+            for (uint32_t d = 0; d < ndev; d++)
+                ov = ov || (st[((uint64_t)p * N + t) * ndev + d].status & SG_ST_TICK_OVERFLOW);
+            if (ov) { ov_any = true; continue; }
+            const uint32_t* e = end + (uint64_t)p * total + t * napps;
+            uint32_t* g = grant + (uint64_t)p * total + t * napps;
+            if (vec) grant_row_avx2(mem.data(), busy.data(), e, g, napps);
+            else grant_row_scalar(mem.data(), busy.data(), e, g, napps);
+        }
+        if (ov_any) overflow.push_back(t);
+    }
+    if (vec) _mm_sfence();
+}
+
+}  // namespace
+
 int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_device,
                            uint64_t chunk_traces) {
     Shape s;
@@ -175,6 +254,8 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
     const uint32_t ndev = in->ndev;
     if (chunk_traces == 0) chunk_traces = 1u << 16;
     if (chunk_traces > N) chunk_traces = N;
+    // grants derived on the host when both tick arrays are requested
+    const bool host_grant = out->grant != nullptr && out->end != nullptr;
     constexpr int NBUF = 3;
     const size_t app_b = chunk_traces * napps * sizeof(sg_app);
     const size_t tick_b = (size_t)s.npol * chunk_traces * napps * sizeof(uint32_t);
@@ -189,6 +270,7 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
         sg_trace_stats* stats = nullptr;
         double *mem = nullptr, *dev = nullptr;
     } B[NBUF];
+    std::vector<HostChunk> chunks;
     // Pipeline buffers come from the device's stream-ordered memory pool
     // (cudaMallocAsync), kept cached between calls: repeated calls pay no
     // cudaMalloc/cudaFree or implicit device synchronisation.
@@ -209,11 +291,12 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
             cudaStreamSynchronize(b.st);
             cudaStreamDestroy(b.st);
         }
+        for (auto& c : chunks) cudaEventDestroy(c.done);
     };
     for (auto& b : B) {
         e = cudaStreamCreateWithFlags(&b.st, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaMallocAsync(&b.apps, app_b, b.st);
-        if (e == cudaSuccess && out->grant) e = cudaMallocAsync(&b.grant, tick_b, b.st);
+        if (e == cudaSuccess && out->grant && !host_grant) e = cudaMallocAsync(&b.grant, tick_b, b.st);
         if (e == cudaSuccess && out->end) e = cudaMallocAsync(&b.end, tick_b, b.st);
         if (e == cudaSuccess) e = cudaMallocAsync(&b.stats, st_b, b.st);
         if (e == cudaSuccess && want_pct) e = cudaMallocAsync(&b.mem, pct_b, b.st);
@@ -244,7 +327,7 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
             const uint64_t ho = (uint64_t)p * n_apps_total + a0;
             const uint64_t hs = ((uint64_t)p * N + t0) * ndev;
             const uint64_t dsrc = (uint64_t)p * nt * ndev;
-            if (out->grant)
+            if (b.grant)
                 e = cudaMemcpyAsync(static_cast<uint32_t*>(out->grant) + ho, b.grant + (uint64_t)p * na,
                                     na * 4, cudaMemcpyDeviceToHost, b.st);
             if (e == cudaSuccess && out->end)
@@ -261,12 +344,68 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
                                     cudaMemcpyDeviceToHost, b.st);
             if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "D2H outputs"); }
         }
+        if (host_grant) {
+            HostChunk c{t0, nt, nullptr};
+            e = cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventRecord(c.done, b.st);
+            if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "chunk event"); }
+            chunks.push_back(c);
+        }
+    }
+    std::vector<uint64_t> overflow;
+    if (host_grant) {
+        // host threads follow the pipeline chunk by chunk, each deriving the
+        // grants of its contiguous share of every chunk's traces
+        const bool avx2 = __builtin_cpu_supports("avx2");
+        unsigned nthr = std::thread::hardware_concurrency();
+        nthr = nthr == 0 ? 1 : (nthr > 16 ? 16 : nthr);
+        std::vector<std::vector<uint64_t>> ov(nthr);
+        std::vector<cudaError_t> errs(nthr, cudaSuccess);
+        std::vector<std::thread> pool;
+        for (unsigned w = 0; w < nthr; w++) {
+            pool.emplace_back([&, w]() {
+                for (const auto& c : chunks) {
+                    const cudaError_t ce = cudaEventSynchronize(c.done);
+                    if (ce != cudaSuccess) { errs[w] = ce; return; }
+                    const uint64_t lo = c.t0 + c.nt * w / nthr, hi = c.t0 + c.nt * (w + 1) / nthr;
+                    derive_grants(in, out, s.npol, lo, hi, ov[w], avx2);
+                }
+            });
+        }
+        for (auto& th : pool) th.join();
+        for (unsigned w = 0; w < nthr; w++) {
+            if (errs[w] != cudaSuccess) { cleanup(); return cuda_fail(errs[w], "pipeline"); }
+            overflow.insert(overflow.end(), ov[w].begin(), ov[w].end());
+        }
     }
     for (auto& b : B) {
         e = cudaStreamSynchronize(b.st);
         if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "pipeline"); }
     }
     cleanup();
+    if (!overflow.empty()) {
+        // exact grants of the (rare) tick-overflow traces: re-simulate them
+        // with device-side grant output
+        const uint64_t no = overflow.size();
+        std::vector<sg_app> h_apps(no * napps);
+        for (uint64_t k = 0; k < no; k++)
+            memcpy(&h_apps[k * napps], in->apps + overflow[k] * napps, napps * sizeof(sg_app));
+        sg_batch rb = *in;
+        rb.n_traces = no;
+        rb.apps = h_apps.data();
+        std::vector<uint32_t> g((size_t)s.npol * no * napps);
+        std::vector<sg_trace_stats> rs((size_t)s.npol * no * ndev);
+        sg_out ro;
+        memset(&ro, 0, sizeof(ro));
+        ro.grant = g.data();  // no end buffer: this call copies device grants
+        ro.stats = rs.data();
+        rc = sg_simulate_batch_host(&rb, &ro, cuda_device, 0);
+        if (rc) return rc;
+        for (uint64_t k = 0; k < no; k++)
+            for (uint32_t p = 0; p < s.npol; p++)
+                memcpy(static_cast<uint32_t*>(out->grant) + (uint64_t)p * n_apps_total + overflow[k] * napps,
+                       &g[((uint64_t)p * no + k) * napps], napps * sizeof(uint32_t));
+    }
     return 0;
 }
 

@@ -296,3 +296,42 @@ def test_host_pipeline_matches_device(cuda):
     np.testing.assert_array_equal(host.stats.view(np.uint8), dres.stats().view(np.uint8))
     assert floats_equal(host.mem_pct, dres.mem_pct.cpu().numpy())
     assert floats_equal(host.dev_pct, dres.dev_pct.cpu().numpy())
+
+
+@pytest.mark.parametrize("case", ["overflow", "c5", "long", "grant_only"])
+def test_host_pipeline_cases(case, cuda):
+    """The host pipeline derives grants on the host (end - busy); traces with
+    a tick overflow are re-simulated for exact grants; multi-device, long
+    (warp-kernel) traces and a grant-only request follow the same contract."""
+    rng = np.random.default_rng(21)
+    caps = (184_320,)
+    if case == "overflow":
+        n, nt = 40, 300
+        apps = np.zeros((nt, n, 4), dtype=np.uint32)
+        apps[:, :, 0] = rng.integers(0, 1000, (nt, n))
+        apps[:, :, 1] = rng.integers(1, 60_000, (nt, n))
+        apps[:, :, 2] = rng.integers(1, 50, (nt, n))
+        apps[5:9, :, 2] = np.uint32(0x7FFFFFF)   # sum(busy) past 2^32 ticks
+        apps[40:42, 0, 0] = np.uint32(0xFFFFFF00)
+    elif case == "c5":
+        cfg = CONFIGS["C5"]
+        apps, caps = as_u32x4(generate(cfg.gen, 0, 700)), cfg.cap_mib
+    elif case == "long":
+        cfg = CONFIGS["C4"]
+        apps, caps = as_u32x4(generate(cfg.gen, 0, 400)), cfg.cap_mib
+    else:
+        apps = as_u32x4(generate(CONFIGS["C2"].gen, 0, 900))
+    dres = run(apps, POLICIES, caps, cuda)
+    pin = B.pinned_apps(*apps.shape[:2])
+    pin[...] = apps
+    want_end = case != "grant_only"
+    out = B.HostBuffers(4, apps.shape[0], apps.shape[1], len(caps))
+    if not want_end:
+        out.end = None
+    host = B.simulate_batch_host(pin, POLICIES, caps, chunk_traces=128, out=out)
+    np.testing.assert_array_equal(host.grant, dres.ticks("grant"))
+    if want_end:
+        np.testing.assert_array_equal(host.end, dres.ticks("end"))
+    np.testing.assert_array_equal(host.stats.view(np.uint8), dres.stats().view(np.uint8))
+    if case == "overflow":
+        assert (dres.stats()["status"] & 1).any()
