@@ -47,6 +47,7 @@ constexpr uint32_t kLaneFifo = 4 * kLaneFifoWords;
 constexpr uint32_t kLaneClassMasks = 64;    // class masks per warp, split over its trace slots
 constexpr int kLaneWarpsPerBlock = 1;
 constexpr uint64_t kInf = ~0ull;
+constexpr uint32_t kLtBuckets = 128;        // rank-lookup buckets per trace
 constexpr uint32_t kBusyBits = 21;          // busy < 2^21 on this path; app index above it
 
 struct LaneParams {
@@ -67,7 +68,7 @@ struct LaneParams {
 template <uint32_t N> struct SlotStride {
     static constexpr uint32_t S32 = N + 4;          // u32 record arrays
     static constexpr uint32_t POR = 80;             // rank -> position (u8, padded)
-    static constexpr uint32_t LTB = 80;             // rank lookup: 64 u8 buckets (+16 B skew)
+    static constexpr uint32_t LTB = kLtBuckets + 16;  // rank lookup: u8 buckets + 3 u32 params (+skew)
     static constexpr uint32_t T4 = N / 4 + 2;       // fit table at every 4th rank (N/4 + 1 entries)
 };
 
@@ -145,9 +146,9 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 
 __device__ __forceinline__ uint32_t ffs64(uint64_t x) { return (uint32_t)__ffsll((long long)x) - 1u; }
 
-// Rank-lookup bucket of a request d = mem - lo >= 0: monotone in d, 0..63.
+// Rank-lookup bucket of a request d = mem - lo >= 0: monotone in d.
 __device__ __forceinline__ uint32_t lt_bucket(uint32_t d, uint32_t scale) {
-    return min((uint32_t)(((uint64_t)d * scale) >> 32), 63u);
+    return min((uint32_t)(((uint64_t)d * scale) >> 32), kLtBuckets - 1u);
 }
 
 template <int K>
@@ -163,7 +164,7 @@ struct LaneSim {
     const uint32_t* s_mem;   // request MiB
     const uint32_t* s_bw;    // busy | app << kBusyBits
     const uint8_t* s_por;    // position of the r-th smallest request (N past the end)
-    const uint8_t* s_lt;     // s_lt[j] = #requests in buckets < j (64 buckets)
+    const uint8_t* s_lt;     // s_lt[j] = #requests in buckets < j
     uint32_t lt_lo, lt_hi, lt_scale;
     const uint64_t* s_t4;    // T[4j]: positions of the 4j smallest requests
     const uint64_t* s_cm;    // class masks of this lane's device, top class first
@@ -267,7 +268,7 @@ struct LaneSim {
         for (uint32_t w = 0; w < NW; w++)
             if (w == (q >> 6)) mask[w] |= 1ull << (q & 63u);
     }
-    // number of requests <= budget in the trace: bucket lookup (64 buckets
+    // number of requests <= budget in the trace: bucket lookup (kLtBuckets
     // spread linearly over [smallest, largest] request), then a short
     // forward scan of the sorted requests inside the bucket
     __device__ __forceinline__ uint32_t fit_rank(uint32_t budget) const {
@@ -706,7 +707,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
 #pragma unroll
         for (int k = 0; k < K; k++) mmax = max(mmax, memk[k] != ~0u ? memk[k] : 0u);
         warp_sort_keys<K>(mk, __reduce_max_sync(FULL, mmax) < (1u << 24), lane);
-        // rank lookup: 64 buckets spread linearly over [lo, hi]
+        // rank lookup: kLtBuckets buckets spread linearly over [lo, hi]
         uint32_t mx = 0, mn = ~0u;
 #pragma unroll
         for (int k = 0; k < K; k++) {
@@ -716,7 +717,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
         mx = __reduce_max_sync(FULL, mx);
         mn = __reduce_min_sync(FULL, mn);
         if (mn > mx) mn = mx;  // empty trace
-        const uint64_t sc = (64ull << 32) / ((uint64_t)(mx - mn) + 1ull);
+        const uint64_t sc = ((uint64_t)kLtBuckets << 32) / ((uint64_t)(mx - mn) + 1ull);
         const uint32_t scale = sc > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)sc;
         uint64_t carry = 0;
         uint32_t bcarry = 0;  // bucket of the last rank of the previous row (+1)
@@ -736,18 +737,18 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
             if ((r & 3u) == 3u) s_t4[(r + 1) >> 2] = v;
             carry = __shfl_sync(FULL, (uint32_t)v, 31) | ((uint64_t)__shfl_sync(FULL, (uint32_t)(v >> 32), 31) << 32);
             // LT[j] = first rank whose bucket is >= j: rank r owns (b[r-1], b[r]]
-            const uint32_t b = valid ? lt_bucket((uint32_t)(mk[k] >> 8) - mn, scale) + 1u : 65u;
+            const uint32_t b = valid ? lt_bucket((uint32_t)(mk[k] >> 8) - mn, scale) + 1u : kLtBuckets + 1u;
             uint32_t bp = __shfl_up_sync(FULL, b, 1);
             if (lane == 0) bp = bcarry;
-            for (uint32_t j = bp; j < min(b, 65u); j++)
-                if (j < 64u) s_lt[j] = (uint8_t)r;
+            for (uint32_t j = bp; j < min(b, kLtBuckets + 1u); j++)
+                if (j < kLtBuckets) s_lt[j] = (uint8_t)r;
             bcarry = __shfl_sync(FULL, b, 31);
         }
         // buckets above the largest request (all ranks valid) -> N
-        for (uint32_t j = bcarry + lane; j < 64u; j += 32u) s_lt[j] = (uint8_t)N;
+        for (uint32_t j = bcarry + lane; j < kLtBuckets; j += 32u) s_lt[j] = (uint8_t)N;
         if (lane == 0) {
             s_t4[0] = 0ull;
-            uint32_t* prm = reinterpret_cast<uint32_t*>(s_lt + 64);
+            uint32_t* prm = reinterpret_cast<uint32_t*>(s_lt + kLtBuckets);
             prm[0] = mn;
             prm[1] = mx;
             prm[2] = scale;
@@ -824,9 +825,9 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel
                 sim.s_bw = reinterpret_cast<const uint32_t*>(ws + L.off_bw) + g * SS::S32;
                 sim.s_por = ws + L.off_por + g * SS::POR;
                 sim.s_lt = ws + L.off_lt + g * SS::LTB;
-                sim.lt_lo = reinterpret_cast<const uint32_t*>(sim.s_lt + 64)[0];
-                sim.lt_hi = reinterpret_cast<const uint32_t*>(sim.s_lt + 64)[1];
-                sim.lt_scale = reinterpret_cast<const uint32_t*>(sim.s_lt + 64)[2];
+                sim.lt_lo = reinterpret_cast<const uint32_t*>(sim.s_lt + kLtBuckets)[0];
+                sim.lt_hi = reinterpret_cast<const uint32_t*>(sim.s_lt + kLtBuckets)[1];
+                sim.lt_scale = reinterpret_cast<const uint32_t*>(sim.s_lt + kLtBuckets)[2];
                 sim.s_t4 = reinterpret_cast<const uint64_t*>(ws + L.off_tbl) + g * SS::T4;
                 uint32_t c0 = 0, c1 = 0;
                 if (L.need_cls) { c0 = meta[19 + d]; c1 = meta[20 + d]; }
@@ -934,7 +935,7 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
     uint32_t fb = L.sp.warp_bytes;
     fb = max(fb, kLaneHeap * 32u * 8u);
     fb = max(fb, N * 16u);
-    const uint32_t S32 = N + 4, POR = 80, LTB = 80, T4 = N / 4 + 2;  // SlotStride<N>
+    const uint32_t S32 = N + 4, POR = 80, LTB = kLtBuckets + 16, T4 = N / 4 + 2;  // SlotStride<N>
     uint32_t o = 0;
     L.off_a = o;
     o = align16(o + L.G * S32 * 4u);
