@@ -41,17 +41,23 @@
 
 namespace sg {
 
-constexpr uint32_t kLaneHeap = 24;          // busy-end heap slots per lane
-constexpr uint32_t kLaneFifoWords = 8;      // wake FIFO: 4 app positions per u32 word
+constexpr uint32_t kLaneHeap = 21;          // busy-end heap slots per lane: a 4-ary heap of depth 2
+constexpr uint32_t kLaneFifoWords = 4;      // wake FIFO: 4 app positions per u32 word
 constexpr uint32_t kLaneFifo = 4 * kLaneFifoWords;
 constexpr uint32_t kLaneClassMasks = 64;    // class masks per warp, split over its trace slots
 constexpr int kLaneWarpsPerBlock = 1;
 constexpr uint64_t kInf = ~0ull;
 constexpr uint32_t kLtBuckets = 128;        // rank-lookup buckets per trace
 constexpr uint32_t kBusyBits = 21;          // busy < 2^21 on this path; app index above it
+constexpr uint32_t kClsShift = 29;          // s_bw bits 29-31: priority class of the app within its device
+constexpr uint32_t kLaneMaxCls = 8;         // classes per device on this path (more: exact fallback)
+
+__device__ __forceinline__ uint32_t bw_busy(uint32_t bw) { return bw & ((1u << kBusyBits) - 1u); }
+__device__ __forceinline__ uint32_t bw_app(uint32_t bw) { return (bw >> kBusyBits) & 0xFFu; }
+__device__ __forceinline__ uint32_t bw_cls(uint32_t bw) { return bw >> kClsShift; }
 
 struct LaneParams {
-    SimParams sp;          // inputs/outputs + the fallback TraceSim layout (off_* relative to off_fb)
+    SimParams sp;          // inputs/outputs + the fallback TraceSim layout (off_* relative to the warp region)
     uint32_t G;            // traces per warp (32 / lpt)
     uint32_t lpt;          // lanes per trace = npol * ndev
     uint32_t need_cls;     // a priority policy is requested: build class masks
@@ -162,7 +168,7 @@ struct LaneSim {
     // trace slot (shared by the trace's lanes), arrival-position order
     const uint32_t* s_a;     // arrival tick
     const uint32_t* s_mem;   // request MiB
-    const uint32_t* s_bw;    // busy | app << kBusyBits
+    const uint32_t* s_bw;    // busy | app << kBusyBits | class << kClsShift
     const uint8_t* s_por;    // position of the r-th smallest request (N past the end)
     const uint8_t* s_lt;     // s_lt[j] = #requests in buckets < j
     uint32_t lt_lo, lt_hi, lt_scale;
@@ -184,6 +190,12 @@ struct LaneSim {
     uint64_t I;
     int32_t busy_level, holders;
     uint32_t maxh, grants, pops;
+    // incremental grant_waiters state (fit-table path): one select_grants
+    // step per loop iteration while `gs` (harness.py:545-558)
+    bool gs;
+    uint32_t clsmask;        // priority classes with waiting entries (bit c: class c, top = 0)
+    uint32_t gc, gbud, gb0, gg;
+    uint64_t gcand, grem;    // unscanned candidates / waiting members of the round's class
 
     __device__ __forceinline__ LaneSim(const SimParams& p) : P(p) {}
 
@@ -198,53 +210,58 @@ struct LaneSim {
     }
 
     // ------------------------------------------------- busy-end heap
-    // 4-ary min-heap: half the levels of a binary heap, and the four child
-    // loads of a level are independent
+    // 4-ary min-heap of at most 21 keys (root + 4 + 16): every sift is at
+    // most two levels, unrolled and predicated, and the four child loads of a
+    // level are independent
     __device__ __forceinline__ void push(uint32_t t, uint32_t q) {
         if (hs >= kLaneHeap) { fail = true; return; }
         const uint64_t key = ((uint64_t)t << 32) | (counter << 8) | q;
         counter += 1;
-        uint32_t i = hs++;
-        while (i > 0) {
-            const uint32_t par = (i - 1) >> 2;
-            const uint64_t pk = heap[par * 32];
-            if (pk < key) break;
-            heap[i * 32] = pk;
-            i = par;
-        }
-        heap[i * 32] = key;
-        if (i == 0) kh = key;
+        const uint32_t i = hs++;
+        // sift up at most two levels: i -> p1 -> p2
+        const uint32_t p1 = i > 0 ? (i - 1) >> 2 : 0u;
+        const uint64_t k1 = i > 0 ? heap[p1 * 32] : 0ull;
+        const bool up1 = i > 0 && key < k1;
+        const uint32_t p2 = p1 > 0 ? (p1 - 1) >> 2 : 0u;
+        const uint64_t k2 = up1 && p1 > 0 ? heap[p2 * 32] : 0ull;
+        const bool up2 = up1 && p1 > 0 && key < k2;
+        if (up1) heap[i * 32] = k1;
+        if (up2) heap[p1 * 32] = k2;
+        const uint32_t dst = up2 ? p2 : (up1 ? p1 : i);
+        heap[dst * 32] = key;
+        if (dst == 0) kh = key;
+    }
+    // min of the (up to) four children c..c+3 of a node; kInf past the end
+    __device__ __forceinline__ uint64_t min_child(uint32_t c, uint32_t& m) const {
+        const uint64_t k0 = c < hs ? heap[c * 32] : kInf;
+        const uint64_t k1 = c + 1 < hs ? heap[(c + 1) * 32] : kInf;
+        const uint64_t k2 = c + 2 < hs ? heap[(c + 2) * 32] : kInf;
+        const uint64_t k3 = c + 3 < hs ? heap[(c + 3) * 32] : kInf;
+        const bool s01 = k1 < k0;
+        const uint64_t x = s01 ? k1 : k0;
+        const uint32_t ix = s01 ? c + 1 : c;
+        const bool s23 = k3 < k2;
+        const uint64_t y = s23 ? k3 : k2;
+        const uint32_t iy = s23 ? c + 3 : c + 2;
+        const bool sxy = y < x;
+        m = sxy ? iy : ix;
+        return sxy ? y : x;
     }
     __device__ __forceinline__ void pop() {
         hs -= 1;
-        if (hs == 0) { kh = kInf; return; }
         const uint64_t lastk = heap[hs * 32];
-        uint32_t i = 0;
-        uint64_t top = lastk;
-        while (true) {
-            const uint32_t c = 4 * i + 1;
-            if (c >= hs) break;
-            uint64_t k0 = heap[c * 32];
-            const uint64_t k1 = c + 1 < hs ? heap[(c + 1) * 32] : kInf;
-            const uint64_t k2 = c + 2 < hs ? heap[(c + 2) * 32] : kInf;
-            const uint64_t k3 = c + 3 < hs ? heap[(c + 3) * 32] : kInf;
-            uint32_t m = c;
-            const bool s01 = k1 < k0;
-            const uint64_t a = s01 ? k1 : k0;
-            const uint32_t ia = s01 ? c + 1 : c;
-            const bool s23 = k3 < k2;
-            const uint64_t b = s23 ? k3 : k2;
-            const uint32_t ib = s23 ? c + 3 : c + 2;
-            const bool sab = b < a;
-            k0 = sab ? b : a;
-            m = sab ? ib : ia;
-            if (lastk < k0) break;
-            heap[i * 32] = k0;
-            if (i == 0) top = k0;
-            i = m;
-        }
-        heap[i * 32] = lastk;
-        kh = top;
+        // level 1: children 1..4 of the root
+        uint32_t m1;
+        const uint64_t k1 = min_child(1u, m1);
+        const bool down1 = k1 < lastk;
+        // level 2: children of m1 (5..20)
+        uint32_t m2;
+        const uint64_t k2 = min_child(4u * m1 + 1u, m2);
+        const bool down2 = down1 && k2 < lastk;
+        heap[0] = down1 ? k1 : lastk;
+        if (down1) heap[m1 * 32] = down2 ? k2 : lastk;
+        if (down2) heap[m2 * 32] = lastk;
+        kh = hs == 0 ? kInf : (down1 ? k1 : lastk);
     }
 
     // ------------------------------------------------- wake FIFO
@@ -263,10 +280,11 @@ struct LaneSim {
     }
 
     // ------------------------------------------------- wait queue
-    __device__ __forceinline__ void enqueue(uint32_t q) {
+    __device__ __forceinline__ void enqueue(uint32_t q, uint32_t bw) {
 #pragma unroll
         for (uint32_t w = 0; w < NW; w++)
             if (w == (q >> 6)) mask[w] |= 1ull << (q & 63u);
+        clsmask |= 1u << bw_cls(bw);
     }
     // number of requests <= budget in the trace: bucket lookup (kLtBuckets
     // spread linearly over [smallest, largest] request), then a short
@@ -303,47 +321,61 @@ struct LaneSim {
         else grant_waiters_scan();
     }
 
-    // <= 64 apps: one code path for all four kinds, so the lanes of a warp
-    // (mixed policies) stay converged.  Per round: the top class (all
-    // waiting entries for FIFO/MMU); per grant: fit = class & T[#requests <=
-    // budget]; FIFO takes the head iff it fits, MMU the lowest fit; both
-    // continue above the granted position.
-    __device__ __forceinline__ void grant_waiters_tbl() {
-        if (!mask[0]) return;
-        const uint32_t nc = prio_pol ? ncls : 1u;
-        uint32_t c = 0;
-        while (true) {
-            uint64_t cm = ~0ull, cand = 0;
-            while (c < nc) {
-                cm = prio_pol ? s_cm[c] : ~0ull;
-                cand = mask[0] & cm;
-                if (cand) break;
-                c += 1;
-            }
-            if (!cand) return;
-            const uint32_t budget0 = cap - used;
-            uint32_t budget = budget0, g = 0;
-            while (cand) {
-                const uint64_t fit = cand & fit_set(fit_rank(budget));
-                const uint64_t head = cand & (0ull - cand);
-                const uint64_t pick = mmu ? fit : (fit & head);
-                if (!pick) break;
-                const uint32_t q = ffs64(pick);
-                grant_one(q, s_mem[q], budget, g);
-                if (fail) return;
-                cand &= ~((2ull << q) - 1ull);
-            }
-            if (g) {
-                mem_point(last);
-                used += budget0 - budget;
-                holders += (int32_t)g;
-                maxh = max(maxh, (uint32_t)holders);
-                grants += g;
-            }
-            // the top class continues only if it drained (harness.py:547-550)
-            if (!prio_pol || g == 0 || (mask[0] & cm) != 0) return;
-            c += 1;
+    // <= 64 apps: grant_waiters as a sequence of steps, one per loop
+    // iteration, so a lane granting several waiters does not hold the whole
+    // warp in a nested loop; the lane pops no event until it is done, so the
+    // order is the reference's.  One code path for all four kinds keeps the
+    // lanes of a warp (mixed policies) converged.  A round: the top class
+    // (all waiting entries for FIFO/MMU, policy.py:58-63); a step: fit =
+    // cand & T[#requests <= budget]; FIFO takes the head iff it fits, MMU the
+    // lowest fit (policy.py:65-73); both continue above the granted position.
+    __device__ __forceinline__ void init_round() {
+        uint64_t cm = ~0ull;
+        if (prio_pol) {
+            gc = ffs64(clsmask);  // clsmask != 0 whenever the queue is not empty
+            cm = s_cm[gc];
         }
+        gcand = mask[0] & cm;
+        grem = gcand;
+        gs = gcand != 0;
+        gb0 = gbud = cap - used;
+        gg = 0;
+    }
+    __device__ __forceinline__ void grant_step() {
+        const uint64_t fit = gcand & fit_set(fit_rank(gbud));
+        const uint64_t head = gcand & (0ull - gcand);
+        const uint64_t pick = mmu ? fit : (fit & head);
+        if (pick) {
+            const uint32_t q = ffs64(pick);
+            const uint64_t bit = 1ull << q;
+            mask[0] &= ~bit;
+            grem &= ~bit;
+            gbud -= s_mem[q];
+            gg += 1;
+            wake(q);
+            gcand &= ~((2ull << q) - 1ull);
+        }
+        if (!pick || !gcand) {  // the round ends
+            if (gg) {
+                mem_point(last);
+                used += gb0 - gbud;
+                holders += (int32_t)gg;
+                maxh = max(maxh, (uint32_t)holders);
+                grants += gg;
+            }
+            // the top class drained: the next class is served in the same
+            // tick (harness.py:547-550); otherwise the next round is empty
+            if (prio_pol && gg && !grem) {
+                clsmask &= ~(1u << gc);
+                if (clsmask) init_round();
+                else gs = false;
+            } else {
+                gs = false;
+            }
+        }
+    }
+    __device__ __forceinline__ void grant_waiters_tbl() {
+        if (mask[0]) init_round();
     }
 
     // longer traces: scan the candidates in queue order
@@ -414,14 +446,14 @@ struct LaneSim {
             holders -= 1;
             grant_waiters();
         }
-        const uint64_t o = out_base + (bw >> kBusyBits);  // end (harness.py:543)
+        const uint64_t o = out_base + bw_app(bw);  // end (harness.py:543)
         if (P.end) reinterpret_cast<uint32_t*>(P.end)[o] = now;
         // the grant is the busy start: busy runs [grant, grant + busy]
         if (P.grant)
-            reinterpret_cast<uint32_t*>(P.grant)[o] = m ? now - (bw & ((1u << kBusyBits) - 1u)) : SG_NEVER;
+            reinterpret_cast<uint32_t*>(P.grant)[o] = m ? now - bw_busy(bw) : SG_NEVER;
     }
     __device__ __forceinline__ void run_from_busy(uint32_t q, uint32_t m, uint32_t bw, uint32_t now) {
-        const uint32_t b = bw & ((1u << kBusyBits) - 1u);
+        const uint32_t b = bw_busy(bw);
         if (b) {  // busy (harness.py:514-520)
             busy_point(now, +1);
             push(now + b, q);
@@ -438,7 +470,7 @@ struct LaneSim {
                 maxh = max(maxh, (uint32_t)holders);
                 grants += 1;
             } else {                // wait (harness.py:532-536)
-                enqueue(q);
+                enqueue(q, bw);
                 return;
             }
         }
@@ -462,12 +494,17 @@ struct LaneSim {
         I = 0;
         busy_level = holders = 0;
         maxh = grants = pops = 0;
+        gs = false;
+        clsmask = 0;
         // initial pops at t = 0: apps without a cpu step run inline, in index
         // order, each in its own virtual counter block
         for (uint32_t q = s; q < s + z; q++) {
             const uint32_t bw = s_bw[q];
-            counter = (bw >> kBusyBits) << LOGN;
+            counter = bw_app(bw) << LOGN;
             arrive(q, s_mem[q], bw, 0u);
+            if constexpr (TBL) {
+                while (gs && !fail) grant_step();
+            }
             if (fail) return false;
         }
         counter = n_trace << LOGN;
@@ -476,54 +513,59 @@ struct LaneSim {
         uint32_t bwa = 0;
         if (ap < e) {
             bwa = s_bw[ap];
-            ka = ((uint64_t)s_a[ap] << 32) | (((bwa >> kBusyBits) << LOGN) << 8) | ap;
+            ka = ((uint64_t)s_a[ap] << 32) | ((bw_app(bwa) << LOGN) << 8) | ap;
         }
         while (true) {
-            // next event: a granted waiter resumes after every other entry of
-            // its tick; otherwise the smaller of the arrival / busy-end keys
-            const uint64_t kmin = ka < kh ? ka : kh;
-            const bool is_wake = fhead != ftail && (kmin >> 32) > last;
-            if (!is_wake && kmin == kInf) break;
-            const bool is_arr = !is_wake && ka < kh;
-            const bool is_end = !is_wake && !is_arr;
-            const uint32_t fslot = fhead % kLaneFifo;
-            const uint32_t fq = (fifo[(fslot >> 2) * 32] >> ((fslot & 3u) * 8u)) & 0xFFu;
-            const uint32_t q = is_wake ? fq : (uint32_t)kmin & 0xFFu;
-            const uint32_t now = is_wake ? last : (uint32_t)(kmin >> 32);
-            if (is_end) pop();
-            if (is_wake) fhead += 1;
-            if (is_arr) {
-                ap += 1;
-                if (ap < e) {
-                    bwa = s_bw[ap];
-                    ka = ((uint64_t)s_a[ap] << 32) | (((bwa >> kBusyBits) << LOGN) << 8) | ap;
-                } else {
-                    ka = kInf;
+            if (!gs) {
+                // next event: a granted waiter resumes after every other entry of
+                // its tick; otherwise the smaller of the arrival / busy-end keys
+                const uint64_t kmin = ka < kh ? ka : kh;
+                const bool is_wake = fhead != ftail && (kmin >> 32) > last;
+                if (!is_wake && kmin == kInf) break;
+                const bool is_arr = !is_wake && ka < kh;
+                const bool is_end = !is_wake && !is_arr;
+                const uint32_t fslot = fhead % kLaneFifo;
+                const uint32_t fq = (fifo[(fslot >> 2) * 32] >> ((fslot & 3u) * 8u)) & 0xFFu;
+                const uint32_t q = is_wake ? fq : (uint32_t)kmin & 0xFFu;
+                const uint32_t now = is_wake ? last : (uint32_t)(kmin >> 32);
+                if (is_end) pop();
+                if (is_wake) fhead += 1;
+                if (is_arr) {
+                    ap += 1;
+                    if (ap < e) {
+                        bwa = s_bw[ap];
+                        ka = ((uint64_t)s_a[ap] << 32) | ((bw_app(bwa) << LOGN) << 8) | ap;
+                    } else {
+                        ka = kInf;
+                    }
                 }
+                const uint32_t m = s_mem[q];
+                const uint32_t bw = s_bw[q];
+                const uint32_t b = bw_busy(bw);
+                pops += 1;
+                last = now;
+                // arrival: memory-fit admission with bypass, else wait (harness.py:521-536)
+                const bool alloc = is_arr && m != 0;
+                const bool fits = m <= cap - used;
+                const bool enq = alloc && !fits;
+                if (enq) enqueue(q, bw);
+                mem_point(now);
+                if (alloc && fits) {
+                    used += m;
+                    holders += 1;
+                    maxh = max(maxh, (uint32_t)holders);
+                    grants += 1;
+                }
+                // busy (harness.py:514-520) or its end
+                const bool to_busy = !is_end && !enq;
+                const bool start = to_busy && b != 0;
+                busy_point(now, start ? 1 : (is_end ? -1 : 0));
+                if (start) push(now + b, q);
+                if ((to_busy && b == 0) || is_end) end_app(m, bw, now);
             }
-            const uint32_t m = s_mem[q];
-            const uint32_t bw = s_bw[q];
-            const uint32_t b = bw & ((1u << kBusyBits) - 1u);
-            pops += 1;
-            last = now;
-            // arrival: memory-fit admission with bypass, else wait (harness.py:521-536)
-            const bool alloc = is_arr && m != 0;
-            const bool fits = m <= cap - used;
-            const bool enq = alloc && !fits;
-            if (enq) enqueue(q);
-            mem_point(now);
-            if (alloc && fits) {
-                used += m;
-                holders += 1;
-                maxh = max(maxh, (uint32_t)holders);
-                grants += 1;
+            if constexpr (TBL) {
+                if (gs) grant_step();
             }
-            // busy (harness.py:514-520) or its end
-            const bool to_busy = !is_end && !enq;
-            const bool start = to_busy && b != 0;
-            busy_point(now, start ? 1 : (is_end ? -1 : 0));
-            if (start) push(now + b, q);
-            if ((to_busy && b == 0) || is_end) end_app(m, bw, now);
             if (fail) return false;
         }
         return true;
@@ -535,7 +577,7 @@ struct LaneSim {
         for (uint32_t w = 0; w < NW; w++) {
             for (uint64_t bits = mask[w]; bits; bits &= bits - 1) {
                 const uint32_t q = 64u * w + ffs64(bits);
-                const uint64_t o = out_base + (s_bw[q] >> kBusyBits);
+                const uint64_t o = out_base + bw_app(s_bw[q]);
                 if (P.grant) reinterpret_cast<uint32_t*>(P.grant)[o] = SG_NEVER;
                 if (P.end) reinterpret_cast<uint32_t*>(P.end)[o] = SG_NEVER;
                 unf += 1;
@@ -662,7 +704,18 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
             bnd[k] = __ballot_sync(FULL, valid && (prev == ~0u || (prev >> 10) != (ck[k] >> 10)));
             ncls_total += __popc(bnd[k]);
         }
-        if (ncls_total > L.cm_per_trace) {
+        // classes per device (lane d: device d) and their index bounds
+        uint32_t nc_d = 0;
+        for (uint32_t d = 0; d < ndev; d++) {
+            uint32_t c = 0;
+#pragma unroll
+            for (int k = 0; k < K; k++)
+                c += __popc(bnd[k] & __ballot_sync(FULL, ck[k] != ~0u && (ck[k] >> 18) == d));
+            if (lane == d) nc_d = c;
+        }
+        const uint32_t cincl = dev_scan_incl(nc_d, lane);
+        const uint32_t cexcl = cincl - nc_d;
+        if (ncls_total > L.cm_per_trace || __any_sync(FULL, nc_d > kLaneMaxCls)) {
             fail = 1;
         } else {
             for (uint32_t i = lane; i < ncls_total * NW; i += 32) cm[i] = 0ull;
@@ -670,24 +723,17 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
             uint32_t before = 0;  // classes starting before word k
 #pragma unroll
             for (int k = 0; k < K; k++) {
+                const uint32_t c0 = __shfl_sync(FULL, cexcl, ck[k] != ~0u ? (ck[k] >> 18) & 31u : 0u);
                 if (ck[k] != ~0u) {
                     const uint32_t ci = before + __popc(bnd[k] & ((2u << lane) - 1u)) - 1u;
                     const uint32_t apos = ck[k] & 0x3FFu;
                     atomicOr(reinterpret_cast<unsigned long long*>(&cm[ci * NW + (apos >> 6)]),
                              1ull << (apos & 63u));
+                    // the app's class within its device, for the lane's class set
+                    s_bw[apos] |= (ci - c0) << kClsShift;
                 }
                 before += __popc(bnd[k]);
             }
-            // class-index bounds per device
-            uint32_t nc_d = 0;
-            for (uint32_t d = 0; d < ndev; d++) {
-                uint32_t c = 0;
-#pragma unroll
-                for (int k = 0; k < K; k++)
-                    c += __popc(bnd[k] & __ballot_sync(FULL, ck[k] != ~0u && (ck[k] >> 18) == d));
-                if (lane == d) nc_d = c;
-            }
-            const uint32_t cincl = dev_scan_incl(nc_d, lane);
             if (lane < ndev) meta[20 + lane] = (uint16_t)cincl;
         }
     }
@@ -854,7 +900,7 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel
             uint64_t a0;
             uint32_t na;
             lane_trace_range(P, t, a0, na);
-            uint8_t* fb = ws + L.off_fb;
+            uint8_t* fb = ws;  // the whole warp region: the group's lane simulations are done
             uint4* apps_s = reinterpret_cast<uint4*>(fb + P.off_app);
             for (uint32_t i = lane; i < na; i += 32)
                 apps_s[i] = __ldg(reinterpret_cast<const uint4*>(P.apps + a0) + i);
@@ -930,11 +976,10 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
     }
     L.need_tbl = N <= 64 ? 1u : 0u;  // all kinds use the fit table on short traces
     L.cm_per_trace = max(kLaneClassMasks / L.G, 8u);
-    // per-warp region: busy-end heap / staging scratch / fallback TraceSim
+    // per-warp region: busy-end heaps / staging scratch; the fallback
+    // TraceSim overlays the whole warp region once the group's lanes are done
     sim_layout(L.sp, false, false);
-    uint32_t fb = L.sp.warp_bytes;
-    fb = max(fb, kLaneHeap * 32u * 8u);
-    fb = max(fb, N * 16u);
+    const uint32_t fb = max(kLaneHeap * 32u * 8u, N * 16u);
     const uint32_t S32 = N + 4, POR = 80, LTB = kLtBuckets + 16, T4 = N / 4 + 2;  // SlotStride<N>
     uint32_t o = 0;
     L.off_a = o;
@@ -957,7 +1002,7 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
     o = align16(o + kLaneFifoWords * 32u * 4u);
     L.off_fb = o;
     o = align16(o + fb);
-    L.warp_bytes = o;
+    L.warp_bytes = max(o, align16(L.sp.warp_bytes));
     switch (N / 32) {
         case 1: return launch_lane_t<1>(L, stream, grid_out);
         case 2: return launch_lane_t<2>(L, stream, grid_out);
