@@ -41,16 +41,17 @@
 
 namespace sg {
 
-constexpr uint32_t kLaneHeap = 21;          // busy-end heap slots per lane: a 4-ary heap of depth 2
+constexpr uint32_t kLaneHeapN = 21;         // busy-end heap slots per lane, 32-bit keys: 4-ary, depth 2
+constexpr uint32_t kLaneHeapW = 10;         // the same region with 64-bit keys
 constexpr uint32_t kLaneFifoWords = 4;      // wake FIFO: 4 app positions per u32 word
 constexpr uint32_t kLaneFifo = 4 * kLaneFifoWords;
 constexpr uint32_t kLaneClassMasks = 64;    // class masks per warp, split over its trace slots
-constexpr int kLaneWarpsPerBlock = 1;
+constexpr int kLaneWarpsPerBlock = 2;      // two warps share a block's 1 KB smem reservation
 constexpr uint64_t kInf = ~0ull;
 constexpr uint32_t kLtBuckets = 128;        // rank-lookup buckets per trace
 constexpr uint32_t kBusyBits = 21;          // busy < 2^21 on this path; app index above it
 constexpr uint32_t kClsShift = 29;          // s_bw bits 29-31: priority class of the app within its device
-constexpr uint32_t kLaneMaxCls = 8;         // classes per device on this path (more: exact fallback)
+constexpr uint32_t kLaneMaxCls = 8;         // classes per device on this path (more: warp-kernel re-run)
 
 __device__ __forceinline__ uint32_t bw_busy(uint32_t bw) { return bw & ((1u << kBusyBits) - 1u); }
 __device__ __forceinline__ uint32_t bw_app(uint32_t bw) { return (bw >> kBusyBits) & 0xFFu; }
@@ -80,7 +81,7 @@ template <uint32_t N> struct SlotStride {
 
 // meta per trace slot (u16): [0] n, [1] fail (big times / too many classes),
 // [2..10] device bounds in arrival order, [11..18] apps arriving at t = 0 per
-// device, [19..27] class-mask index bounds per device, [28] rank-lookup shift
+// device, [19..27] class-mask index bounds per device, [30] 32-bit event keys allowed
 constexpr uint32_t kMetaU16 = 32;
 
 __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
@@ -157,12 +158,39 @@ __device__ __forceinline__ uint32_t lt_bucket(uint32_t d, uint32_t scale) {
     return min((uint32_t)(((uint64_t)d * scale) >> 32), kLtBuckets - 1u);
 }
 
-template <int K>
+template <int K> struct LogN { static constexpr uint32_t v = K == 1 ? 5 : K == 2 ? 6 : K == 4 ? 7 : 8; };
+
+// Event keys (t, virtual counter, position).  NARROW: one u32, t << (2 LOGN
+// + 1) | counter << LOGN | q, usable when every event time of the trace is
+// below 2^(31 - 2 LOGN) (arrival max + busy sum, checked at staging): each
+// app pushes at most one busy end, so the counter of the initial pop of app i
+// is i and later pushes count up from N (< 2N).  Wide: one u64, t << 32 |
+// counter << 8 | q with the block counters described above.
+template <int K, bool NARROW> struct LaneKey {
+    static constexpr uint32_t LOGN = LogN<K>::v;
+    using T = typename std::conditional<NARROW, uint32_t, uint64_t>::type;
+    static constexpr uint32_t QB = NARROW ? LOGN : 8u;
+    static constexpr uint32_t TS = NARROW ? 2u * LOGN + 1u : 32u;
+    static constexpr T INF = (T)~(T)0;
+    static constexpr uint32_t HCAP = NARROW ? kLaneHeapN : kLaneHeapW;
+    static __device__ __forceinline__ T make(uint32_t t, uint32_t c, uint32_t q) {
+        return ((T)t << TS) | ((T)c << QB) | (T)q;
+    }
+    static __device__ __forceinline__ uint32_t time(T k) { return (uint32_t)(k >> TS); }
+    static __device__ __forceinline__ uint32_t pos(T k) { return (uint32_t)k & ((1u << QB) - 1u); }
+    // counter of the initial pop of app i / first counter of later pushes
+    static __device__ __forceinline__ uint32_t c_init(uint32_t i) { return NARROW ? i : i << LOGN; }
+    static __device__ __forceinline__ uint32_t c_base(uint32_t n) { return NARROW ? 32u * K : n << LOGN; }
+};
+
+template <int K, bool NARROW>
 struct LaneSim {
     static constexpr uint32_t N = 32u * K;
     static constexpr uint32_t NW = (N + 63u) / 64u;  // queue mask words
-    static constexpr uint32_t LOGN = K == 1 ? 5 : K == 2 ? 6 : K == 4 ? 7 : 8;
+    static constexpr uint32_t LOGN = LogN<K>::v;
     static constexpr bool TBL = K <= 2;              // fit table (one mask word)
+    using KY = LaneKey<K, NARROW>;
+    using Key = typename KY::T;
 
     const SimParams& P;
     // trace slot (shared by the trace's lanes), arrival-position order
@@ -176,14 +204,14 @@ struct LaneSim {
     const uint64_t* s_cm;    // class masks of this lane's device, top class first
     uint32_t ncls;
     // this lane's columns
-    uint64_t* heap;          // heap[h * 32]
+    Key* heap;               // heap[h * 32]
     uint32_t* fifo;          // fifo[w * 32]
     uint64_t out_base;       // grant/end index of app 0 of the trace under this policy
     uint32_t cap, used;
     bool prio_pol, mmu, fail;
     uint64_t mask[NW];
     uint32_t hs, fhead, ftail;
-    uint64_t kh;             // heap top (kInf when empty)
+    Key kh;                  // heap top (KY::INF when empty)
     uint32_t counter;
     // statistics (harness.py:373-461 integer forms)
     uint32_t last, mem_t, busy_prev, B;
@@ -214,16 +242,16 @@ struct LaneSim {
     // most two levels, unrolled and predicated, and the four child loads of a
     // level are independent
     __device__ __forceinline__ void push(uint32_t t, uint32_t q) {
-        if (hs >= kLaneHeap) { fail = true; return; }
-        const uint64_t key = ((uint64_t)t << 32) | (counter << 8) | q;
+        if (hs >= KY::HCAP) { fail = true; return; }
+        const Key key = KY::make(t, counter, q);
         counter += 1;
         const uint32_t i = hs++;
         // sift up at most two levels: i -> p1 -> p2
         const uint32_t p1 = i > 0 ? (i - 1) >> 2 : 0u;
-        const uint64_t k1 = i > 0 ? heap[p1 * 32] : 0ull;
+        const Key k1 = i > 0 ? heap[p1 * 32] : (Key)0;
         const bool up1 = i > 0 && key < k1;
         const uint32_t p2 = p1 > 0 ? (p1 - 1) >> 2 : 0u;
-        const uint64_t k2 = up1 && p1 > 0 ? heap[p2 * 32] : 0ull;
+        const Key k2 = up1 && p1 > 0 ? heap[p2 * 32] : (Key)0;
         const bool up2 = up1 && p1 > 0 && key < k2;
         if (up1) heap[i * 32] = k1;
         if (up2) heap[p1 * 32] = k2;
@@ -231,17 +259,17 @@ struct LaneSim {
         heap[dst * 32] = key;
         if (dst == 0) kh = key;
     }
-    // min of the (up to) four children c..c+3 of a node; kInf past the end
-    __device__ __forceinline__ uint64_t min_child(uint32_t c, uint32_t& m) const {
-        const uint64_t k0 = c < hs ? heap[c * 32] : kInf;
-        const uint64_t k1 = c + 1 < hs ? heap[(c + 1) * 32] : kInf;
-        const uint64_t k2 = c + 2 < hs ? heap[(c + 2) * 32] : kInf;
-        const uint64_t k3 = c + 3 < hs ? heap[(c + 3) * 32] : kInf;
+    // min of the (up to) four children c..c+3 of a node; INF past the end
+    __device__ __forceinline__ Key min_child(uint32_t c, uint32_t& m) const {
+        const Key k0 = c < hs ? heap[c * 32] : KY::INF;
+        const Key k1 = c + 1 < hs ? heap[(c + 1) * 32] : KY::INF;
+        const Key k2 = c + 2 < hs ? heap[(c + 2) * 32] : KY::INF;
+        const Key k3 = c + 3 < hs ? heap[(c + 3) * 32] : KY::INF;
         const bool s01 = k1 < k0;
-        const uint64_t x = s01 ? k1 : k0;
+        const Key x = s01 ? k1 : k0;
         const uint32_t ix = s01 ? c + 1 : c;
         const bool s23 = k3 < k2;
-        const uint64_t y = s23 ? k3 : k2;
+        const Key y = s23 ? k3 : k2;
         const uint32_t iy = s23 ? c + 3 : c + 2;
         const bool sxy = y < x;
         m = sxy ? iy : ix;
@@ -249,19 +277,19 @@ struct LaneSim {
     }
     __device__ __forceinline__ void pop() {
         hs -= 1;
-        const uint64_t lastk = heap[hs * 32];
+        const Key lastk = heap[hs * 32];
         // level 1: children 1..4 of the root
         uint32_t m1;
-        const uint64_t k1 = min_child(1u, m1);
+        const Key k1 = min_child(1u, m1);
         const bool down1 = k1 < lastk;
         // level 2: children of m1 (5..20)
         uint32_t m2;
-        const uint64_t k2 = min_child(4u * m1 + 1u, m2);
+        const Key k2 = min_child(4u * m1 + 1u, m2);
         const bool down2 = down1 && k2 < lastk;
         heap[0] = down1 ? k1 : lastk;
         if (down1) heap[m1 * 32] = down2 ? k2 : lastk;
         if (down2) heap[m2 * 32] = lastk;
-        kh = hs == 0 ? kInf : (down1 ? k1 : lastk);
+        kh = hs == 0 ? KY::INF : (down1 ? k1 : lastk);
     }
 
     // ------------------------------------------------- wake FIFO
@@ -489,7 +517,7 @@ struct LaneSim {
 #pragma unroll
         for (uint32_t w = 0; w < NW; w++) mask[w] = 0;
         hs = fhead = ftail = 0;
-        kh = kInf;
+        kh = KY::INF;
         last = mem_t = busy_prev = B = 0;
         I = 0;
         busy_level = holders = 0;
@@ -500,43 +528,43 @@ struct LaneSim {
         // order, each in its own virtual counter block
         for (uint32_t q = s; q < s + z; q++) {
             const uint32_t bw = s_bw[q];
-            counter = bw_app(bw) << LOGN;
+            counter = KY::c_init(bw_app(bw));
             arrive(q, s_mem[q], bw, 0u);
             if constexpr (TBL) {
                 while (gs && !fail) grant_step();
             }
             if (fail) return false;
         }
-        counter = n_trace << LOGN;
+        counter = KY::c_base(n_trace);
         uint32_t ap = s + z;
-        uint64_t ka = kInf;
+        Key ka = KY::INF;
         uint32_t bwa = 0;
         if (ap < e) {
             bwa = s_bw[ap];
-            ka = ((uint64_t)s_a[ap] << 32) | ((bw_app(bwa) << LOGN) << 8) | ap;
+            ka = KY::make(s_a[ap], KY::c_init(bw_app(bwa)), ap);
         }
         while (true) {
             if (!gs) {
                 // next event: a granted waiter resumes after every other entry of
                 // its tick; otherwise the smaller of the arrival / busy-end keys
-                const uint64_t kmin = ka < kh ? ka : kh;
-                const bool is_wake = fhead != ftail && (kmin >> 32) > last;
-                if (!is_wake && kmin == kInf) break;
+                const Key kmin = ka < kh ? ka : kh;
+                const bool is_wake = fhead != ftail && KY::time(kmin) > last;
+                if (!is_wake && kmin == KY::INF) break;
                 const bool is_arr = !is_wake && ka < kh;
                 const bool is_end = !is_wake && !is_arr;
                 const uint32_t fslot = fhead % kLaneFifo;
                 const uint32_t fq = (fifo[(fslot >> 2) * 32] >> ((fslot & 3u) * 8u)) & 0xFFu;
-                const uint32_t q = is_wake ? fq : (uint32_t)kmin & 0xFFu;
-                const uint32_t now = is_wake ? last : (uint32_t)(kmin >> 32);
+                const uint32_t q = is_wake ? fq : KY::pos(kmin);
+                const uint32_t now = is_wake ? last : KY::time(kmin);
                 if (is_end) pop();
                 if (is_wake) fhead += 1;
                 if (is_arr) {
                     ap += 1;
                     if (ap < e) {
                         bwa = s_bw[ap];
-                        ka = ((uint64_t)s_a[ap] << 32) | ((bw_app(bwa) << LOGN) << 8) | ap;
+                        ka = KY::make(s_a[ap], KY::c_init(bw_app(bwa)), ap);
                     } else {
-                        ka = kInf;
+                        ka = KY::INF;
                     }
                 }
                 const uint32_t m = s_mem[q];
@@ -632,6 +660,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
 
     uint64_t key[K];
     bool big = false;
+    uint32_t bsum = 0;  // busy sum (each busy < 2^21 unless `big`)
 #pragma unroll
     for (int k = 0; k < K; k++) {
         const uint32_t i = (uint32_t)k * 32u + lane;
@@ -643,6 +672,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
             if (dv >= ndev) dv = 0;
             key[k] = ((uint64_t)dv << 42) | ((uint64_t)f.x << 10) | i;
             big = big || f.x >= (1u << 31) || f.z >= (1u << kBusyBits);
+            bsum += min(f.z, 1u << kBusyBits);
         }
     }
     uint32_t fail = __any_sync(FULL, big) ? 1u : 0u;
@@ -650,6 +680,10 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
 #pragma unroll
     for (int k = 0; k < K; k++) amax = max(amax, key[k] != kInf ? (uint32_t)(key[k] >> 10) : 0u);
     amax = __reduce_max_sync(FULL, amax);
+    bsum = __reduce_add_sync(FULL, bsum);
+    // every event time is <= max arrival + busy sum: 32-bit keys suffice
+    // when that stays below 2^(32 - TS) (LaneKey)
+    const bool narrow = (uint64_t)amax + bsum < (1ull << (32u - LaneKey<K, true>::TS));
     warp_sort_keys<K>(key, ndev == 1 && amax < (1u << 22), lane);  // device bits sit above bit 41
     __syncwarp();
     // SoA records in arrival order
@@ -809,17 +843,53 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
     if (lane == 0) {
         meta[0] = (uint16_t)na;
         meta[1] = (uint16_t)fail;
+        meta[30] = narrow ? 1u : 0u;
         meta[2] = 0;
         meta[19] = 0;
     }
     __syncwarp();
 }
 
-template <int K>
-__global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel(const LaneParams L) {
+// One lane's simulation of (trace t, device d, policy slot pslot) from the
+// staged slot g.  Returns false if the lane must be re-run by the fallback.
+template <int K, bool NARROW>
+__device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const uint16_t* meta, uint32_t g,
+                                         uint32_t d, uint32_t pslot, uint32_t policy, uint32_t cap_d,
+                                         uint64_t t, uint32_t lane) {
     const SimParams& P = L.sp;
     constexpr uint32_t N = 32u * K;
     constexpr uint32_t NW = (N + 63u) / 64u;
+    using SS = SlotStride<N>;
+    const uint32_t na = meta[0];
+    const uint32_t s0 = meta[2 + d], s1 = meta[3 + d], z = meta[11 + d];
+    uint64_t a0;
+    uint32_t na_unused;
+    lane_trace_range(P, t, a0, na_unused);
+    LaneSim<K, NARROW> sim(P);
+    sim.s_a = reinterpret_cast<const uint32_t*>(ws + L.off_a) + g * SS::S32;
+    sim.s_mem = reinterpret_cast<const uint32_t*>(ws + L.off_mem) + g * SS::S32;
+    sim.s_bw = reinterpret_cast<const uint32_t*>(ws + L.off_bw) + g * SS::S32;
+    sim.s_por = ws + L.off_por + g * SS::POR;
+    sim.s_lt = ws + L.off_lt + g * SS::LTB;
+    sim.lt_lo = reinterpret_cast<const uint32_t*>(sim.s_lt + kLtBuckets)[0];
+    sim.lt_hi = reinterpret_cast<const uint32_t*>(sim.s_lt + kLtBuckets)[1];
+    sim.lt_scale = reinterpret_cast<const uint32_t*>(sim.s_lt + kLtBuckets)[2];
+    sim.s_t4 = reinterpret_cast<const uint64_t*>(ws + L.off_tbl) + g * SS::T4;
+    uint32_t c0 = 0, c1 = 0;
+    if (L.need_cls) { c0 = meta[19 + d]; c1 = meta[20 + d]; }
+    sim.s_cm = reinterpret_cast<const uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW + 1) + c0 * NW;
+    sim.ncls = c1 - c0;
+    sim.heap = reinterpret_cast<typename LaneSim<K, NARROW>::Key*>(ws + L.off_fb) + lane;
+    sim.fifo = reinterpret_cast<uint32_t*>(ws + L.off_fifo) + lane;
+    sim.out_base = (uint64_t)pslot * P.n_apps_total + a0;
+    if (!sim.run(na, s0, s1, z, policy, cap_d)) return false;
+    sim.finish(((uint64_t)pslot * P.n_traces + t) * P.ndev + d, s1 - s0);
+    return true;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel(const LaneParams L) {
+    const SimParams& P = L.sp;
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
@@ -853,40 +923,16 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel
         }
 
         bool fail = false;
+        const uint16_t* meta = reinterpret_cast<const uint16_t*>(ws + L.off_meta) + g * kMetaU16;
+        // 32-bit event keys when every trace of the group allows them (warp-uniform)
+        const bool narrow = __all_sync(FULL, g >= gcount || meta[30] != 0);
         if (g < gcount) {
-            const uint64_t t = t0 + g;
-            const uint16_t* meta = reinterpret_cast<const uint16_t*>(ws + L.off_meta) + g * kMetaU16;
-            const uint32_t na = meta[0];
-            if (meta[1]) {
+            if (meta[1])
                 fail = true;
-            } else {
-                const uint32_t s0 = meta[2 + d], s1 = meta[3 + d], z = meta[11 + d];
-                uint64_t a0;
-                uint32_t na_unused;
-                lane_trace_range(P, t, a0, na_unused);
-                LaneSim<K> sim(P);
-                using SS = SlotStride<N>;
-                sim.s_a = reinterpret_cast<const uint32_t*>(ws + L.off_a) + g * SS::S32;
-                sim.s_mem = reinterpret_cast<const uint32_t*>(ws + L.off_mem) + g * SS::S32;
-                sim.s_bw = reinterpret_cast<const uint32_t*>(ws + L.off_bw) + g * SS::S32;
-                sim.s_por = ws + L.off_por + g * SS::POR;
-                sim.s_lt = ws + L.off_lt + g * SS::LTB;
-                sim.lt_lo = reinterpret_cast<const uint32_t*>(sim.s_lt + kLtBuckets)[0];
-                sim.lt_hi = reinterpret_cast<const uint32_t*>(sim.s_lt + kLtBuckets)[1];
-                sim.lt_scale = reinterpret_cast<const uint32_t*>(sim.s_lt + kLtBuckets)[2];
-                sim.s_t4 = reinterpret_cast<const uint64_t*>(ws + L.off_tbl) + g * SS::T4;
-                uint32_t c0 = 0, c1 = 0;
-                if (L.need_cls) { c0 = meta[19 + d]; c1 = meta[20 + d]; }
-                sim.s_cm = reinterpret_cast<const uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW + 1) + c0 * NW;
-                sim.ncls = c1 - c0;
-                sim.heap = reinterpret_cast<uint64_t*>(ws + L.off_fb) + lane;
-                sim.fifo = reinterpret_cast<uint32_t*>(ws + L.off_fifo) + lane;
-                sim.out_base = (uint64_t)pslot * P.n_apps_total + a0;
-                if (sim.run(na, s0, s1, z, policy, cap_d))
-                    sim.finish(((uint64_t)pslot * P.n_traces + t) * ndev + d, s1 - s0);
-                else
-                    fail = true;
-            }
+            else if (narrow)
+                fail = !lane_run<K, true>(L, ws, meta, g, d, pslot, policy, cap_d, t0 + g, lane);
+            else
+                fail = !lane_run<K, false>(L, ws, meta, g, d, pslot, policy, cap_d, t0 + g, lane);
         }
         __syncwarp();
         // exact fallback: the whole warp re-simulates each failed lane
@@ -979,7 +1025,7 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
     // per-warp region: busy-end heaps / staging scratch; the fallback
     // TraceSim overlays the whole warp region once the group's lanes are done
     sim_layout(L.sp, false, false);
-    const uint32_t fb = max(kLaneHeap * 32u * 8u, N * 16u);
+    const uint32_t fb = max(max(kLaneHeapN * 32u * 4u, kLaneHeapW * 32u * 8u), N * 16u);
     const uint32_t S32 = N + 4, POR = 80, LTB = kLtBuckets + 16, T4 = N / 4 + 2;  // SlotStride<N>
     uint32_t o = 0;
     L.off_a = o;

@@ -11,9 +11,11 @@ from collections import defaultdict
 src_file = "paper_1712_04495_b200/csrc/sgpu_lane.cu"
 lines = open(src_file).read().split("\n")
 # region starts: (regex on the source line, name)
-marks = [(r"void push\(", "heap push"), (r"void pop\(", "heap pop"), (r"void wake\(", "wake fifo"),
-         (r"void enqueue\(", "queue mask"), (r"uint32_t fit_rank\(", "fit_rank"),
-         (r"void grant_one\(", "grant_one"), (r"void grant_waiters\(\)", "grant_waiters"),
+marks = [(r"void push\(", "heap push"), (r"uint64_t min_child\(", "heap pop"), (r"void pop\(", "heap pop"),
+         (r"void wake\(", "wake fifo"), (r"void enqueue\(", "queue mask"),
+         (r"uint32_t fit_rank\(", "fit_rank/fit_set"), (r"void grant_one\(", "grant (scan path)"),
+         (r"void init_round\(", "grant round init"), (r"void grant_step\(", "grant step"),
+         (r"void grant_waiters_tbl\(", "grant round init"), (r"void grant_waiters_scan\(", "grant (scan path)"),
          (r"void end_app\(", "end_app/outputs"), (r"void run_from_busy\(", "advance (phase 0)"),
          (r"bool run\(", "event loop"), (r"void finish\(", "finish/stats"),
          (r"void lane_trace_range\(", "staging"), (r"__global__", "kernel body"),
