@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
 #include <thread>
 #include <immintrin.h>
 #include <vector>
@@ -304,6 +305,10 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
         if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "allocating pipeline buffers"); }
     }
     const uint64_t n_apps_total = N * napps;
+    // SGPU_PIPE_TRACE=1: print host-side pipeline timings (stderr)
+    static const bool trace = getenv("SGPU_PIPE_TRACE") != nullptr;
+    const auto tp0 = std::chrono::steady_clock::now();
+    auto ms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count(); };
     uint64_t chunk = 0;
     for (uint64_t t0 = 0; t0 < N; t0 += chunk_traces, chunk++) {
         Buf& b = B[chunk % NBUF];
@@ -359,20 +364,28 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
         const bool avx2 = __builtin_cpu_supports("avx2");
         unsigned nthr = std::thread::hardware_concurrency();
         nthr = nthr == 0 ? 1 : (nthr > 16 ? 16 : nthr);
+        if (const char* ev = getenv("SGPU_HOST_THREADS")) {  // tuning knob
+            const int v = atoi(ev);
+            if (v > 0 && v <= 256) nthr = (unsigned)v;
+        }
         std::vector<std::vector<uint64_t>> ov(nthr);
         std::vector<cudaError_t> errs(nthr, cudaSuccess);
         std::vector<std::thread> pool;
+        if (trace) fprintf(stderr, "[pipe] enqueued %zu chunks at %.2f ms\n", chunks.size(), ms());
         for (unsigned w = 0; w < nthr; w++) {
             pool.emplace_back([&, w]() {
                 for (const auto& c : chunks) {
                     const cudaError_t ce = cudaEventSynchronize(c.done);
                     if (ce != cudaSuccess) { errs[w] = ce; return; }
+                    const double tr = ms();
                     const uint64_t lo = c.t0 + c.nt * w / nthr, hi = c.t0 + c.nt * (w + 1) / nthr;
                     derive_grants(in, out, s.npol, lo, hi, ov[w], avx2);
+                    if (trace && w == 0) fprintf(stderr, "[pipe] chunk %llu ready %.2f derived %.2f ms\n", (unsigned long long)(c.t0 / chunk_traces), tr, ms());
                 }
             });
         }
         for (auto& th : pool) th.join();
+        if (trace) fprintf(stderr, "[pipe] joined %.2f ms\n", ms());
         for (unsigned w = 0; w < nthr; w++) {
             if (errs[w] != cudaSuccess) { cleanup(); return cuda_fail(errs[w], "pipeline"); }
             overflow.insert(overflow.end(), ov[w].begin(), ov[w].end());
