@@ -293,18 +293,14 @@ struct LaneSim {
     }
 
     // ------------------------------------------------- wake FIFO
+    // byte slots: slot j of this lane is byte j & 3 of word (j >> 2) of its column
+    __device__ __forceinline__ uint8_t* fifo_slot(uint32_t j) const {
+        return reinterpret_cast<uint8_t*>(fifo + ((j % kLaneFifo) >> 2) * 32) + (j & 3u);
+    }
     __device__ __forceinline__ void wake(uint32_t q) {
         if (ftail - fhead >= kLaneFifo) { fail = true; return; }
-        const uint32_t slot = ftail % kLaneFifo;
-        uint32_t* w = fifo + (slot >> 2) * 32;
-        const uint32_t sh = (slot & 3u) * 8u;
-        *w = (*w & ~(0xFFu << sh)) | (q << sh);
+        *fifo_slot(ftail) = (uint8_t)q;
         ftail += 1;
-    }
-    __device__ __forceinline__ uint32_t unwake() {
-        const uint32_t slot = fhead % kLaneFifo;
-        fhead += 1;
-        return (fifo[(slot >> 2) * 32] >> ((slot & 3u) * 8u)) & 0xFFu;
     }
 
     // ------------------------------------------------- wait queue
@@ -547,14 +543,28 @@ struct LaneSim {
             if (!gs) {
                 // next event: a granted waiter resumes after every other entry of
                 // its tick; otherwise the smaller of the arrival / busy-end keys
-                const Key kmin = ka < kh ? ka : kh;
+                Key kmin = ka < kh ? ka : kh;
+                if (fhead != ftail && KY::time(kmin) > last) {
+                    // every other entry of tick `last` is done: the woken
+                    // waiters resume in grant order, each starting its busy
+                    // step (harness.py:514-520, 558); a zero-length busy step
+                    // frees at once and is handled below as an event
+                    do {
+                        const uint32_t wq = *fifo_slot(fhead);
+                        const uint32_t wb = bw_busy(s_bw[wq]);
+                        if (wb == 0) break;
+                        fhead += 1;
+                        pops += 1;
+                        busy_point(last, +1);
+                        push(last + wb, wq);
+                    } while (fhead != ftail);
+                    kmin = ka < kh ? ka : kh;
+                }
                 const bool is_wake = fhead != ftail && KY::time(kmin) > last;
                 if (!is_wake && kmin == KY::INF) break;
                 const bool is_arr = !is_wake && ka < kh;
                 const bool is_end = !is_wake && !is_arr;
-                const uint32_t fslot = fhead % kLaneFifo;
-                const uint32_t fq = (fifo[(fslot >> 2) * 32] >> ((fslot & 3u) * 8u)) & 0xFFu;
-                const uint32_t q = is_wake ? fq : KY::pos(kmin);
+                const uint32_t q = is_wake ? (uint32_t)*fifo_slot(fhead) : KY::pos(kmin);
                 const uint32_t now = is_wake ? last : KY::time(kmin);
                 if (is_end) pop();
                 if (is_wake) fhead += 1;
