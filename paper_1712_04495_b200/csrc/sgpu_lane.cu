@@ -726,7 +726,43 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
         if (lane == d) { cnt_d = c; z_d = zc; }
     }
     const uint32_t dincl = dev_scan_incl(cnt_d, lane);
-    if (L.need_cls) {
+    uint32_t pmax = 0;
+#pragma unroll
+    for (int k = 0; k < K; k++) pmax = max(pmax, key[k] != kInf ? prk[k] : 0u);
+    pmax = __reduce_max_sync(FULL, pmax);
+    if (L.need_cls && ndev == 1 && pmax < 32) {
+        // one device, priorities below 32: the classes (policy.py:58-63) are
+        // the distinct priorities, highest first; class index = number of
+        // distinct priorities above the app's own
+        uint64_t* cm = reinterpret_cast<uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW + 1);
+        uint32_t pres = 0;
+#pragma unroll
+        for (int k = 0; k < K; k++) pres |= key[k] != kInf ? 1u << prk[k] : 0u;
+        pres = __reduce_or_sync(FULL, pres);
+        const uint32_t ncls_total = __popc(pres);
+        if (ncls_total > L.cm_per_trace || ncls_total > kLaneMaxCls) {
+            fail = 1;
+        } else {
+            uint32_t cls[K];
+#pragma unroll
+            for (int k = 0; k < K; k++) {
+                cls[k] = ~0u;
+                if (key[k] != kInf) {
+                    cls[k] = __popc((uint32_t)((uint64_t)pres >> (prk[k] + 1u)));
+                    s_bw[(uint32_t)k * 32u + lane] |= cls[k] << kClsShift;
+                }
+            }
+            for (uint32_t c = 0; c < ncls_total; c++) {
+#pragma unroll
+                for (uint32_t w = 0; w < NW; w++) {
+                    const uint32_t lo = __ballot_sync(FULL, cls[min(2u * w, (uint32_t)K - 1u)] == c && 2u * w < (uint32_t)K);
+                    const uint32_t hi = __ballot_sync(FULL, cls[min(2u * w + 1u, (uint32_t)K - 1u)] == c && 2u * w + 1u < (uint32_t)K);
+                    if (lane == 0) cm[c * NW + w] = ((uint64_t)hi << 32) | lo;
+                }
+            }
+            if (lane == 0) meta[20] = (uint16_t)ncls_total;
+        }
+    } else if (L.need_cls) {
         // classes = (device, priority) groups, highest priority first
         // (policy.py:58-63); one mask of arrival positions per class
         uint64_t* cm = reinterpret_cast<uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW + 1);

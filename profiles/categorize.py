@@ -11,7 +11,7 @@ from collections import defaultdict
 src_file = "paper_1712_04495_b200/csrc/sgpu_lane.cu"
 lines = open(src_file).read().split("\n")
 # region starts: (regex on the source line, name)
-marks = [(r"void push\(", "heap push"), (r"uint64_t min_child\(", "heap pop"), (r"void pop\(", "heap pop"),
+marks = [(r"void push\(", "heap push"), (r"min_child\(", "heap pop"), (r"void pop\(", "heap pop"),
          (r"void wake\(", "wake fifo"), (r"void enqueue\(", "queue mask"),
          (r"uint32_t fit_rank\(", "fit_rank/fit_set"), (r"void grant_one\(", "grant (scan path)"),
          (r"void init_round\(", "grant round init"), (r"void grant_step\(", "grant step"),
