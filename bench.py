@@ -343,6 +343,7 @@ def main():
         dist.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
     kern_ms = [a.elapsed_time(b) for a, b in ev]
+    print(f"[bench] K1 per-step ms: {' '.join(f'{x:.2f}' for x in kern_ms)}", file=sys.stderr)
     tt = torch.tensor([elapsed_ms, max(kern_ms)], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)

@@ -21,7 +21,7 @@ LIB_NAME = "libsgpu.so"
 LIB_PATH = os.path.join(HERE, LIB_NAME)
 
 SOURCES = ["sgpu_sim.cu", "sgpu_lane.cu", "sgpu_aux.cu", "sgpu_abi.cu"]
-DEPS = SOURCES + ["sgpu_common.cuh", "sgpu_internal.h", "sgpu_tracesim.cuh"]
+DEPS = SOURCES + ["sgpu_common.cuh", "sgpu_internal.h", "sgpu_tracesim.cuh", "sgpu_lanesim.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

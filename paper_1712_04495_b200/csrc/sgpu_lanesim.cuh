@@ -1,0 +1,525 @@
+// sgpu_lanesim.cuh — the per-lane simulation of K1 v5 (LaneSim): one
+// (trace, device, policy) simulated by one thread from a staged trace slot.
+// Included by sgpu_lane.cu (device code) and, with the shims below, compiled
+// by the host C++ compiler for tests/test_lanesim_host.py, which checks this
+// exact decision logic against the oracle on CPU.  Semantics: see the header
+// of sgpu_lane.cu and SURVEY.md Appendix A.
+#pragma once
+
+#include <cstdint>
+#include <type_traits>
+
+#ifdef __CUDACC__
+#include "sgpu_tracesim.cuh"
+#define SG_HD __device__ __forceinline__
+#else
+// host build: plain C++ (the only intrinsic used is find-first-set)
+#include <algorithm>
+#include "../../include/sgpu.h"
+#define SG_HD inline
+namespace sg {
+using std::max;
+using std::min;
+struct SimParams {  // the two output arrays LaneSim writes
+    void* grant;
+    void* end;
+};
+inline int __ffsll(long long x) { return __builtin_ffsll(x); }
+}  // namespace sg
+#endif
+
+namespace sg {
+
+constexpr uint32_t kLaneHeapN = 21;         // busy-end heap slots per lane, 32-bit keys: 4-ary, depth 2
+constexpr uint32_t kLaneHeapW = 10;         // the same region with 64-bit keys
+constexpr uint32_t kLaneFifoWords = 4;      // wake FIFO: 4 app positions per u32 word
+constexpr uint32_t kLaneFifo = 4 * kLaneFifoWords;
+constexpr uint64_t kInf = ~0ull;
+constexpr uint32_t kLtBuckets = 128;        // rank-lookup buckets per trace
+constexpr uint32_t kBusyBits = 21;          // busy < 2^21 on this path; app index above it
+constexpr uint32_t kClsShift = 29;          // s_bw bits 29-31: priority class of the app within its device
+constexpr uint32_t kLaneMaxCls = 8;         // classes per device on this path (more: warp-kernel re-run)
+
+SG_HD uint32_t bw_busy(uint32_t bw) { return bw & ((1u << kBusyBits) - 1u); }
+SG_HD uint32_t bw_app(uint32_t bw) { return (bw >> kBusyBits) & 0xFFu; }
+SG_HD uint32_t bw_cls(uint32_t bw) { return bw >> kClsShift; }
+
+
+SG_HD uint32_t ffs64(uint64_t x) { return (uint32_t)__ffsll((long long)x) - 1u; }
+
+// Rank-lookup bucket of a request d = mem - lo >= 0: monotone in d.
+SG_HD uint32_t lt_bucket(uint32_t d, uint32_t scale) {
+    return min((uint32_t)(((uint64_t)d * scale) >> 32), kLtBuckets - 1u);
+}
+
+template <int K> struct LogN { static constexpr uint32_t v = K == 1 ? 5 : K == 2 ? 6 : K == 4 ? 7 : 8; };
+
+// Event keys (t, virtual counter, position).  NARROW: one u32, t << (2 LOGN
+// + 1) | counter << LOGN | q, usable when every event time of the trace is
+// below 2^(31 - 2 LOGN) (arrival max + busy sum, checked at staging): each
+// app pushes at most one busy end, so the counter of the initial pop of app i
+// is i and later pushes count up from N (< 2N).  Wide: one u64, t << 32 |
+// counter << 8 | q with the block counters described above.
+template <int K, bool NARROW> struct LaneKey {
+    static constexpr uint32_t LOGN = LogN<K>::v;
+    using T = typename std::conditional<NARROW, uint32_t, uint64_t>::type;
+    static constexpr uint32_t QB = NARROW ? LOGN : 8u;
+    static constexpr uint32_t TS = NARROW ? 2u * LOGN + 1u : 32u;
+    static constexpr T INF = (T)~(T)0;
+    static constexpr uint32_t HCAP = NARROW ? kLaneHeapN : kLaneHeapW;
+    static SG_HD T make(uint32_t t, uint32_t c, uint32_t q) {
+        return ((T)t << TS) | ((T)c << QB) | (T)q;
+    }
+    static SG_HD uint32_t time(T k) { return (uint32_t)(k >> TS); }
+    static SG_HD uint32_t pos(T k) { return (uint32_t)k & ((1u << QB) - 1u); }
+    // counter of the initial pop of app i / first counter of later pushes
+    static SG_HD uint32_t c_init(uint32_t i) { return NARROW ? i : i << LOGN; }
+    static SG_HD uint32_t c_base(uint32_t n) { return NARROW ? 32u * K : n << LOGN; }
+};
+
+template <int K, bool NARROW>
+struct LaneSim {
+    static constexpr uint32_t N = 32u * K;
+    static constexpr uint32_t NW = (N + 63u) / 64u;  // queue mask words
+    static constexpr uint32_t LOGN = LogN<K>::v;
+    static constexpr bool TBL = K <= 2;              // fit table (one mask word)
+    using KY = LaneKey<K, NARROW>;
+    using Key = typename KY::T;
+
+    const SimParams& P;
+    // trace slot (shared by the trace's lanes), arrival-position order
+    const uint32_t* s_a;     // arrival tick
+    const uint32_t* s_mem;   // request MiB
+    const uint32_t* s_bw;    // busy | app << kBusyBits | class << kClsShift
+    const uint8_t* s_por;    // position of the r-th smallest request (N past the end)
+    const uint8_t* s_lt;     // s_lt[j] = #requests in buckets < j
+    uint32_t lt_lo, lt_hi, lt_scale;
+    const uint64_t* s_t4;    // T[4j]: positions of the 4j smallest requests
+    const uint64_t* s_cm;    // class masks of this lane's device, top class first
+    uint32_t ncls;
+    // this lane's columns
+    Key* heap;               // heap[h * 32]
+    uint32_t* fifo;          // fifo[w * 32]
+    uint64_t out_base;       // grant/end index of app 0 of the trace under this policy
+    uint32_t cap, used;
+    bool prio_pol, mmu, fail;
+    uint64_t mask[NW];
+    uint32_t hs, fhead, ftail;
+    Key kh;                  // heap top (KY::INF when empty)
+    uint32_t counter;
+    // statistics (harness.py:373-461 integer forms)
+    uint32_t last, mem_t, busy_prev, B;
+    uint64_t I;
+    int32_t busy_level, holders;
+    uint32_t maxh, grants, pops;
+    // incremental grant_waiters state (fit-table path): one select_grants
+    // step per loop iteration while `gs` (harness.py:545-558)
+    bool gs;
+    uint32_t clsmask;        // priority classes with waiting entries (bit c: class c, top = 0)
+    uint32_t gc, gbud, gb0, gg;
+    uint64_t gcand, grem;    // unscanned candidates / waiting members of the round's class
+
+    SG_HD LaneSim(const SimParams& p) : P(p) {}
+
+    SG_HD void mem_point(uint32_t now) {
+        I += (uint64_t)used * (now - mem_t);
+        mem_t = now;
+    }
+    SG_HD void busy_point(uint32_t now, int32_t delta) {
+        B += busy_level > 0 ? now - busy_prev : 0u;
+        busy_prev = now;
+        busy_level += delta;
+    }
+
+    // ------------------------------------------------- busy-end heap
+    // 4-ary min-heap of at most 21 keys (root + 4 + 16): every sift is at
+    // most two levels, unrolled and predicated, and the four child loads of a
+    // level are independent
+    SG_HD void push(uint32_t t, uint32_t q) {
+        if (hs >= KY::HCAP) { fail = true; return; }
+        const Key key = KY::make(t, counter, q);
+        counter += 1;
+        const uint32_t i = hs++;
+        // sift up at most two levels: i -> p1 -> p2
+        const uint32_t p1 = i > 0 ? (i - 1) >> 2 : 0u;
+        const Key k1 = i > 0 ? heap[p1 * 32] : (Key)0;
+        const bool up1 = i > 0 && key < k1;
+        const uint32_t p2 = p1 > 0 ? (p1 - 1) >> 2 : 0u;
+        const Key k2 = up1 && p1 > 0 ? heap[p2 * 32] : (Key)0;
+        const bool up2 = up1 && p1 > 0 && key < k2;
+        if (up1) heap[i * 32] = k1;
+        if (up2) heap[p1 * 32] = k2;
+        const uint32_t dst = up2 ? p2 : (up1 ? p1 : i);
+        heap[dst * 32] = key;
+        if (dst == 0) kh = key;
+    }
+    // min of the (up to) four children c..c+3 of a node; INF past the end
+    SG_HD Key min_child(uint32_t c, uint32_t& m) const {
+        const Key k0 = c < hs ? heap[c * 32] : KY::INF;
+        const Key k1 = c + 1 < hs ? heap[(c + 1) * 32] : KY::INF;
+        const Key k2 = c + 2 < hs ? heap[(c + 2) * 32] : KY::INF;
+        const Key k3 = c + 3 < hs ? heap[(c + 3) * 32] : KY::INF;
+        const bool s01 = k1 < k0;
+        const Key x = s01 ? k1 : k0;
+        const uint32_t ix = s01 ? c + 1 : c;
+        const bool s23 = k3 < k2;
+        const Key y = s23 ? k3 : k2;
+        const uint32_t iy = s23 ? c + 3 : c + 2;
+        const bool sxy = y < x;
+        m = sxy ? iy : ix;
+        return sxy ? y : x;
+    }
+    SG_HD void pop() {
+        hs -= 1;
+        const Key lastk = heap[hs * 32];
+        // level 1: children 1..4 of the root
+        uint32_t m1;
+        const Key k1 = min_child(1u, m1);
+        const bool down1 = k1 < lastk;
+        // level 2: children of m1 (5..20)
+        uint32_t m2;
+        const Key k2 = min_child(4u * m1 + 1u, m2);
+        const bool down2 = down1 && k2 < lastk;
+        heap[0] = down1 ? k1 : lastk;
+        if (down1) heap[m1 * 32] = down2 ? k2 : lastk;
+        if (down2) heap[m2 * 32] = lastk;
+        kh = hs == 0 ? KY::INF : (down1 ? k1 : lastk);
+    }
+
+    // ------------------------------------------------- wake FIFO
+    // byte slots: slot j of this lane is byte j & 3 of word (j >> 2) of its column
+    SG_HD uint8_t* fifo_slot(uint32_t j) const {
+        return reinterpret_cast<uint8_t*>(fifo + ((j % kLaneFifo) >> 2) * 32) + (j & 3u);
+    }
+    SG_HD void wake(uint32_t q) {
+        if (ftail - fhead >= kLaneFifo) { fail = true; return; }
+        *fifo_slot(ftail) = (uint8_t)q;
+        ftail += 1;
+    }
+
+    // ------------------------------------------------- wait queue
+    SG_HD void enqueue(uint32_t q, uint32_t bw) {
+#pragma unroll
+        for (uint32_t w = 0; w < NW; w++)
+            if (w == (q >> 6)) mask[w] |= 1ull << (q & 63u);
+        clsmask |= 1u << bw_cls(bw);
+    }
+    // number of requests <= budget in the trace: bucket lookup (kLtBuckets
+    // spread linearly over [smallest, largest] request), then a short
+    // forward scan of the sorted requests inside the bucket
+    SG_HD uint32_t fit_rank(uint32_t budget) const {
+        if (budget > lt_hi) return N;
+        const uint32_t bi = budget < lt_lo ? 0u : lt_bucket(budget - lt_lo, lt_scale);
+        uint32_t r = s_lt[bi];
+        while (s_mem[s_por[r]] <= budget) r += 1;  // s_mem[N] = ~0 ends the scan
+        return r;
+    }
+    // T[r]: positions of the r smallest requests = T[4 floor(r/4)] + up to 3
+    SG_HD uint64_t fit_set(uint32_t r) const {
+        uint64_t t = s_t4[r >> 2];
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(s_por + (r & ~3u));
+        const uint32_t k = r & 3u;
+        if (k > 0) t |= 1ull << (w & 0xFFu);
+        if (k > 1) t |= 1ull << ((w >> 8) & 0xFFu);
+        if (k > 2) t |= 1ull << ((w >> 16) & 0xFFu);
+        return t;
+    }
+    SG_HD void grant_one(uint32_t q, uint32_t m, uint32_t& budget, uint32_t& g) {
+#pragma unroll
+        for (uint32_t w = 0; w < NW; w++)
+            if (w == (q >> 6)) mask[w] &= ~(1ull << (q & 63u));
+        budget -= m;
+        g += 1;
+        wake(q);
+    }
+
+    // grant_waiters (harness.py:545-558) + select_grants (policy.py:52-74)
+    SG_HD void grant_waiters() {
+        if constexpr (TBL) grant_waiters_tbl();
+        else grant_waiters_scan();
+    }
+
+    // <= 64 apps: grant_waiters as a sequence of steps, one per loop
+    // iteration, so a lane granting several waiters does not hold the whole
+    // warp in a nested loop; the lane pops no event until it is done, so the
+    // order is the reference's.  One code path for all four kinds keeps the
+    // lanes of a warp (mixed policies) converged.  A round: the top class
+    // (all waiting entries for FIFO/MMU, policy.py:58-63); a step: fit =
+    // cand & T[#requests <= budget]; FIFO takes the head iff it fits, MMU the
+    // lowest fit (policy.py:65-73); both continue above the granted position.
+    SG_HD void init_round() {
+        uint64_t cm = ~0ull;
+        if (prio_pol) {
+            gc = ffs64(clsmask);  // clsmask != 0 whenever the queue is not empty
+            cm = s_cm[gc];
+        }
+        gcand = mask[0] & cm;
+        grem = gcand;
+        gs = gcand != 0;
+        gb0 = gbud = cap - used;
+        gg = 0;
+    }
+    SG_HD void grant_step() {
+        const uint64_t fit = gcand & fit_set(fit_rank(gbud));
+        const uint64_t head = gcand & (0ull - gcand);
+        const uint64_t pick = mmu ? fit : (fit & head);
+        if (pick) {
+            const uint32_t q = ffs64(pick);
+            const uint64_t bit = 1ull << q;
+            mask[0] &= ~bit;
+            grem &= ~bit;
+            gbud -= s_mem[q];
+            gg += 1;
+            wake(q);
+            gcand &= ~((2ull << q) - 1ull);
+        }
+        if (!pick || !gcand) {  // the round ends
+            if (gg) {
+                mem_point(last);
+                used += gb0 - gbud;
+                holders += (int32_t)gg;
+                maxh = max(maxh, (uint32_t)holders);
+                grants += gg;
+            }
+            // the top class drained: the next class is served in the same
+            // tick (harness.py:547-550); otherwise the next round is empty
+            if (prio_pol && gg && !grem) {
+                clsmask &= ~(1u << gc);
+                if (clsmask) init_round();
+                else gs = false;
+            } else {
+                gs = false;
+            }
+        }
+    }
+    SG_HD void grant_waiters_tbl() {
+        if (mask[0]) init_round();
+    }
+
+    // longer traces: scan the candidates in queue order
+    SG_HD void grant_waiters_scan() {
+        uint32_t c = 0;  // current class (priority kinds)
+        while (true) {
+            // candidate set: the waiting entries of the top class (policy.py:58-63)
+            uint64_t cand[NW];
+            bool any = false;
+            if (prio_pol) {
+                while (c < ncls) {
+#pragma unroll
+                    for (uint32_t w = 0; w < NW; w++) {
+                        cand[w] = mask[w] & s_cm[c * NW + w];
+                        any = any || cand[w] != 0;
+                    }
+                    if (any) break;
+                    c += 1;
+                }
+            } else {
+#pragma unroll
+                for (uint32_t w = 0; w < NW; w++) {
+                    cand[w] = mask[w];
+                    any = any || cand[w] != 0;
+                }
+            }
+            if (!any) return;
+            const uint32_t budget0 = cap - used;
+            uint32_t budget = budget0, g = 0;
+            // FIFO: grant the head while it fits; MMU: skip misfits
+            bool stop = false;
+#pragma unroll
+            for (uint32_t w = 0; w < NW; w++) {
+                uint64_t bits = cand[w];
+                while (bits && !stop) {
+                    const uint32_t q = 64u * w + ffs64(bits);
+                    bits &= bits - 1;
+                    const uint32_t m = s_mem[q];
+                    if (m <= budget) {
+                        grant_one(q, m, budget, g);
+                        if (fail) return;
+                    } else if (!mmu) {
+                        stop = true;
+                    }
+                }
+            }
+            if (g) {
+                mem_point(last);
+                used += budget0 - budget;
+                holders += (int32_t)g;
+                maxh = max(maxh, (uint32_t)holders);
+                grants += g;
+            }
+            if (!prio_pol || g == 0) return;
+            bool left = false;
+#pragma unroll
+            for (uint32_t w = 0; w < NW; w++) left = left || (mask[w] & s_cm[c * NW + w]) != 0;
+            if (left) return;
+            c += 1;
+        }
+    }
+
+    // --------------------------------------------------------- advance
+    SG_HD void end_app(uint32_t m, uint32_t bw, uint32_t now) {
+        if (m) {  // free -> grant_waiters (harness.py:537-542)
+            mem_point(now);
+            used -= m;
+            holders -= 1;
+            grant_waiters();
+        }
+        const uint64_t o = out_base + bw_app(bw);  // end (harness.py:543)
+        if (P.end) reinterpret_cast<uint32_t*>(P.end)[o] = now;
+        // the grant is the busy start: busy runs [grant, grant + busy]
+        if (P.grant)
+            reinterpret_cast<uint32_t*>(P.grant)[o] = m ? now - bw_busy(bw) : SG_NEVER;
+    }
+    SG_HD void run_from_busy(uint32_t q, uint32_t m, uint32_t bw, uint32_t now) {
+        const uint32_t b = bw_busy(bw);
+        if (b) {  // busy (harness.py:514-520)
+            busy_point(now, +1);
+            push(now + b, q);
+            return;
+        }
+        end_app(m, bw, now);
+    }
+    SG_HD void arrive(uint32_t q, uint32_t m, uint32_t bw, uint32_t now) {
+        if (m) {
+            if (m <= cap - used) {  // arrival bypass (harness.py:521-531)
+                mem_point(now);
+                used += m;
+                holders += 1;
+                maxh = max(maxh, (uint32_t)holders);
+                grants += 1;
+            } else {                // wait (harness.py:532-536)
+                enqueue(q, bw);
+                return;
+            }
+        }
+        run_from_busy(q, m, bw, now);
+    }
+
+    // Simulate device range [s, e) of the slot's arrival order (z apps arrive
+    // at t = 0).  Returns false if this lane must be re-run by the fallback.
+    SG_HD bool run(uint32_t n_trace, uint32_t s, uint32_t e, uint32_t z,
+                                        uint32_t policy, uint32_t cap_mib) {
+        cap = cap_mib;
+        used = 0;
+        prio_pol = policy >= SG_POLICY_PFIFO;
+        mmu = (policy & 1u) != 0;
+        fail = false;
+#pragma unroll
+        for (uint32_t w = 0; w < NW; w++) mask[w] = 0;
+        hs = fhead = ftail = 0;
+        kh = KY::INF;
+        last = mem_t = busy_prev = B = 0;
+        I = 0;
+        busy_level = holders = 0;
+        maxh = grants = pops = 0;
+        gs = false;
+        clsmask = 0;
+        // initial pops at t = 0: apps without a cpu step run inline, in index
+        // order, each in its own virtual counter block
+        for (uint32_t q = s; q < s + z; q++) {
+            const uint32_t bw = s_bw[q];
+            counter = KY::c_init(bw_app(bw));
+            arrive(q, s_mem[q], bw, 0u);
+            if constexpr (TBL) {
+                while (gs && !fail) grant_step();
+            }
+            if (fail) return false;
+        }
+        counter = KY::c_base(n_trace);
+        uint32_t ap = s + z;
+        Key ka = KY::INF;
+        uint32_t bwa = 0;
+        if (ap < e) {
+            bwa = s_bw[ap];
+            ka = KY::make(s_a[ap], KY::c_init(bw_app(bwa)), ap);
+        }
+        while (true) {
+            if (!gs) {
+                // next event: a granted waiter resumes after every other entry of
+                // its tick; otherwise the smaller of the arrival / busy-end keys
+                Key kmin = ka < kh ? ka : kh;
+                if (fhead != ftail && KY::time(kmin) > last) {
+                    // every other entry of tick `last` is done: the woken
+                    // waiters resume in grant order, each starting its busy
+                    // step (harness.py:514-520, 558); a zero-length busy step
+                    // frees at once and is handled below as an event
+                    do {
+                        const uint32_t wq = *fifo_slot(fhead);
+                        const uint32_t wb = bw_busy(s_bw[wq]);
+                        if (wb == 0) break;
+                        fhead += 1;
+                        pops += 1;
+                        busy_point(last, +1);
+                        push(last + wb, wq);
+                    } while (fhead != ftail);
+                    kmin = ka < kh ? ka : kh;
+                }
+                const bool is_wake = fhead != ftail && KY::time(kmin) > last;
+                if (!is_wake && kmin == KY::INF) break;
+                const bool is_arr = !is_wake && ka < kh;
+                const bool is_end = !is_wake && !is_arr;
+                const uint32_t q = is_wake ? (uint32_t)*fifo_slot(fhead) : KY::pos(kmin);
+                const uint32_t now = is_wake ? last : KY::time(kmin);
+                if (is_end) pop();
+                if (is_wake) fhead += 1;
+                if (is_arr) {
+                    ap += 1;
+                    if (ap < e) {
+                        bwa = s_bw[ap];
+                        ka = KY::make(s_a[ap], KY::c_init(bw_app(bwa)), ap);
+                    } else {
+                        ka = KY::INF;
+                    }
+                }
+                const uint32_t m = s_mem[q];
+                const uint32_t bw = s_bw[q];
+                const uint32_t b = bw_busy(bw);
+                pops += 1;
+                last = now;
+                // arrival: memory-fit admission with bypass, else wait (harness.py:521-536)
+                const bool alloc = is_arr && m != 0;
+                const bool fits = m <= cap - used;
+                const bool enq = alloc && !fits;
+                if (enq) enqueue(q, bw);
+                mem_point(now);
+                if (alloc && fits) {
+                    used += m;
+                    holders += 1;
+                    maxh = max(maxh, (uint32_t)holders);
+                    grants += 1;
+                }
+                // busy (harness.py:514-520) or its end
+                const bool to_busy = !is_end && !enq;
+                const bool start = to_busy && b != 0;
+                busy_point(now, start ? 1 : (is_end ? -1 : 0));
+                if (start) push(now + b, q);
+                if ((to_busy && b == 0) || is_end) end_app(m, bw, now);
+            }
+            if constexpr (TBL) {
+                if (gs) grant_step();
+            }
+            if (fail) return false;
+        }
+        return true;
+    }
+
+#ifdef __CUDACC__
+    SG_HD void finish(uint64_t srec, uint32_t nd) {
+        uint32_t unf = 0;
+#pragma unroll
+        for (uint32_t w = 0; w < NW; w++) {
+            for (uint64_t bits = mask[w]; bits; bits &= bits - 1) {
+                const uint32_t q = 64u * w + ffs64(bits);
+                const uint64_t o = out_base + bw_app(s_bw[q]);
+                if (P.grant) reinterpret_cast<uint32_t*>(P.grant)[o] = SG_NEVER;
+                if (P.end) reinterpret_cast<uint32_t*>(P.end)[o] = SG_NEVER;
+                unf += 1;
+            }
+        }
+        store_tick_record(P, srec, nd, cap, last, mem_t, I, B, (int64_t)used, grants, pops + nd,
+                          maxh, unf, 0u);
+    }
+#endif
+};
+
+}  // namespace sg

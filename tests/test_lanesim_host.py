@@ -1,0 +1,124 @@
+"""The K1 v5 per-lane simulator (csrc/sgpu_lanesim.cuh, LaneSim) compiled
+for the HOST with g++ (tests/lanesim_host.cpp) and checked against the
+oracle: the exact decision logic the kernel runs (arrival stream, virtual
+counters, 32- and 64-bit event keys, the two-level heap, wake FIFO drain,
+incremental select_grants steps over the fit table, class sets) on CPU,
+bit for bit, including edge shapes (zero fields, ties, stuck requests,
+eight priority classes).  No GPU needed; the -m gpu tests run the same
+logic inside the kernel."""
+
+import os
+import shutil
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1712_04495_b200.tracegen import CONFIGS, as_u32x4, generate
+from util import POLICIES
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "lanesim_host.cpp")
+HDR = os.path.join(os.path.dirname(HERE), "paper_1712_04495_b200", "csrc", "sgpu_lanesim.cuh")
+CODES = {"fifo": 0, "mmu": 1, "pfifo": 2, "pmmu": 3}
+STAT_FIELDS = ("makespan", "busy", "mem_integral", "grants", "pops", "max_holders", "unfinished")
+
+
+@pytest.fixture(scope="module")
+def lanesim(tmp_path_factory):
+    cxx = shutil.which("g++") or shutil.which("c++")
+    if cxx is None:
+        pytest.skip("no host C++ compiler")
+    exe = str(tmp_path_factory.mktemp("lanesim") / "lanesim_host")
+    subprocess.run([cxx, "-O2", "-std=c++17", "-Wall", "-Wno-unknown-pragmas", "-o", exe, SRC],
+                   check=True)
+    return exe
+
+
+def run_host(exe, apps, pol, cap, narrow):
+    lines = []
+    for tr in apps:
+        lines.append(f"{len(tr)} {CODES[pol]} {cap} {int(narrow)}")
+        lines.extend(" ".join(str(int(x)) for x in (r[0], r[1], r[2], r[3] & 0xFF)) for r in tr)
+    out = subprocess.run([exe], input="\n".join(lines) + "\n", capture_output=True, text=True,
+                         check=True).stdout.split("\n")
+    return [list(map(int, o.split())) for o in out[:len(apps)]]
+
+
+def check(exe, apps, pol, cap, narrow, min_checked):
+    g, e, st = O.simulate_burst(apps, (cap,), pol)
+    res = run_host(exe, apps, pol, cap, narrow)
+    checked = 0
+    for t, v in enumerate(res):
+        if v[0] == 0:       # lane path declined (capacity): the kernel's warp fallback runs it
+            continue
+        checked += 1
+        stats = v[1:8]
+        ref = [int(st[t][0][f]) for f in STAT_FIELDS]
+        assert stats == ref, (pol, narrow, t, stats, ref)
+        ticks = np.array(v[8:], dtype=np.uint64)
+        np.testing.assert_array_equal(ticks[0::2], g[t].astype(np.uint64), err_msg=f"grant {pol} {t}")
+        np.testing.assert_array_equal(ticks[1::2], e[t].astype(np.uint64), err_msg=f"end {pol} {t}")
+    assert checked >= min_checked, (checked, len(res))
+    return checked
+
+
+def narrow_ok(apps, n):
+    """The kernel's staging rule for 32-bit keys (sgpu_lane.cu stage_trace)."""
+    logn = 5 if n <= 32 else 6
+    a = apps.astype(np.uint64)
+    return bool(np.all(a[..., 0].max(axis=1) + a[..., 2].sum(axis=1) < (1 << (31 - 2 * logn))))
+
+
+@pytest.mark.parametrize("pol", POLICIES)
+def test_lanesim_c2_traces(lanesim, pol):
+    cfg = CONFIGS["C2"]
+    apps = as_u32x4(generate(cfg.gen, 123_456, 150))
+    assert narrow_ok(apps, 64)
+    check(lanesim, apps, pol, cfg.cap_mib[0], True, 150)
+    # 64-bit keys: 10 heap slots, so the busiest traces decline to the fallback
+    check(lanesim, apps, pol, cfg.cap_mib[0], False, 1)
+
+
+def random_edge_traces(rng, n_traces, n, cap):
+    apps = np.zeros((n_traces, n, 4), np.uint32)
+    # arrivals: many ties and zeros
+    apps[..., 0] = rng.integers(0, 12, (n_traces, n)) * rng.integers(0, 2, (n_traces, n)) * 7
+    apps[..., 1] = rng.integers(0, cap // 3, (n_traces, n))
+    apps[..., 1] *= rng.random((n_traces, n)) > 0.1            # some mem = 0
+    apps[..., 2] = rng.integers(0, 25, (n_traces, n))            # some busy = 0
+    apps[..., 3] = rng.integers(0, 8, (n_traces, n))             # up to 8 classes
+    stuck = rng.random((n_traces, n)) < 0.02                     # requests above capacity
+    apps[..., 1][stuck] = cap + 1
+    return apps
+
+
+@pytest.mark.parametrize("pol", POLICIES)
+@pytest.mark.parametrize("n", [7, 32, 45, 64])
+def test_lanesim_edge_shapes(lanesim, pol, n):
+    rng = np.random.default_rng(1000 + n)
+    cap = 1000
+    apps = random_edge_traces(rng, 300, n, cap)
+    check(lanesim, apps, pol, cap, True, 250)
+    check(lanesim, apps, pol, cap, False, 10)
+
+
+@pytest.mark.parametrize("pol", POLICIES)
+def test_lanesim_near_capacity(lanesim, pol):
+    """C4-like: requests of 1/4..1x capacity, long queues, head-of-line blocking."""
+    rng = np.random.default_rng(77)
+    cap = 184_320
+    apps = np.zeros((200, 64, 4), np.uint32)
+    apps[..., 0] = rng.integers(0, 8192, (200, 64))
+    apps[..., 1] = rng.integers(46_080, cap + 1, (200, 64))
+    apps[..., 2] = rng.integers(1, 2049, (200, 64))
+    apps[..., 3] = rng.integers(0, 4, (200, 64))
+    check(lanesim, apps, pol, cap, narrow_ok(apps, 64), 200)
+
+
+def test_header_is_shared_with_the_kernel():
+    """The kernel includes the same header the host test compiles."""
+    src = open(os.path.join(os.path.dirname(HDR), "sgpu_lane.cu")).read()
+    assert '#include "sgpu_lanesim.cuh"' in src
+    assert "struct LaneSim" in open(HDR).read()
