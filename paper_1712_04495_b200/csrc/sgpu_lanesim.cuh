@@ -25,6 +25,7 @@ struct SimParams {  // the two output arrays LaneSim writes
     void* end;
 };
 inline int __ffsll(long long x) { return __builtin_ffsll(x); }
+inline int __ffs(int x) { return __builtin_ffs(x); }
 }  // namespace sg
 #endif
 
@@ -46,6 +47,7 @@ SG_HD uint32_t bw_cls(uint32_t bw) { return bw >> kClsShift; }
 
 
 SG_HD uint32_t ffs64(uint64_t x) { return (uint32_t)__ffsll((long long)x) - 1u; }
+SG_HD uint32_t ffs32(uint32_t x) { return (uint32_t)__ffs((int)x) - 1u; }
 
 // Rank-lookup bucket of a request d = mem - lo >= 0: monotone in d.
 SG_HD uint32_t lt_bucket(uint32_t d, uint32_t scale) {
@@ -250,7 +252,7 @@ struct LaneSim {
     SG_HD void init_round() {
         uint64_t cm = ~0ull;
         if (prio_pol) {
-            gc = ffs64(clsmask);  // clsmask != 0 whenever the queue is not empty
+            gc = ffs32(clsmask);  // clsmask != 0 whenever the queue is not empty
             cm = s_cm[gc];
         }
         gcand = mask[0] & cm;

@@ -185,6 +185,11 @@ static cudaError_t launch_t(const SimParams& p, cudaStream_t stream, int* grid_o
     if (smem > 227u * 1024u) return cudaErrorInvalidConfiguration;
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
+    // all of the unified L1/shared array as shared memory: the occupancy the
+    // grid is sized for must not depend on the driver's carveout choice
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+    if (err != cudaSuccess) return err;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
