@@ -20,6 +20,8 @@ Layouts (include/sgpu.h):
 
 from __future__ import annotations
 
+import os
+
 import ctypes
 from dataclasses import dataclass
 from typing import Iterable, Optional, Sequence
@@ -213,11 +215,21 @@ class HostBuffers:
 
     def d2h_bytes(self) -> int:
         """Bytes the host pipeline copies device -> host per call.  With both
-        tick arrays requested the grants are derived on the host from the
-        end ticks and the inputs (grant = end - busy), so they cross no bus."""
-        derived = self.grant if (self.grant is not None and self.end is not None) else None
-        return sum(a.nbytes for a in (self.grant, self.end, self.stats, self.mem_pct, self.dev_pct)
-                   if a is not None and a is not derived)
+        tick arrays requested, the grants of the first npol // 4 policies are
+        copied and the others derived on the host from the end ticks and the
+        inputs (grant = end - busy), crossing no bus (sg_simulate_batch_host,
+        csrc/sgpu_abi.cu; SGPU_GRANT_DMA overrides the split there and here)."""
+        n = sum(a.nbytes for a in (self.end, self.stats, self.mem_pct, self.dev_pct) if a is not None)
+        if self.grant is not None:
+            npol = self.grant.shape[0]
+            n_dma = npol
+            if self.end is not None:
+                n_dma = npol // 4
+                env = os.environ.get("SGPU_GRANT_DMA")
+                if env is not None and int(env) >= 0:
+                    n_dma = min(int(env), npol)
+            n += self.grant[:n_dma].nbytes
+        return n
 
 
 def pinned_apps(n_traces: int, n_apps: int) -> np.ndarray:

@@ -202,7 +202,7 @@ void grant_row_scalar(const uint32_t* mem, const uint32_t* busy, const uint32_t*
 
 // grant[p][a] for traces [t_lo, t_hi) of the batch; overflowing (trace,
 // policy) pairs are skipped and reported.
-void derive_grants(const sg_batch* in, const sg_out* out, uint32_t npol, uint64_t t_lo, uint64_t t_hi,
+void derive_grants(const sg_batch* in, const sg_out* out, uint32_t p0, uint32_t npol, uint64_t t_lo, uint64_t t_hi,
                    std::vector<uint64_t>& overflow, bool avx2) {
     const uint64_t N = in->n_traces;
     const uint32_t napps = in->apps_per_trace, ndev = in->ndev;
@@ -220,7 +220,7 @@ void derive_grants(const sg_batch* in, const sg_out* out, uint32_t npol, uint64_
             busy[i] = ap[i].busy;
         }
         bool ov_any = false;
-        for (uint32_t p = 0; p < npol; p++) {
+        for (uint32_t p = p0; p < npol; p++) {
             bool ov = false;
             for (uint32_t d = 0; d < ndev; d++)
                 ov = ov || (st[((uint64_t)p * N + t) * ndev + d].status & SG_ST_TICK_OVERFLOW);
@@ -257,6 +257,16 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
     if (chunk_traces > N) chunk_traces = N;
     // grants derived on the host when both tick arrays are requested
     const bool host_grant = out->grant != nullptr && out->end != nullptr;
+    // With both tick arrays requested, the grants of policies [0, n_dma) are
+    // copied from the device and those of [n_dma, npol) derived by host
+    // threads: the split balances PCIe time against host-memory traffic
+    // ("End to end").  SGPU_GRANT_DMA overrides.
+    uint32_t n_dma = host_grant ? s.npol / 4 : s.npol;
+    if (const char* ev = getenv("SGPU_GRANT_DMA")) {
+        const int v = atoi(ev);
+        if (host_grant && v >= 0) n_dma = (uint32_t)v < s.npol ? (uint32_t)v : s.npol;
+    }
+    const bool derive = host_grant && n_dma < s.npol;
     constexpr int NBUF = 3;
     const size_t app_b = chunk_traces * napps * sizeof(sg_app);
     const size_t tick_b = (size_t)s.npol * chunk_traces * napps * sizeof(uint32_t);
@@ -297,7 +307,7 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
     for (auto& b : B) {
         e = cudaStreamCreateWithFlags(&b.st, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaMallocAsync(&b.apps, app_b, b.st);
-        if (e == cudaSuccess && out->grant && !host_grant) e = cudaMallocAsync(&b.grant, tick_b, b.st);
+        if (e == cudaSuccess && out->grant && n_dma > 0) e = cudaMallocAsync(&b.grant, tick_b, b.st);
         if (e == cudaSuccess && out->end) e = cudaMallocAsync(&b.end, tick_b, b.st);
         if (e == cudaSuccess) e = cudaMallocAsync(&b.stats, st_b, b.st);
         if (e == cudaSuccess && want_pct) e = cudaMallocAsync(&b.mem, pct_b, b.st);
@@ -332,7 +342,7 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
             const uint64_t ho = (uint64_t)p * n_apps_total + a0;
             const uint64_t hs = ((uint64_t)p * N + t0) * ndev;
             const uint64_t dsrc = (uint64_t)p * nt * ndev;
-            if (b.grant)
+            if (b.grant && p < n_dma)
                 e = cudaMemcpyAsync(static_cast<uint32_t*>(out->grant) + ho, b.grant + (uint64_t)p * na,
                                     na * 4, cudaMemcpyDeviceToHost, b.st);
             if (e == cudaSuccess && out->end)
@@ -349,7 +359,7 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
                                     cudaMemcpyDeviceToHost, b.st);
             if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "D2H outputs"); }
         }
-        if (host_grant) {
+        if (derive) {
             HostChunk c{t0, nt, nullptr};
             e = cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming);
             if (e == cudaSuccess) e = cudaEventRecord(c.done, b.st);
@@ -358,7 +368,7 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
         }
     }
     std::vector<uint64_t> overflow;
-    if (host_grant) {
+    if (derive) {
         // host threads follow the pipeline chunk by chunk, each deriving the
         // grants of its contiguous share of every chunk's traces
         const bool avx2 = __builtin_cpu_supports("avx2");
@@ -379,7 +389,7 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
                     if (ce != cudaSuccess) { errs[w] = ce; return; }
                     const double tr = ms();
                     const uint64_t lo = c.t0 + c.nt * w / nthr, hi = c.t0 + c.nt * (w + 1) / nthr;
-                    derive_grants(in, out, s.npol, lo, hi, ov[w], avx2);
+                    derive_grants(in, out, n_dma, s.npol, lo, hi, ov[w], avx2);
                     if (trace && w == 0) fprintf(stderr, "[pipe] chunk %llu ready %.2f derived %.2f ms\n", (unsigned long long)(c.t0 / chunk_traces), tr, ms());
                 }
             });
