@@ -534,10 +534,11 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel
 static inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
 // Lane path eligibility: T0 ticks mode, no event log, <= 256 apps per trace.
-// By default only traces of <= 64 apps take it (the fit-table path); longer
-// ones are faster on the warp kernel unless `forced`.
+// By default traces of <= 128 apps take it (measured on one B200: C4, 128
+// apps, 2.07e7 vs 1.41e7 trace-sims/s on the warp kernel); 256-app traces
+// are faster on the warp kernel (C3: 2.7e6 vs 4.5e5) unless `forced`.
 bool lane_eligible(const SimParams& p, bool program_mode, bool f64, bool forced) {
-    return !program_mode && !f64 && p.events == nullptr && p.n_pad <= (forced ? 256u : 64u) &&
+    return !program_mode && !f64 && p.events == nullptr && p.n_pad <= (forced ? 256u : 128u) &&
            p.npol * p.ndev <= 32;
 }
 
