@@ -22,6 +22,7 @@ oracle/_ref) on the host cores over a bounded sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import multiprocessing as mp
@@ -123,16 +124,50 @@ def cpu_port_rate(cfg_name: str, n_traces: int):
 # ------------------------------------------------------------- clocks
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """SM clocks and throttle reasons during the timed region, polled through
+    NVML from a thread every 50 ms (an nvidia-smi child process was seen to
+    stall single kernel launches when its queries land inside them); falls
+    back to `nvidia-smi -lms 200` when pynvml is missing."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.proc = None
+        self.thread = None
+        self.rows = []
+        self.out = ""
+        self.window = None
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            bits = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+            sm_max = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            import threading
+            self.stop = threading.Event()
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)), sm_max,
+                                          ["Active" if r & b else "Not Active" for b in bits],
+                                          time.perf_counter()))
+                    except pynvml.NVMLError:
+                        pass
+                    self.stop.wait(0.05)
+
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.thread = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
@@ -143,7 +178,9 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
-        self.out = ""
+        if self.thread is not None:
+            self.stop.set()
+            self.thread.join(timeout=5)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -151,23 +188,30 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
                 self.out, _ = self.proc.communicate()
+            for line in (self.out or "").splitlines():
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    self.rows.append((float(f[1]), float(f[2]), f[5:9], None))
+                except ValueError:
+                    continue
+
+    def mark(self, t0, t1):
+        """The timed region (host perf_counter): summary() keeps its samples."""
+        self.window = (t0, t1)
 
     def summary(self):
-        rows = []
-        for line in (self.out or "").splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                rows.append((float(f[1]), float(f[2]), f[5:9]))
-            except ValueError:
-                continue
+        rows = self.rows
+        if self.window is not None:
+            inside = [r for r in rows if r[3] is not None and self.window[0] <= r[3] <= self.window[1]]
+            rows = inside or rows
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        reasons = sorted({self.NAMES[i] for _, _, r, _ in rows for i, v in enumerate(r) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(r[0] for r in rows),
-                "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons, "samples": len(rows)}
+                "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons, "samples": len(rows),
+                "source": "nvml" if self.thread is not None else "nvidia-smi"}
 
 
 # ------------------------------------------------------------- helpers
@@ -324,21 +368,32 @@ def main():
             agg = PAR.allreduce_aggregate(agg)
         return res, agg
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    launches = 0
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
+    # the clock sampler (an nvidia-smi child) starts before the warm-up: its
+    # start-up must not land inside the timed steps; it keeps sampling
+    # through them
     with ClockSampler(local) as clk:
+        time.sleep(0.2)
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        launches = 0
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        # a Python garbage-collection pass between two launches would leave
+        # the stream idle (the host feeds the queue step by step)
+        gc.collect()
+        gc.disable()
+        w0 = time.perf_counter()
         t_start.record(stream)
         for i in range(args.steps):
             res, agg = step(i)
         t_end.record(stream)
         torch.cuda.synchronize()
+        clk.mark(w0, time.perf_counter())
+        gc.enable()
     if ws > 1:
         dist.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
@@ -374,12 +429,15 @@ def main():
         e2e_steps = max(1, min(args.steps, 5))
         if ws > 1:
             dist.barrier()
+        gc.collect()
+        gc.disable()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             B.simulate_batch_host(host_apps, pols, cfg.cap_mib, device=local, out=outb,
                                   chunk_traces=args.chunk)
             _ = float(outb.stats["makespan"][0, 0, 0])
         dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        gc.enable()
         if ws > 1:
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e = {"value": units_per_step * e2e_steps / float(dt[0]), "unit": "traces/s",

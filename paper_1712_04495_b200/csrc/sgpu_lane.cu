@@ -60,9 +60,9 @@ struct LaneParams {
 // a warp (fence / block / table reads) hit disjoint bank groups.
 template <uint32_t N> struct SlotStride {
     static constexpr uint32_t S32 = N + 4;          // u32 record arrays
-    static constexpr uint32_t POR = 80;             // rank -> position (u8, padded)
+    static constexpr uint32_t POR = N + 16;         // rank -> position (u8, padded)
     static constexpr uint32_t LTB = kLtBuckets + 16;  // rank lookup: u8 buckets + 3 u32 params (+skew)
-    static constexpr uint32_t T4 = N / 4 + 2;       // fit table at every 4th rank (N/4 + 1 entries)
+    static constexpr uint32_t T4 = (N / 4 + 2) * ((N + 63) / 64);  // fit table at every 4th rank (N/4 + 1 entries of NW words)
 };
 
 // meta per trace slot (u16): [0] n, [1] fail (big times / too many classes),
@@ -356,23 +356,30 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
         if (mn > mx) mn = mx;  // empty trace
         const uint64_t sc = ((uint64_t)kLtBuckets << 32) / ((uint64_t)(mx - mn) + 1ull);
         const uint32_t scale = sc > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)sc;
-        uint64_t carry = 0;
+        uint64_t carry[NW];
+#pragma unroll
+        for (uint32_t w = 0; w < NW; w++) carry[w] = 0;
         uint32_t bcarry = 0;  // bucket of the last rank of the previous row (+1)
 #pragma unroll
         for (int k = 0; k < K; k++) {
             const uint32_t r = (uint32_t)k * 32u + lane;
             const bool valid = mk[k] != kInf;
             s_por[r] = valid ? (uint8_t)(mk[k] & 0xFFu) : (uint8_t)N;
-            // prefix OR over ranks: v = T[r + 1]
-            uint64_t v = valid ? (1ull << ((uint32_t)mk[k] & 63u)) : 0ull;
+            // prefix OR over ranks, word by word: v = T[r + 1]
+            const uint32_t pos = (uint32_t)mk[k] & 0xFFu;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint64_t u = shfl_up_u64(v, o);
-                if (lane >= (uint32_t)o) v |= u;
+            for (uint32_t w = 0; w < NW; w++) {
+                uint64_t v = valid && (pos >> 6) == w ? (1ull << (pos & 63u)) : 0ull;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint64_t u = shfl_up_u64(v, o);
+                    if (lane >= (uint32_t)o) v |= u;
+                }
+                v |= carry[w];
+                if ((r & 3u) == 3u) s_t4[((r + 1) >> 2) * NW + w] = v;
+                carry[w] = __shfl_sync(FULL, (uint32_t)v, 31) |
+                           ((uint64_t)__shfl_sync(FULL, (uint32_t)(v >> 32), 31) << 32);
             }
-            v |= carry;
-            if ((r & 3u) == 3u) s_t4[(r + 1) >> 2] = v;
-            carry = __shfl_sync(FULL, (uint32_t)v, 31) | ((uint64_t)__shfl_sync(FULL, (uint32_t)(v >> 32), 31) << 32);
             // LT[j] = first rank whose bucket is >= j: rank r owns (b[r-1], b[r]]
             const uint32_t b = valid ? lt_bucket((uint32_t)(mk[k] >> 8) - mn, scale) + 1u : kLtBuckets + 1u;
             uint32_t bp = __shfl_up_sync(FULL, b, 1);
@@ -383,8 +390,8 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
         }
         // buckets above the largest request (all ranks valid) -> N
         for (uint32_t j = bcarry + lane; j < kLtBuckets; j += 32u) s_lt[j] = (uint8_t)N;
+        if (lane < NW) s_t4[lane] = 0ull;
         if (lane == 0) {
-            s_t4[0] = 0ull;
             uint32_t* prm = reinterpret_cast<uint32_t*>(s_lt + kLtBuckets);
             prm[0] = mn;
             prm[1] = mx;
@@ -583,13 +590,13 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
         const uint32_t pol = (p.policy_list >> (4 * i)) & 0xFu;
         if (pol >= SG_POLICY_PFIFO) L.need_cls = 1;
     }
-    L.need_tbl = N <= 64 ? 1u : 0u;  // all kinds use the fit table on short traces
+    L.need_tbl = N <= 128 ? 1u : 0u;  // all kinds use the fit table (one or two mask words)
     L.cm_per_trace = max(kLaneClassMasks / L.G, 8u);
     // per-warp region: busy-end heaps / staging scratch; the fallback
     // TraceSim overlays the whole warp region once the group's lanes are done
     sim_layout(L.sp, false, false);
     const uint32_t fb = max(max(kLaneHeapN * 32u * 4u, kLaneHeapW * 32u * 8u), N * 16u);
-    const uint32_t S32 = N + 4, POR = 80, LTB = kLtBuckets + 16, T4 = N / 4 + 2;  // SlotStride<N>
+    const uint32_t S32 = N + 4, POR = N + 16, LTB = kLtBuckets + 16, T4 = (N / 4 + 2) * NW;  // SlotStride<N>
     uint32_t o = 0;
     L.off_a = o;
     o = align16(o + L.G * S32 * 4u);

@@ -84,7 +84,7 @@ struct LaneSim {
     static constexpr uint32_t N = 32u * K;
     static constexpr uint32_t NW = (N + 63u) / 64u;  // queue mask words
     static constexpr uint32_t LOGN = LogN<K>::v;
-    static constexpr bool TBL = K <= 2;              // fit table (one mask word)
+    static constexpr bool TBL = K <= 4;              // fit table (one or two mask words)
     using KY = LaneKey<K, NARROW>;
     using Key = typename KY::T;
 
@@ -96,8 +96,8 @@ struct LaneSim {
     const uint8_t* s_por;    // position of the r-th smallest request (N past the end)
     const uint8_t* s_lt;     // s_lt[j] = #requests in buckets < j
     uint32_t lt_lo, lt_hi, lt_scale;
-    const uint64_t* s_t4;    // T[4j]: positions of the 4j smallest requests
-    const uint64_t* s_cm;    // class masks of this lane's device, top class first
+    const uint64_t* s_t4;    // T[4j] (NW words): positions of the 4j smallest requests
+    const uint64_t* s_cm;    // class masks (NW words each) of this lane's device, top class first
     uint32_t ncls;
     // this lane's columns
     Key* heap;               // heap[h * 32]
@@ -119,7 +119,7 @@ struct LaneSim {
     bool gs;
     uint32_t clsmask;        // priority classes with waiting entries (bit c: class c, top = 0)
     uint32_t gc, gbud, gb0, gg;
-    uint64_t gcand, grem;    // unscanned candidates / waiting members of the round's class
+    uint64_t gcand[NW], grem[NW];  // unscanned candidates / waiting members of the round's class
 
     SG_HD LaneSim(const SimParams& p) : P(p) {}
 
@@ -217,14 +217,18 @@ struct LaneSim {
         return r;
     }
     // T[r]: positions of the r smallest requests = T[4 floor(r/4)] + up to 3
-    SG_HD uint64_t fit_set(uint32_t r) const {
-        uint64_t t = s_t4[r >> 2];
-        const uint32_t w = *reinterpret_cast<const uint32_t*>(s_por + (r & ~3u));
+    SG_HD void fit_set(uint32_t r, uint64_t (&t)[NW]) const {
+#pragma unroll
+        for (uint32_t w = 0; w < NW; w++) t[w] = s_t4[(r >> 2) * NW + w];
+        const uint32_t pw = *reinterpret_cast<const uint32_t*>(s_por + (r & ~3u));
         const uint32_t k = r & 3u;
-        if (k > 0) t |= 1ull << (w & 0xFFu);
-        if (k > 1) t |= 1ull << ((w >> 8) & 0xFFu);
-        if (k > 2) t |= 1ull << ((w >> 16) & 0xFFu);
-        return t;
+#pragma unroll
+        for (uint32_t j = 0; j < 3; j++) {
+            const uint32_t p = (pw >> (8u * j)) & 0xFFu;
+#pragma unroll
+            for (uint32_t w = 0; w < NW; w++)
+                if (k > j && (NW == 1 || w == (p >> 6))) t[w] |= 1ull << (p & 63u);
+        }
     }
     SG_HD void grant_one(uint32_t q, uint32_t m, uint32_t& budget, uint32_t& g) {
 #pragma unroll
@@ -250,52 +254,97 @@ struct LaneSim {
     // cand & T[#requests <= budget]; FIFO takes the head iff it fits, MMU the
     // lowest fit (policy.py:65-73); both continue above the granted position.
     SG_HD void init_round() {
-        uint64_t cm = ~0ull;
-        if (prio_pol) {
-            gc = ffs32(clsmask);  // clsmask != 0 whenever the queue is not empty
-            cm = s_cm[gc];
+        if (prio_pol) gc = ffs32(clsmask);  // clsmask != 0 whenever the queue is not empty
+        bool any = false;
+#pragma unroll
+        for (uint32_t w = 0; w < NW; w++) {
+            gcand[w] = mask[w] & (prio_pol ? s_cm[gc * NW + w] : ~0ull);
+            grem[w] = gcand[w];
+            any = any || gcand[w] != 0;
         }
-        gcand = mask[0] & cm;
-        grem = gcand;
-        gs = gcand != 0;
+        gs = any;
         gb0 = gbud = cap - used;
         gg = 0;
     }
     SG_HD void grant_step() {
-        const uint64_t fit = gcand & fit_set(fit_rank(gbud));
-        const uint64_t head = gcand & (0ull - gcand);
-        const uint64_t pick = mmu ? fit : (fit & head);
+        uint64_t t[NW];
+        fit_set(fit_rank(gbud), t);
+        if constexpr (NW == 1) {
+            const uint64_t fit = gcand[0] & t[0];
+            const uint64_t head = gcand[0] & (0ull - gcand[0]);
+            const uint64_t pick = mmu ? fit : (fit & head);
+            if (pick) {
+                const uint32_t q = ffs64(pick);
+                const uint64_t bit = 1ull << q;
+                mask[0] &= ~bit;
+                grem[0] &= ~bit;
+                gbud -= s_mem[q];
+                gg += 1;
+                wake(q);
+                gcand[0] &= ~((bit << 1) - 1ull);
+            }
+            if (!pick || !gcand[0]) end_round(grem[0] == 0);
+            return;
+        }
+        // lowest candidate (the queue head of the round) and lowest fit
+        uint32_t hq = N, fq = N;
+#pragma unroll
+        for (int w = (int)NW - 1; w >= 0; w--) {
+            const uint64_t fit = gcand[w] & t[w];
+            if (gcand[w]) hq = 64u * (uint32_t)w + ffs64(gcand[w]);
+            if (fit) fq = 64u * (uint32_t)w + ffs64(fit);
+        }
+        // FIFO takes the head iff it fits, MMU the lowest fit (policy.py:65-73)
+        const uint32_t q = mmu ? fq : (fq == hq ? hq : N);
+        const bool pick = q < N;
+        bool more = false;
         if (pick) {
-            const uint32_t q = ffs64(pick);
-            const uint64_t bit = 1ull << q;
-            mask[0] &= ~bit;
-            grem &= ~bit;
+            const uint32_t qw = q >> 6;
+            const uint64_t bit = 1ull << (q & 63u);
+#pragma unroll
+            for (uint32_t w = 0; w < NW; w++) {
+                if (w == qw) {
+                    mask[w] &= ~bit;
+                    grem[w] &= ~bit;
+                }
+                // continue above the granted position
+                gcand[w] &= w < qw ? 0ull : (w == qw ? ~((bit << 1) - 1ull) : ~0ull);
+                more = more || gcand[w] != 0;
+            }
             gbud -= s_mem[q];
             gg += 1;
             wake(q);
-            gcand &= ~((2ull << q) - 1ull);
         }
-        if (!pick || !gcand) {  // the round ends
-            if (gg) {
-                mem_point(last);
-                used += gb0 - gbud;
-                holders += (int32_t)gg;
-                maxh = max(maxh, (uint32_t)holders);
-                grants += gg;
-            }
-            // the top class drained: the next class is served in the same
-            // tick (harness.py:547-550); otherwise the next round is empty
-            if (prio_pol && gg && !grem) {
-                clsmask &= ~(1u << gc);
-                if (clsmask) init_round();
-                else gs = false;
-            } else {
-                gs = false;
-            }
+        if (!more) {  // the round ends
+            bool left = false;
+#pragma unroll
+            for (uint32_t w = 0; w < NW; w++) left = left || grem[w] != 0;
+            end_round(!left);
+        }
+    }
+    SG_HD void end_round(bool drained) {
+        if (gg) {
+            mem_point(last);
+            used += gb0 - gbud;
+            holders += (int32_t)gg;
+            maxh = max(maxh, (uint32_t)holders);
+            grants += gg;
+        }
+        // the top class drained: the next class is served in the same tick
+        // (harness.py:547-550); otherwise the next round is empty
+        if (prio_pol && gg && drained) {
+            clsmask &= ~(1u << gc);
+            if (clsmask) init_round();
+            else gs = false;
+        } else {
+            gs = false;
         }
     }
     SG_HD void grant_waiters_tbl() {
-        if (mask[0]) init_round();
+        bool any = false;
+#pragma unroll
+        for (uint32_t w = 0; w < NW; w++) any = any || mask[w] != 0;
+        if (any) init_round();
     }
 
     // longer traces: scan the candidates in queue order

@@ -21,6 +21,7 @@ static void run_case(int n, uint32_t policy, uint32_t cap, const std::vector<uin
                      const std::vector<uint32_t>& Pr) {
     constexpr uint32_t N = 32u * K;
     using Sim = LaneSim<K, NAR>;
+    constexpr uint32_t NW = Sim::NW;
     // arrival order: (arrival, index)
     std::vector<int> ord(n);
     for (int i = 0; i < n; i++) ord[i] = i;
@@ -41,18 +42,18 @@ static void run_case(int n, uint32_t policy, uint32_t cap, const std::vector<uin
     pl.erase(std::unique(pl.begin(), pl.end()), pl.end());
     std::reverse(pl.begin(), pl.end());
     if (pl.size() > kLaneMaxCls) { printf("0\n"); return; }
-    std::vector<uint64_t> s_cm(pl.size() + 1, 0);
+    std::vector<uint64_t> s_cm((pl.size() + 1) * NW, 0);
     for (size_t c = 0; c < pl.size(); c++)
         for (int e = 0; e < n; e++)
             if (Pr[ord[e]] == pl[c]) {
-                s_cm[c] |= 1ull << e;
+                s_cm[c * NW + (e >> 6)] |= 1ull << (e & 63);
                 s_bw[e] |= (uint32_t)c << kClsShift;
             }
     // fit table: requests ascending, T at every 4th rank, rank -> position
     std::vector<int> rk(n);
     for (int e = 0; e < n; e++) rk[e] = e;
     std::stable_sort(rk.begin(), rk.end(), [&](int x, int y) { return s_mem[x] < s_mem[y]; });
-    std::vector<uint8_t> s_por(N + 8, (uint8_t)N), s_lt(kLtBuckets + 16, 0);
+    std::vector<uint8_t> s_por(N + 16, (uint8_t)N), s_lt(kLtBuckets + 16, 0);
     for (int r = 0; r < n; r++) s_por[r] = (uint8_t)rk[r];
     const uint32_t mn = n ? s_mem[rk[0]] : 0, mx = n ? s_mem[rk[n - 1]] : 0;
     const uint64_t sc = ((uint64_t)kLtBuckets << 32) / ((uint64_t)(mx - mn) + 1);
@@ -62,13 +63,14 @@ static void run_case(int n, uint32_t policy, uint32_t cap, const std::vector<uin
         while (r < (uint32_t)n && lt_bucket(s_mem[rk[r]] - mn, scale) + 1 <= j) r++;
         s_lt[j] = (uint8_t)r;
     }
-    std::vector<uint64_t> s_t4(N / 4 + 2, 0);
-    uint64_t T = 0;
+    std::vector<uint64_t> s_t4((N / 4 + 2) * NW, 0);
+    uint64_t T[NW] = {};
     for (uint32_t r = 0; r < N; r++) {
-        if (r < (uint32_t)n) T |= 1ull << rk[r];
-        if ((r & 3) == 3) s_t4[(r + 1) >> 2] = T;
+        if (r < (uint32_t)n) T[rk[r] >> 6] |= 1ull << (rk[r] & 63);
+        if ((r & 3) == 3)
+            for (uint32_t w = 0; w < NW; w++) s_t4[((r + 1) >> 2) * NW + w] = T[w];
     }
-    std::vector<uint64_t> heap(32 * 32, 0);
+    std::vector<uint64_t> heap(32 * 32, 0);  // column 0 of the [slot][lane] layout
     std::vector<uint32_t> fifo(32 * kLaneFifoWords, 0);
     std::vector<uint32_t> grant(n, SG_NEVER), end(n, SG_NEVER);
     SimParams P{grant.data(), end.data()};
@@ -111,9 +113,12 @@ int main() {
         if (n <= 32) {
             if (narrow) run_case<1, true>(n, policy, cap, A, M, Bz, Pr);
             else run_case<1, false>(n, policy, cap, A, M, Bz, Pr);
-        } else {
+        } else if (n <= 64) {
             if (narrow) run_case<2, true>(n, policy, cap, A, M, Bz, Pr);
             else run_case<2, false>(n, policy, cap, A, M, Bz, Pr);
+        } else {
+            if (narrow) run_case<4, true>(n, policy, cap, A, M, Bz, Pr);
+            else run_case<4, false>(n, policy, cap, A, M, Bz, Pr);
         }
         fflush(stdout);
     }

@@ -66,7 +66,7 @@ def check(exe, apps, pol, cap, narrow, min_checked):
 
 def narrow_ok(apps, n):
     """The kernel's staging rule for 32-bit keys (sgpu_lane.cu stage_trace)."""
-    logn = 5 if n <= 32 else 6
+    logn = 5 if n <= 32 else 6 if n <= 64 else 7
     a = apps.astype(np.uint64)
     return bool(np.all(a[..., 0].max(axis=1) + a[..., 2].sum(axis=1) < (1 << (31 - 2 * logn))))
 
@@ -95,26 +95,34 @@ def random_edge_traces(rng, n_traces, n, cap):
 
 
 @pytest.mark.parametrize("pol", POLICIES)
-@pytest.mark.parametrize("n", [7, 32, 45, 64])
+@pytest.mark.parametrize("n", [7, 32, 45, 64, 65, 100, 128])
 def test_lanesim_edge_shapes(lanesim, pol, n):
     rng = np.random.default_rng(1000 + n)
     cap = 1000
     apps = random_edge_traces(rng, 300, n, cap)
     check(lanesim, apps, pol, cap, True, 250)
-    check(lanesim, apps, pol, cap, False, 10)
+    check(lanesim, apps, pol, cap, False, 10 if n <= 64 else 0)
 
 
 @pytest.mark.parametrize("pol", POLICIES)
-def test_lanesim_near_capacity(lanesim, pol):
+@pytest.mark.parametrize("n", [64, 128])
+def test_lanesim_near_capacity(lanesim, pol, n):
     """C4-like: requests of 1/4..1x capacity, long queues, head-of-line blocking."""
-    rng = np.random.default_rng(77)
+    rng = np.random.default_rng(77 + n)
     cap = 184_320
-    apps = np.zeros((200, 64, 4), np.uint32)
-    apps[..., 0] = rng.integers(0, 8192, (200, 64))
-    apps[..., 1] = rng.integers(46_080, cap + 1, (200, 64))
-    apps[..., 2] = rng.integers(1, 2049, (200, 64))
-    apps[..., 3] = rng.integers(0, 4, (200, 64))
-    check(lanesim, apps, pol, cap, narrow_ok(apps, 64), 200)
+    apps = np.zeros((100, n, 4), np.uint32)
+    apps[..., 0] = rng.integers(0, 8192, (100, n))
+    apps[..., 1] = rng.integers(46_080, cap + 1, (100, n))
+    apps[..., 2] = rng.integers(1, 2049, (100, n))
+    apps[..., 3] = rng.integers(0, 4, (100, n))
+    check(lanesim, apps, pol, cap, narrow_ok(apps, n), 100)
+
+
+@pytest.mark.parametrize("pol", POLICIES)
+def test_lanesim_c4_traces(lanesim, pol):
+    cfg = CONFIGS["C4"]
+    apps = as_u32x4(generate(cfg.gen, 7_000, 40))
+    check(lanesim, apps, pol, cfg.cap_mib[0], narrow_ok(apps, 128), 40)
 
 
 def test_header_is_shared_with_the_kernel():
