@@ -1,5 +1,5 @@
 """Group per-source-line instruction counts (attribute.py input) of the K1
-lane kernel into code regions by line range of sgpu_lane.cu.
+lane kernel into code regions by line range of sgpu_lanesim.cuh / sgpu_lane.cu.
 
     python profiles/categorize.py mix.csv
 """
@@ -8,29 +8,37 @@ import re
 import sys
 from collections import defaultdict
 
-src_file = "paper_1712_04495_b200/csrc/sgpu_lane.cu"
-lines = open(src_file).read().split("\n")
-# region starts: (regex on the source line, name)
-marks = [(r"void push\(", "heap push"), (r"min_child\(", "heap pop"), (r"void pop\(", "heap pop"),
-         (r"void wake\(", "wake fifo"), (r"void enqueue\(", "queue mask"),
-         (r"uint32_t fit_rank\(", "fit_rank/fit_set"), (r"void grant_one\(", "grant (scan path)"),
-         (r"void init_round\(", "grant round init"), (r"void grant_step\(", "grant step"),
-         (r"void grant_waiters_tbl\(", "grant round init"), (r"void grant_waiters_scan\(", "grant (scan path)"),
-         (r"void end_app\(", "end_app/outputs"), (r"void run_from_busy\(", "advance (phase 0)"),
-         (r"bool run\(", "event loop"), (r"void finish\(", "finish/stats"),
-         (r"void lane_trace_range\(", "staging"), (r"__global__", "kernel body"),
-         (r"exact fallback", "fallback"), (r"static inline uint32_t align16", "host")]
-starts = []
-for i, l in enumerate(lines, 1):
-    for rx, name in marks:
-        if re.search(rx, l):
-            starts.append((i, name))
-starts.sort()
+CSRC = "paper_1712_04495_b200/csrc/"
+# region starts per source file: (regex on the source line, name)
+MARKS = {
+    "sgpu_lanesim.cuh": [
+        (r"struct LaneKey", "keys/helpers"), (r"SG_HD void push\(", "heap push"), (r"SG_HD Key min_child\(", "heap pop"),
+        (r"SG_HD void pop\(", "heap pop"), (r"SG_HD uint8_t\* fifo_slot\(", "wake fifo"), (r"SG_HD void enqueue\(", "queue mask"),
+        (r"SG_HD uint32_t fit_rank\(", "fit_rank/fit_set"), (r"SG_HD void grant_one\(", "grant (scan path)"),
+        (r"SG_HD void init_round\(", "grant round init"), (r"SG_HD void grant_step\(", "grant step"),
+        (r"SG_HD void end_round\(", "grant round end"), (r"SG_HD void grant_waiters_tbl\(", "grant round init"),
+        (r"SG_HD void grant_waiters_scan\(", "grant (scan path)"), (r"SG_HD void end_app\(", "end_app/outputs"),
+        (r"SG_HD void run_from_busy\(", "advance (phase 0)"), (r"SG_HD bool run\(", "event loop"),
+        (r"SG_HD void finish\(", "finish/stats")],
+    "sgpu_lane.cu": [
+        (r"void lane_trace_range\(", "staging"), (r"bool lane_run\(", "lane setup"),
+        (r"__global__", "kernel body"), (r"exact fallback", "fallback"),
+        (r"static inline uint32_t align16", "host")],
+}
+STARTS = {}
+for fname, marks in MARKS.items():
+    lines = open(CSRC + fname).read().split("\n")
+    st = []
+    for i, l in enumerate(lines, 1):
+        for rx, name in marks:
+            if re.search(rx, l):
+                st.append((i, name))
+    STARTS[fname] = sorted(st)
 
 
-def region(n):
+def region(fname, n):
     r = "header/helpers"
-    for s, name in starts:
+    for s, name in STARTS[fname]:
         if n >= s:
             r = name
     return r
@@ -51,7 +59,7 @@ for r in rows:
         cur_line = int(r[0])
         continue
     if len(r) > ie and r[2].startswith("0x") and r[ie].isdigit():
-        k = region(cur_line) if cur_file == "sgpu_lane.cu" else f"[{cur_file}]"
+        k = region(cur_file, cur_line) if cur_file in STARTS else f"[{cur_file}]"
         inst[k] += int(r[ie])
         thr[k] += int(r[te]) if r[te].isdigit() else 0
 tot = sum(inst.values())
