@@ -240,7 +240,7 @@ def measured_traffic(config, traces_per_gpu):
     from paper_1712_04495_b200.tracegen import CONFIGS
     if t.get("config") != config or traces_per_gpu != CONFIGS[config].n_traces:
         return None
-    return int(t["dram_bytes_read"]) + int(t["dram_bytes_write"])
+    return int(t["dram_bytes_read"]) + int(t["dram_bytes_write"]), t.get("issue_active_pct")
 
 
 def dist_env():
@@ -415,7 +415,7 @@ def main():
     mean_k = statistics.mean(kern_ms) / 1000.0
     peak, peak_src = hbm_peak()
     achieved = alg_bytes / mean_k / 1e9
-    traffic = measured_traffic(args.config, n)
+    traffic, issue_pct = measured_traffic(args.config, n) or (None, None)
 
     # e2e through the C ABI host-buffer pipeline
     e2e = None
@@ -480,7 +480,9 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch",
                          "traffic_source": TRAFFIC_SOURCE if traffic else None, "peak_source": peak_src,
                          "kernel": os.environ.get("SGPU_K1_NAME", "trace_sim_lane_kernel"), "alg_bytes_per_launch": alg_bytes,
-                         "mean_launch_ms": mean_k * 1000.0},
+                         "mean_launch_ms": mean_k * 1000.0,
+                         # what bounds this kernel instead: issue slots (the ncu capture above)
+                         "issue_active_frac": issue_pct / 100.0 if issue_pct else None},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
