@@ -122,7 +122,7 @@ static int simulate_device(const sg_batch* in, const sg_out* out, cudaStream_t s
     sg::sim_layout(p, s.program, s.f64);
     if (p.warp_bytes > 227u * 1024u)
         return fail(E_RANGE, "shared memory per warp exceeds 227 KB (n_pad=%u)", s.n_pad);
-    // K1 engine: the lane kernel (v4) where eligible, else the warp kernel
+    // K1 engine: the lane kernel (v5) where eligible, else the warp kernel
     // (v3).  SGPU_K1=warp|lane overrides (A/B runs and parity tests).
     const char* eng = getenv("SGPU_K1");
     const bool want_warp = eng && strcmp(eng, "warp") == 0;

@@ -44,7 +44,7 @@ void sim_layout(SimParams& p, bool program_mode, bool f64);
 cudaError_t launch_sim(const SimParams& p, bool program_mode, bool f64, cudaStream_t stream,
                        int* grid_out);
 
-// K1 v4: lane-per-(trace, device, policy) kernel for T0 tick-mode batches
+// K1 v5: lane-per-(trace, device, policy) kernel for T0 tick-mode batches
 // (sgpu_lane.cu), with an in-kernel exact fallback to TraceSim.
 bool lane_eligible(const SimParams& p, bool program_mode, bool f64, bool forced);
 cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_out);

@@ -1,5 +1,7 @@
-// sgpu_lane.cu — K1 v4 `trace_sim_lane`: one LANE simulates one (trace,
+// sgpu_lane.cu — K1 v5 `trace_sim_lane`: one LANE simulates one (trace,
 // device, policy) of a T0 (burst) batch, 32 simulations per warp in SIMT.
+// This file stages traces into shared memory and launches; the per-lane
+// simulator itself (LaneSim) is in sgpu_lanesim.cuh.
 //
 // Same semantics as trace_sim_kernel (sgpu_sim.cu),
 // restated for a single thread.  The T0 shape (cpu(arrival) -> alloc ->
@@ -10,27 +12,30 @@
 //    c increasing in the app index, so arrivals pop in (a, index) order: a
 //    per-trace sort, shared by every lane of the trace, replaces those heap
 //    entries.  Heap counters are restated as order-preserving virtual
-//    counters: the initial pop of app i owns the counter block [i << LOGN,
-//    (i + 1) << LOGN) (its arrival push, or the pushes its inline run at
-//    t = 0 makes), and every later push counts up from n << LOGN.  Comparing
-//    (t, virtual counter) is therefore the reference's (t, counter) order
-//    (harness.py:505-508, 563-565).
+//    counters (LaneKey): the initial pop of app i owns counter i (its
+//    arrival push, or the one busy end its inline run at t = 0 pushes), and
+//    every later push counts up from N.  Comparing (t, virtual counter) is
+//    therefore the reference's (t, counter) order (harness.py:505-508,
+//    563-565).  32-bit keys when every time of the group's traces fits,
+//    else 64-bit keys.
 //  * Wake-ups.  grant_waiters pushes each granted waiter at (now, ++counter)
 //    (harness.py:558): later than every pending entry of time `now`, earlier
-//    than any entry of a later time.  They are a per-lane FIFO, drained once
-//    no arrival / busy end of time `now` remains.  The heap keeps busy ends
-//    only: per-lane binary heap in shared memory, laid out [slot][lane] so a
-//    warp's accesses are bank-conflict free whatever slot each lane touches.
+//    than any entry of a later time.  They sit in a per-lane FIFO, drained in
+//    one inner loop once no arrival / busy end of time `now` remains.  The
+//    heap keeps busy ends only: a 4-ary heap of depth 2 per lane in shared
+//    memory, laid out [slot][lane] so a warp's accesses are bank-conflict
+//    free whatever slot each lane touches.
 //  * Wait queue.  An app enqueues at most once, at its arrival pop, so the
 //    queue (harness.py:532-536) is a presence bitmask over arrival positions,
 //    in registers; queue order is position order.  select_grants
-//    (policy.py:52-74) works on masks: the priority kinds restrict to the
-//    top class (per-trace class masks, policy.py:58-63), FIFO grants the
-//    head while it fits, MMU takes first fits with a shrinking budget.  For
-//    traces of <= 64 apps MMU is O(1) per grant: a per-trace table T[r] of
-//    the positions whose request is among the r smallest gives the set that
-//    fits `budget` as T[#requests <= budget] (one binary search), and the
-//    next first fit is the lowest bit of mask & class & T & above(last).
+//    (policy.py:52-74) works on masks, one step per loop iteration: the
+//    priority kinds restrict to the top class (per-trace class masks,
+//    policy.py:58-63), FIFO grants the head while it fits, MMU takes first
+//    fits with a shrinking budget.  For traces of <= 128 apps each step is
+//    O(1): a per-trace table T[r] of the positions whose request is among the
+//    r smallest gives the set that fits `budget` as T[#requests <= budget]
+//    (bucket lookup), and the next first fit is the lowest bit of
+//    mask & class & T above the last grant.
 //
 // Lanes that cannot take this path (heap or FIFO capacity exceeded, too many
 // priority classes, or a trace whose times could leave the 32-bit tick

@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(params=["auto", "warp"], autouse=True)
 def engine(request, monkeypatch):
     """Every parity test runs on both K1 engines: `auto` takes the lane kernel
-    (v4) wherever the batch is eligible (T0, <= 256 apps), `warp` forces the
+    (v5) wherever the batch is eligible (T0, <= 128 apps), `warp` forces the
     warp-per-trace kernel (v3)."""
     if request.param == "warp":
         monkeypatch.setenv("SGPU_K1", "warp")
