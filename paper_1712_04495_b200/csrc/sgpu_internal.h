@@ -34,7 +34,7 @@ struct SimParams {
     uint32_t* event_counts;
     // per-warp shared-memory layout (bytes)
     uint32_t off_app, off_sub, off_idx, off_key, off_kc, off_q, off_grant, off_end, off_st, off_held,
-        off_bar, warp_bytes;
+        off_pc, off_bar, warp_bytes;
 };
 
 // Shared-memory layout for one warp simulating traces of up to n_pad apps.

@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel
 #pragma unroll
             for (uint32_t j = 1; j < SG_MAX_DEV; j++)
                 if (fd == j) fcap = P.cap[j];
-            TraceSim<TickTM, K, false> sim(P, lane, fb, sub);
+            TraceSim<TickTM, K, false, false> sim(P, lane, fb, sub);
             sim.run(nd, (P.policy_list >> (4 * fp)) & 0xFu, fcap, nullptr);
             sim.finish(((uint64_t)fp * P.n_traces + t) * ndev + fd, (uint64_t)fp * P.n_apps_total + a0,
                        idx, nullptr);

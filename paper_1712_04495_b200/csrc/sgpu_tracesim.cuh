@@ -176,7 +176,10 @@ __device__ __forceinline__ uint32_t build_subtrace(const uint4* apps, uint32_t n
 }
 
 // One (sub-)trace of n apps on one simulated device under one policy.
-template <class TM, int K, bool PROG>
+// PSET: T0 priority kinds keep a per-priority presence set (O(1) top class);
+// the lane kernel's rarely taken fallback instance scans instead, which keeps
+// that kernel's register allocation independent of this path.
+template <class TM, int K, bool PROG, bool PSET = true>
 struct TraceSim {
     using T = typename TM::T;
     using Key = typename TM::Key;
@@ -193,6 +196,7 @@ struct TraceSim {
     T* s_end;
     uint16_t* s_st;
     int32_t* s_held;
+    uint16_t* s_pc;           // T0 priority kinds: waiting entries per priority
     // trace / policy
     uint32_t n, cap;
     bool prio_pol, mmu;
@@ -202,6 +206,7 @@ struct TraceSim {
     uint32_t qtail;           // T0: next queue position (apps enqueue at most once)
     uint32_t qhead;           // T0 FIFO: first waiting position
     uint32_t qm_lane;         // T0: lane j holds the presence bits of queue positions 32j..32j+31
+    uint32_t pm_lane;         // T0 priority kinds: lane j < 8 holds the waiting priorities 32j..32j+31
     // statistics (harness.py:373-461 integer forms)
     T last, mem_t, busy_prev;
     typename TM::Acc I, B;
@@ -222,6 +227,7 @@ struct TraceSim {
         s_end = reinterpret_cast<T*>(ws + p.off_end);
         s_st = reinterpret_cast<uint16_t*>(ws + p.off_st);
         s_held = reinterpret_cast<int32_t*>(ws + p.off_held);
+        s_pc = reinterpret_cast<uint16_t*>(ws + p.off_pc);
     }
 
     // harness.py:505-508: a push takes the next counter value
@@ -312,14 +318,21 @@ struct TraceSim {
             const uint32_t active = __ballot_sync(FULL, qm_lane != 0);  // chunks with waiters
             if (prio_pol) {
                 // top = max waiting priority (policy.py:58-63)
-                uint32_t best = 0;
-                for (uint32_t a = active; a; a &= a - 1) {
-                    const uint32_t j = __ffs(a) - 1;
-                    const uint32_t m = __shfl_sync(FULL, qm_lane, j);
-                    const uint64_t e = s_q[32 * j + lane];
-                    if ((m >> lane) & 1u) best = max(best, q_prio(e) + 1);
+                if constexpr (PSET) {
+                    // the highest bit of the per-priority presence set
+                    const uint32_t hb = __ballot_sync(FULL, pm_lane != 0);
+                    const uint32_t j = 31u - __clz(hb);
+                    top = 32u * j + 31u - __clz(__shfl_sync(FULL, pm_lane, j));
+                } else {
+                    uint32_t best = 0;
+                    for (uint32_t a = active; a; a &= a - 1) {
+                        const uint32_t j = __ffs(a) - 1;
+                        const uint32_t m = __shfl_sync(FULL, qm_lane, j);
+                        const uint64_t e = s_q[32 * j + lane];
+                        if ((m >> lane) & 1u) best = max(best, q_prio(e) + 1);
+                    }
+                    top = __reduce_max_sync(FULL, best) - 1;
                 }
-                top = __reduce_max_sync(FULL, best) - 1;
             }
             uint32_t granted = 0;
             bool stop = false;
@@ -374,6 +387,13 @@ struct TraceSim {
                 maxh = max(maxh, (uint32_t)holders);
                 grants += granted;
                 qlen -= granted;
+                if (PSET && prio_pol) {  // every grant of the round was of priority `top`
+                    const uint32_t left = s_pc[top] - granted;
+                    __syncwarp();
+                    if (lane == 0) s_pc[top] = (uint16_t)left;
+                    __syncwarp();
+                    if (left == 0 && lane == (top >> 5)) pm_lane &= ~(1u << (top & 31u));
+                }
             }
             // FIFO/MMU: a second round is provably empty; priority policies
             // drain the top class and may serve the next one (harness.py:547-550)
@@ -500,6 +520,12 @@ struct TraceSim {
                 } else {                   // wait (harness.py:532-536)
                     s_q[qtail] = q_pack(app, min(f.y, kSat), f.w & 0xFFu);
                     if (lane == (qtail >> 5)) qm_lane |= 1u << (qtail & 31);
+                    if (PSET && prio_pol) {
+                        const uint32_t p = f.w & 0xFFu;
+                        if (lane == 0) s_pc[p] += 1;
+                        if (lane == (p >> 5)) pm_lane |= 1u << (p & 31u);
+                        __syncwarp();
+                    }
                     qtail += 1;
                     qlen += 1;
                     TM::store(s_kt, s_kc, app, nk);
@@ -626,6 +652,13 @@ struct TraceSim {
         qtail = 0;
         qhead = 0;
         qm_lane = 0;
+        pm_lane = 0;
+        if constexpr (!PROG && PSET) {
+            if (prio_pol) {
+                for (uint32_t i = lane; i < 128; i += 32) reinterpret_cast<uint32_t*>(s_pc)[i] = 0;
+                __syncwarp();
+            }
+        }
         last = mem_t = busy_prev = TM::zero();
         I = 0;
         B = 0;
