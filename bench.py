@@ -317,6 +317,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: check the multi-rank flow with several ranks on one GPU")
     args = ap.parse_args()
     ws, rank, local = dist_env()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
@@ -337,10 +339,15 @@ def main():
     from paper_1712_04495_b200 import parallel as PAR
     from paper_1712_04495_b200.policy import policy_mask
 
+    if args.dist_backend == "gloo":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     n = args.traces
     t_begin = rank * n
