@@ -42,6 +42,9 @@
 // range) are re-simulated by the whole warp with the exact warp-per-trace
 // TraceSim (sgpu_tracesim.cuh) right after, in the same kernel: no host
 // round trip, no extra buffers.
+#include <map>
+#include <mutex>
+
 #include "sgpu_lanesim.cuh"
 
 namespace sg {
@@ -58,6 +61,9 @@ struct LaneParams {
     // per-warp shared-memory layout (bytes)
     uint32_t off_a, off_mem, off_bw, off_por, off_lt, off_tbl, off_cm, off_meta, off_fifo, off_fb,
         warp_bytes;
+    // dynamic group scheduling: group = atomicAdd(work, 1) - work_base
+    unsigned long long* work;
+    uint64_t work_base;
 };
 
 // Per-trace-slot strides (in elements) of the shared arrays, skewed so the
@@ -464,9 +470,16 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel
     const uint32_t lane = lane_id();
     uint8_t* ws = smem + (size_t)warp * L.warp_bytes;
     const uint64_t n_groups = (P.n_traces + L.G - 1) / L.G;
-    const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
     const uint32_t ndev = P.ndev;
+    // groups are handed out by one atomic counter (each warp takes the next
+    // group when it finishes one): no tail of warps with more groups than
+    // others.  Every warp makes exactly one fetch past the end, so a launch
+    // advances the counter by n_groups + warps (tracked on the host).
+    auto fetch = [&]() -> uint64_t {
+        unsigned long long v = 0;
+        if (lane == 0) v = atomicAdd(L.work, 1ull);
+        return (uint64_t)__shfl_sync(FULL, v, 0) - L.work_base;
+    };
 
     // lane -> (slot, device, policy slot)
     const uint32_t g = lane / L.lpt;
@@ -479,13 +492,15 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel
     for (uint32_t j = 1; j < SG_MAX_DEV; j++)
         if (d == j) cap_d = P.cap[j];
 
-    for (uint64_t grp = gw; grp < n_groups; grp += stride) {
+    uint64_t grp = fetch();
+    while (grp < n_groups) {
+        const uint64_t next = fetch();
         const uint64_t t0 = grp * L.G;
         const uint32_t gcount = (uint32_t)min((uint64_t)L.G, P.n_traces - t0);
         for (uint32_t s = 0; s < gcount; s++) stage_trace<K>(L, ws, s, t0 + s, lane);
         // warm L2 with the next group's records while this one simulates
-        if (grp + stride < n_groups && !P.trace_offsets) {
-            const uint64_t nt0 = (grp + stride) * L.G;
+        if (next < n_groups && !P.trace_offsets) {
+            const uint64_t nt0 = next * L.G;
             const uint64_t nb = min((uint64_t)L.G, P.n_traces - nt0) * P.apps_per_trace * 16u;
             const uint8_t* base = reinterpret_cast<const uint8_t*>(P.apps + nt0 * P.apps_per_trace);
             for (uint64_t off = (uint64_t)lane * 128u; off < nb; off += 32u * 128u) prefetch_l2(base + off);
@@ -540,10 +555,62 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel
                        idx, nullptr);
         }
         __syncwarp();
+        grp = next;
     }
 }
 
 static inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
+
+// Group counters for dynamic scheduling, one per (device, stream): launches
+// on one stream are ordered, so the host knows each counter's value at the
+// start of the next launch (it advances by exactly n_groups + warps).
+// Allocated once per device as a pool; streams take slots round robin.
+namespace {
+constexpr int kWorkSlots = 512;
+struct WorkPool {
+    unsigned long long* ctr = nullptr;
+    uint64_t base[kWorkSlots] = {};
+    std::map<cudaStream_t, int> slot;
+    int next = 0;
+};
+std::mutex g_work_mu;
+std::map<int, WorkPool> g_work;
+}  // namespace
+
+static cudaError_t work_counter(cudaStream_t stream, unsigned long long** ctr, int* slot, uint64_t* base) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(g_work_mu);
+    WorkPool& w = g_work[dev];
+    if (!w.ctr) {
+        e = cudaMalloc(&w.ctr, kWorkSlots * sizeof(unsigned long long));
+        if (e == cudaSuccess) e = cudaMemset(w.ctr, 0, kWorkSlots * sizeof(unsigned long long));
+        if (e != cudaSuccess) { w.ctr = nullptr; return e; }
+    }
+    auto it = w.slot.find(stream);
+    int s;
+    if (it == w.slot.end()) {
+        s = w.next;
+        w.next = (w.next + 1) % kWorkSlots;
+        // a reused slot's previous stream has been idle for kWorkSlots new streams
+        for (auto i = w.slot.begin(); i != w.slot.end();) i = i->second == s ? w.slot.erase(i) : std::next(i);
+        w.slot[stream] = s;
+    } else {
+        s = it->second;
+    }
+    *ctr = w.ctr + s;
+    *slot = s;
+    *base = w.base[s];
+    return cudaSuccess;
+}
+
+static void work_consumed(int slot, uint64_t n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_work_mu);
+    g_work[dev].base[slot] += n;
+}
 
 // Lane path eligibility: T0 ticks mode, no event log, <= 256 apps per trace.
 // By default traces of <= 128 apps take it (measured on one B200: C4, 128
@@ -579,8 +646,13 @@ static cudaError_t launch_lane_t(LaneParams& L, cudaStream_t stream, int* grid_o
     if (need < grid) grid = need;
     if (grid == 0) grid = 1;
     if (grid_out) *grid_out = (int)grid;
+    int slot = 0;
+    err = work_counter(stream, &L.work, &slot, &L.work_base);
+    if (err != cudaSuccess) return err;
     kern<<<(unsigned)grid, wpb * 32, smem, stream>>>(L);
-    return cudaGetLastError();
+    err = cudaGetLastError();
+    if (err == cudaSuccess) work_consumed(slot, groups + grid * wpb);
+    return err;
 }
 
 cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_out) {
