@@ -35,7 +35,16 @@ struct SimParams {
     // per-warp shared-memory layout (bytes)
     uint32_t off_app, off_sub, off_idx, off_key, off_kc, off_q, off_grant, off_end, off_st, off_held,
         off_pc, off_bar, warp_bytes;
+    // dynamic scheduling: work item = atomicAdd(work, 1) - work_base
+    unsigned long long* work;
+    uint64_t work_base;
 };
+
+// Work counter of `stream` on the current device for a launch that will
+// consume `items` counter values (work items + one failing fetch per warp):
+// sets p.work / p.work_base; call work_commit() once the launch succeeded.
+cudaError_t work_reserve(cudaStream_t stream, SimParams& p, int* slot);
+void work_commit(int slot, uint64_t items);
 
 // Shared-memory layout for one warp simulating traces of up to n_pad apps.
 void sim_layout(SimParams& p, bool program_mode, bool f64);

@@ -42,9 +42,6 @@
 // range) are re-simulated by the whole warp with the exact warp-per-trace
 // TraceSim (sgpu_tracesim.cuh) right after, in the same kernel: no host
 // round trip, no extra buffers.
-#include <map>
-#include <mutex>
-
 #include "sgpu_lanesim.cuh"
 
 namespace sg {
@@ -61,9 +58,6 @@ struct LaneParams {
     // per-warp shared-memory layout (bytes)
     uint32_t off_a, off_mem, off_bw, off_por, off_lt, off_tbl, off_cm, off_meta, off_fifo, off_fb,
         warp_bytes;
-    // dynamic group scheduling: group = atomicAdd(work, 1) - work_base
-    unsigned long long* work;
-    uint64_t work_base;
 };
 
 // Per-trace-slot strides (in elements) of the shared arrays, skewed so the
@@ -477,8 +471,8 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel
     // advances the counter by n_groups + warps (tracked on the host).
     auto fetch = [&]() -> uint64_t {
         unsigned long long v = 0;
-        if (lane == 0) v = atomicAdd(L.work, 1ull);
-        return (uint64_t)__shfl_sync(FULL, v, 0) - L.work_base;
+        if (lane == 0) v = atomicAdd(P.work, 1ull);
+        return (uint64_t)__shfl_sync(FULL, v, 0) - P.work_base;
     };
 
     // lane -> (slot, device, policy slot)
@@ -561,56 +555,6 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel
 
 static inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
-// Group counters for dynamic scheduling, one per (device, stream): launches
-// on one stream are ordered, so the host knows each counter's value at the
-// start of the next launch (it advances by exactly n_groups + warps).
-// Allocated once per device as a pool; streams take slots round robin.
-namespace {
-constexpr int kWorkSlots = 512;
-struct WorkPool {
-    unsigned long long* ctr = nullptr;
-    uint64_t base[kWorkSlots] = {};
-    std::map<cudaStream_t, int> slot;
-    int next = 0;
-};
-std::mutex g_work_mu;
-std::map<int, WorkPool> g_work;
-}  // namespace
-
-static cudaError_t work_counter(cudaStream_t stream, unsigned long long** ctr, int* slot, uint64_t* base) {
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    std::lock_guard<std::mutex> lk(g_work_mu);
-    WorkPool& w = g_work[dev];
-    if (!w.ctr) {
-        e = cudaMalloc(&w.ctr, kWorkSlots * sizeof(unsigned long long));
-        if (e == cudaSuccess) e = cudaMemset(w.ctr, 0, kWorkSlots * sizeof(unsigned long long));
-        if (e != cudaSuccess) { w.ctr = nullptr; return e; }
-    }
-    auto it = w.slot.find(stream);
-    int s;
-    if (it == w.slot.end()) {
-        s = w.next;
-        w.next = (w.next + 1) % kWorkSlots;
-        // a reused slot's previous stream has been idle for kWorkSlots new streams
-        for (auto i = w.slot.begin(); i != w.slot.end();) i = i->second == s ? w.slot.erase(i) : std::next(i);
-        w.slot[stream] = s;
-    } else {
-        s = it->second;
-    }
-    *ctr = w.ctr + s;
-    *slot = s;
-    *base = w.base[s];
-    return cudaSuccess;
-}
-
-static void work_consumed(int slot, uint64_t n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lk(g_work_mu);
-    g_work[dev].base[slot] += n;
-}
 
 // Lane path eligibility: T0 ticks mode, no event log, <= 256 apps per trace.
 // By default traces of <= 128 apps take it (measured on one B200: C4, 128
@@ -647,11 +591,11 @@ static cudaError_t launch_lane_t(LaneParams& L, cudaStream_t stream, int* grid_o
     if (grid == 0) grid = 1;
     if (grid_out) *grid_out = (int)grid;
     int slot = 0;
-    err = work_counter(stream, &L.work, &slot, &L.work_base);
+    err = work_reserve(stream, L.sp, &slot);
     if (err != cudaSuccess) return err;
     kern<<<(unsigned)grid, wpb * 32, smem, stream>>>(L);
     err = cudaGetLastError();
-    if (err == cudaSuccess) work_consumed(slot, groups + grid * wpb);
+    if (err == cudaSuccess) work_commit(slot, groups + grid * wpb);
     return err;
 }
 

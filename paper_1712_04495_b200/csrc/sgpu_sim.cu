@@ -30,6 +30,9 @@
 //   * traces with several simulated devices run as per-device sub-traces: the
 //     devices share only the global push counter, whose interleaving cannot
 //     reorder events of one device (pinned by tests/golden/ref_multidev.npz)
+#include <map>
+#include <mutex>
+
 #include "sgpu_tracesim.cuh"
 
 namespace sg {
@@ -54,8 +57,13 @@ __global__ void SG_SIM_BOUNDS trace_sim_kernel(const SimParams P) {
     uint64_t* bar = reinterpret_cast<uint64_t*>(ws + P.off_bar);
     const uint32_t buf_bytes = P.n_pad * 16u;
 
-    const uint64_t gw = (uint64_t)blockIdx.x * wpb + warp;
-    const uint64_t stride = (uint64_t)gridDim.x * wpb;
+    // traces are handed out by one atomic counter (sgpu_internal.h
+    // work_reserve); each warp makes exactly one fetch past the end
+    auto fetch = [&]() -> uint64_t {
+        unsigned long long v = 0;
+        if (lane == 0) v = atomicAdd(P.work, 1ull);
+        return (uint64_t)__shfl_sync(FULL, v, 0) - P.work_base;
+    };
 
     auto trace_range = [&](uint64_t t, uint64_t& a0, uint32_t& na) {
         if (P.trace_offsets) {
@@ -79,6 +87,7 @@ __global__ void SG_SIM_BOUNDS trace_sim_kernel(const SimParams P) {
         }
     };
 
+    uint64_t t = fetch();
     if constexpr (!PROG) {
         if (lane == 0) {
             mbar_init(&bar[0], 1);
@@ -86,11 +95,12 @@ __global__ void SG_SIM_BOUNDS trace_sim_kernel(const SimParams P) {
             fence_mbar_init();
         }
         __syncwarp();
-        if (gw < P.n_traces) stage(gw, 0);
+        if (t < P.n_traces) stage(t, 0);
     }
 
     uint32_t iter = 0;
-    for (uint64_t t = gw; t < P.n_traces; t += stride, iter++) {
+    while (t < P.n_traces) {
+        const uint64_t next = fetch();
         uint64_t a0;
         uint32_t na;
         trace_range(t, a0, na);
@@ -98,7 +108,7 @@ __global__ void SG_SIM_BOUNDS trace_sim_kernel(const SimParams P) {
         if constexpr (!PROG) {
             mbar_wait(&bar[b], (iter >> 1) & 1u);
             __syncwarp();
-            if (t + stride < P.n_traces) stage(t + stride, b ^ 1u);
+            if (next < P.n_traces) stage(next, b ^ 1u);
         } else {
             uint4* dst = reinterpret_cast<uint4*>(ws + P.off_app);
             const uint32_t s0 = P.step_offsets[0];
@@ -138,10 +148,64 @@ __global__ void SG_SIM_BOUNDS trace_sim_kernel(const SimParams P) {
             }
         }
         __syncwarp();
+        t = next;
+        iter++;
     }
 }
 
 // ------------------------------------------------------------------ launch
+
+// Group counters for dynamic scheduling, one per (device, stream): launches
+// on one stream are ordered, so the host knows each counter's value at the
+// start of the next launch (it advances by exactly n_groups + warps).
+// Allocated once per device as a pool; streams take slots round robin.
+namespace {
+constexpr int kWorkSlots = 512;
+struct WorkPool {
+    unsigned long long* ctr = nullptr;
+    uint64_t base[kWorkSlots] = {};
+    std::map<cudaStream_t, int> slot;
+    int next = 0;
+};
+std::mutex g_work_mu;
+std::map<int, WorkPool> g_work;
+}  // namespace
+
+cudaError_t work_reserve(cudaStream_t stream, SimParams& p, int* slot) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(g_work_mu);
+    WorkPool& w = g_work[dev];
+    if (!w.ctr) {
+        e = cudaMalloc(&w.ctr, kWorkSlots * sizeof(unsigned long long));
+        if (e == cudaSuccess) e = cudaMemset(w.ctr, 0, kWorkSlots * sizeof(unsigned long long));
+        if (e != cudaSuccess) { w.ctr = nullptr; return e; }
+    }
+    auto it = w.slot.find(stream);
+    int s;
+    if (it == w.slot.end()) {
+        s = w.next;
+        w.next = (w.next + 1) % kWorkSlots;
+        // a reused slot's previous stream has been idle for kWorkSlots new streams
+        for (auto i = w.slot.begin(); i != w.slot.end();) i = i->second == s ? w.slot.erase(i) : std::next(i);
+        w.slot[stream] = s;
+    } else {
+        s = it->second;
+    }
+    p.work = w.ctr + s;
+    p.work_base = w.base[s];
+    *slot = s;
+    return cudaSuccess;
+}
+
+void work_commit(int slot, uint64_t n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_work_mu);
+    g_work[dev].base[slot] += n;
+}
+
 
 static inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
@@ -203,8 +267,14 @@ static cudaError_t launch_t(const SimParams& p, cudaStream_t stream, int* grid_o
     if (need < grid) grid = need;
     if (grid == 0) grid = 1;
     if (grid_out) *grid_out = (int)grid;
-    kern<<<(unsigned)grid, wpb * 32, smem, stream>>>(p);
-    return cudaGetLastError();
+    SimParams q = p;
+    int slot = 0;
+    err = work_reserve(stream, q, &slot);
+    if (err != cudaSuccess) return err;
+    kern<<<(unsigned)grid, wpb * 32, smem, stream>>>(q);
+    err = cudaGetLastError();
+    if (err == cudaSuccess) work_commit(slot, p.n_traces + grid * wpb);
+    return err;
 }
 
 template <class TM, bool PROG>

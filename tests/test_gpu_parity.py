@@ -335,3 +335,24 @@ def test_host_pipeline_cases(case, cuda):
     np.testing.assert_array_equal(host.stats.view(np.uint8), dres.stats().view(np.uint8))
     if case == "overflow":
         assert (dres.stats()["status"] & 1).any()
+
+
+def test_work_counters_across_streams_and_sizes(cuda):
+    """Dynamic scheduling hands out work items from one counter per stream
+    whose base the host tracks launch by launch: many launches of varying
+    size, interleaved over several streams (and both engines, via the
+    fixture), must each cover every trace exactly once."""
+    cfg = CONFIGS["C2"]
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    rng = np.random.default_rng(11)
+    for i in range(24):
+        n = int(rng.choice([1, 7, 33, 100, 257, 1000]))
+        apps = as_u32x4(generate(dataclasses.replace(cfg.gen, seed=200 + i), 0, n))
+        s = streams[i % 3]
+        with torch.cuda.stream(s):
+            res = B.simulate_batch(to_dev(apps, cuda), ("fifo", "pmmu"), cfg.cap_mib, stream=s)
+        s.synchronize()
+        for pi, pol in enumerate(res.policies):
+            g, e, st = O.simulate_burst(apps, cfg.cap_mib, pol.value)
+            np.testing.assert_array_equal(res.ticks("end")[pi].reshape(e.shape), e, err_msg=f"launch {i}")
+            np.testing.assert_array_equal(res.stats()[pi].view(np.uint8), st.view(np.uint8))
