@@ -48,6 +48,11 @@ namespace sg {
 
 constexpr uint32_t kLaneClassMasks = 64;    // class masks per warp, split over its trace slots
 constexpr int kLaneWarpsPerBlock = 2;      // two warps share a block's 1 KB smem reservation
+// Resident two-warp blocks per SM the register allocation is sized for.
+// Nine (18 warps) caps registers at 96 per thread: a win for 128-app traces
+// (C4: 3.46e7 -> 4.13e7 trace-sims/s), a small loss at 64 apps (C2: 18.13
+// -> 18.30 ms), where eight blocks keep 118 registers (one-box A/B).
+template <int K> struct LaneMinBlocks { static constexpr int v = K == 2 ? 8 : 9; };
 struct LaneParams {
     SimParams sp;          // inputs/outputs + the fallback TraceSim layout (off_* relative to the warp region)
     uint32_t G;            // traces per warp (32 / lpt)
@@ -55,25 +60,30 @@ struct LaneParams {
     uint32_t need_cls;     // a priority policy is requested: build class masks
     uint32_t need_tbl;     // an MMU-type policy on <= 64-app traces: build the fit table
     uint32_t cm_per_trace; // class-mask capacity of one trace slot
+    uint32_t meta_stride;  // u16 per trace slot of the meta array
     // per-warp shared-memory layout (bytes)
     uint32_t off_a, off_mem, off_bw, off_por, off_lt, off_tbl, off_cm, off_meta, off_fifo, off_fb,
         warp_bytes;
 };
 
-// Per-trace-slot strides (in elements) of the shared arrays, skewed so the
-// slots of a warp start on different banks: 16-byte loads of the 8 slots of
-// a warp (fence / block / table reads) hit disjoint bank groups.
+// Per-trace-slot strides (in elements) of the shared arrays.  The u32
+// record arrays hold N entries + the s_mem[N] sentinel; an odd stride skews
+// the slots of a warp onto different banks.
 template <uint32_t N> struct SlotStride {
-    static constexpr uint32_t S32 = N + 4;          // u32 record arrays
-    static constexpr uint32_t POR = N + 16;         // rank -> position (u8, padded)
-    static constexpr uint32_t LTB = kLtBuckets + 16;  // rank lookup: u8 buckets + 3 u32 params (+skew)
-    static constexpr uint32_t T4 = (N / 4 + 2) * ((N + 63) / 64);  // fit table at every 4th rank (N/4 + 1 entries of NW words)
+    static constexpr uint32_t S32 = N + 1;          // u32 record arrays
+    static constexpr uint32_t POR = N + 4;          // rank -> position (u8) + 4 sentinels
+    static constexpr uint32_t LTB = kLtBuckets + 12;  // rank lookup: u8 buckets + 3 u32 params
+    static constexpr uint32_t T4 = (N / 4 + 1) * ((N + 63) / 64);  // fit table at every 4th rank (NW words)
 };
 
-// meta per trace slot (u16): [0] n, [1] fail (big times / too many classes),
-// [2..10] device bounds in arrival order, [11..18] apps arriving at t = 0 per
-// device, [19..27] class-mask index bounds per device, [30] 32-bit event keys allowed
-constexpr uint32_t kMetaU16 = 32;
+// meta per trace slot (u16), for ndev devices: [0] n, [1] fail (big times /
+// too many classes), [2] 32-bit keys allowed, [3 + d] (d = 0..ndev) device
+// bounds in arrival order, [4 + ndev + d] apps of device d arriving at t = 0,
+// [4 + 2 ndev + d] (d = 0..ndev) class-mask index bounds per device
+__host__ __device__ constexpr uint32_t meta_dev(uint32_t d) { return 3u + d; }
+__host__ __device__ constexpr uint32_t meta_z(uint32_t ndev, uint32_t d) { return 4u + ndev + d; }
+__host__ __device__ constexpr uint32_t meta_cls(uint32_t ndev, uint32_t d) { return 4u + 2u * ndev + d; }
+__host__ __device__ constexpr uint32_t meta_u16(uint32_t ndev) { return (5u + 3u * ndev + 7u) & ~7u; }
 
 __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
     const uint32_t lo = __shfl_xor_sync(FULL, (uint32_t)v, m);
@@ -181,7 +191,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
     uint32_t* s_a = reinterpret_cast<uint32_t*>(ws + L.off_a) + g * SS::S32;
     uint32_t* s_mem = reinterpret_cast<uint32_t*>(ws + L.off_mem) + g * SS::S32;
     uint32_t* s_bw = reinterpret_cast<uint32_t*>(ws + L.off_bw) + g * SS::S32;
-    uint16_t* meta = reinterpret_cast<uint16_t*>(ws + L.off_meta) + g * kMetaU16;
+    uint16_t* meta = reinterpret_cast<uint16_t*>(ws + L.off_meta) + g * L.meta_stride;
     const uint32_t ndev = P.ndev;
 
     uint64_t key[K];
@@ -250,7 +260,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
         // one device, priorities below 32: the classes (policy.py:58-63) are
         // the distinct priorities, highest first; class index = number of
         // distinct priorities above the app's own
-        uint64_t* cm = reinterpret_cast<uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW + 1);
+        uint64_t* cm = reinterpret_cast<uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW);
         uint32_t pres = 0;
 #pragma unroll
         for (int k = 0; k < K; k++) pres |= key[k] != kInf ? 1u << prk[k] : 0u;
@@ -276,12 +286,12 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
                     if (lane == 0) cm[c * NW + w] = ((uint64_t)hi << 32) | lo;
                 }
             }
-            if (lane == 0) meta[20] = (uint16_t)ncls_total;
+            if (lane == 0) meta[meta_cls(1, 1)] = (uint16_t)ncls_total;
         }
     } else if (L.need_cls) {
         // classes = (device, priority) groups, highest priority first
         // (policy.py:58-63); one mask of arrival positions per class
-        uint64_t* cm = reinterpret_cast<uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW + 1);
+        uint64_t* cm = reinterpret_cast<uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW);
         uint32_t ck[K];
 #pragma unroll
         for (int k = 0; k < K; k++) {
@@ -330,7 +340,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
                 }
                 before += __popc(bnd[k]);
             }
-            if (lane < ndev) meta[20 + lane] = (uint16_t)cincl;
+            if (lane < ndev) meta[meta_cls(ndev, lane + 1)] = (uint16_t)cincl;
         }
     }
     if (L.need_tbl) {
@@ -406,15 +416,15 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
         if (lane < 4) s_por[N + lane] = (uint8_t)N;
     }
     if (lane < ndev) {
-        meta[3 + lane] = (uint16_t)dincl;
-        meta[11 + lane] = (uint16_t)z_d;
+        meta[meta_dev(lane + 1)] = (uint16_t)dincl;
+        meta[meta_z(ndev, lane)] = (uint16_t)z_d;
     }
     if (lane == 0) {
         meta[0] = (uint16_t)na;
         meta[1] = (uint16_t)fail;
-        meta[30] = narrow ? 1u : 0u;
-        meta[2] = 0;
-        meta[19] = 0;
+        meta[2] = narrow ? 1u : 0u;
+        meta[meta_dev(0)] = 0;
+        meta[meta_cls(ndev, 0)] = 0;
     }
     __syncwarp();
 }
@@ -430,7 +440,8 @@ __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const
     constexpr uint32_t NW = (N + 63u) / 64u;
     using SS = SlotStride<N>;
     const uint32_t na = meta[0];
-    const uint32_t s0 = meta[2 + d], s1 = meta[3 + d], z = meta[11 + d];
+    const uint32_t ndev = P.ndev;
+    const uint32_t s0 = meta[meta_dev(d)], s1 = meta[meta_dev(d + 1)], z = meta[meta_z(ndev, d)];
     uint64_t a0;
     uint32_t na_unused;
     lane_trace_range(P, t, a0, na_unused);
@@ -445,8 +456,8 @@ __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const
     sim.lt_scale = reinterpret_cast<const uint32_t*>(sim.s_lt + kLtBuckets)[2];
     sim.s_t4 = reinterpret_cast<const uint64_t*>(ws + L.off_tbl) + g * SS::T4;
     uint32_t c0 = 0, c1 = 0;
-    if (L.need_cls) { c0 = meta[19 + d]; c1 = meta[20 + d]; }
-    sim.s_cm = reinterpret_cast<const uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW + 1) + c0 * NW;
+    if (L.need_cls) { c0 = meta[meta_cls(ndev, d)]; c1 = meta[meta_cls(ndev, d + 1)]; }
+    sim.s_cm = reinterpret_cast<const uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW) + c0 * NW;
     sim.ncls = c1 - c0;
     sim.heap = reinterpret_cast<typename LaneSim<K, NARROW>::Key*>(ws + L.off_fb) + lane;
     sim.fifo = reinterpret_cast<uint32_t*>(ws + L.off_fifo) + lane;
@@ -457,7 +468,7 @@ __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const
 }
 
 template <int K>
-__global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel(const LaneParams L) {
+__global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, LaneMinBlocks<K>::v) trace_sim_lane_kernel(const LaneParams L) {
     const SimParams& P = L.sp;
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5;
@@ -501,9 +512,9 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32) trace_sim_lane_kernel
         }
 
         bool fail = false;
-        const uint16_t* meta = reinterpret_cast<const uint16_t*>(ws + L.off_meta) + g * kMetaU16;
+        const uint16_t* meta = reinterpret_cast<const uint16_t*>(ws + L.off_meta) + g * L.meta_stride;
         // 32-bit event keys when every trace of the group allows them (warp-uniform)
-        const bool narrow = __all_sync(FULL, g >= gcount || meta[30] != 0);
+        const bool narrow = __all_sync(FULL, g >= gcount || meta[2] != 0);
         if (g < gcount) {
             if (meta[1])
                 fail = true;
@@ -617,7 +628,8 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
     // TraceSim overlays the whole warp region once the group's lanes are done
     sim_layout(L.sp, false, false);
     const uint32_t fb = max(max(kLaneHeapN * 32u * 4u, kLaneHeapW * 32u * 8u), N * 16u);
-    const uint32_t S32 = N + 4, POR = N + 16, LTB = kLtBuckets + 16, T4 = (N / 4 + 2) * NW;  // SlotStride<N>
+    const uint32_t S32 = N + 1, POR = N + 4, LTB = kLtBuckets + 12, T4 = (N / 4 + 1) * NW;  // SlotStride<N>
+    L.meta_stride = meta_u16(p.ndev);
     uint32_t o = 0;
     L.off_a = o;
     o = align16(o + L.G * S32 * 4u);
@@ -632,14 +644,15 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
     L.off_tbl = o;
     o = align16(o + (L.need_tbl ? L.G * T4 * 8u : 0u));
     L.off_cm = o;
-    o = align16(o + (L.need_cls ? L.G * (L.cm_per_trace * NW + 1) * 8u : 0u));
+    o = align16(o + (L.need_cls ? L.G * (L.cm_per_trace * NW) * 8u : 0u));
     L.off_meta = o;
-    o = align16(o + L.G * kMetaU16 * 2u);
+    o = align16(o + L.G * L.meta_stride * 2u);
     L.off_fifo = o;
     o = align16(o + kLaneFifoWords * 32u * 4u);
     L.off_fb = o;
     o = align16(o + fb);
     L.warp_bytes = max(o, align16(L.sp.warp_bytes));
+    if (const char* pad = getenv("SGPU_LANE_SMEM_PAD")) L.warp_bytes += align16((uint32_t)atoi(pad));  // occupancy experiments
     switch (N / 32) {
         case 1: return launch_lane_t<1>(L, stream, grid_out);
         case 2: return launch_lane_t<2>(L, stream, grid_out);

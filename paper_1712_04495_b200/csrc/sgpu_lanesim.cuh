@@ -31,9 +31,9 @@ inline int __ffs(int x) { return __builtin_ffs(x); }
 
 namespace sg {
 
-constexpr uint32_t kLaneHeapN = 21;         // busy-end heap slots per lane, 32-bit keys: 4-ary, depth 2
+constexpr uint32_t kLaneHeapN = 20;         // busy-end heap slots per lane, 32-bit keys: 4-ary, depth 2
 constexpr uint32_t kLaneHeapW = 10;         // the same region with 64-bit keys
-constexpr uint32_t kLaneFifoWords = 4;      // wake FIFO: 4 app positions per u32 word
+constexpr uint32_t kLaneFifoWords = 2;      // wake FIFO: 4 app positions per u32 word
 constexpr uint32_t kLaneFifo = 4 * kLaneFifoWords;
 constexpr uint64_t kInf = ~0ull;
 constexpr uint32_t kLtBuckets = 128;        // rank-lookup buckets per trace

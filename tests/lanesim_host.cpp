@@ -53,7 +53,7 @@ static void run_case(int n, uint32_t policy, uint32_t cap, const std::vector<uin
     std::vector<int> rk(n);
     for (int e = 0; e < n; e++) rk[e] = e;
     std::stable_sort(rk.begin(), rk.end(), [&](int x, int y) { return s_mem[x] < s_mem[y]; });
-    std::vector<uint8_t> s_por(N + 16, (uint8_t)N), s_lt(kLtBuckets + 16, 0);
+    std::vector<uint8_t> s_por(N + 16, (uint8_t)N), s_lt(kLtBuckets + 16, 0);  // (host: roomier than the kernel slots)
     for (int r = 0; r < n; r++) s_por[r] = (uint8_t)rk[r];
     const uint32_t mn = n ? s_mem[rk[0]] : 0, mx = n ? s_mem[rk[n - 1]] : 0;
     const uint64_t sc = ((uint64_t)kLtBuckets << 32) / ((uint64_t)(mx - mn) + 1);
