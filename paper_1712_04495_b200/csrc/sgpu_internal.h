@@ -42,9 +42,9 @@ struct SimParams {
 
 // Work counter of `stream` on the current device for a launch that will
 // consume `items` counter values (work items + one failing fetch per warp):
-// sets p.work / p.work_base; call work_commit() once the launch succeeded.
-cudaError_t work_reserve(cudaStream_t stream, SimParams& p, int* slot);
-void work_commit(int slot, uint64_t items);
+// sets p.work / p.work_base; call work_abort() if the launch then fails.
+cudaError_t work_reserve(cudaStream_t stream, SimParams& p, uint64_t items, int* slot);
+void work_abort(int slot);
 
 // Shared-memory layout for one warp simulating traces of up to n_pad apps.
 void sim_layout(SimParams& p, bool program_mode, bool f64);

@@ -602,11 +602,11 @@ static cudaError_t launch_lane_t(LaneParams& L, cudaStream_t stream, int* grid_o
     if (grid == 0) grid = 1;
     if (grid_out) *grid_out = (int)grid;
     int slot = 0;
-    err = work_reserve(stream, L.sp, &slot);
+    err = work_reserve(stream, L.sp, groups + grid * wpb, &slot);
     if (err != cudaSuccess) return err;
     kern<<<(unsigned)grid, wpb * 32, smem, stream>>>(L);
     err = cudaGetLastError();
-    if (err == cudaSuccess) work_commit(slot, groups + grid * wpb);
+    if (err != cudaSuccess) work_abort(slot);
     return err;
 }
 

@@ -32,6 +32,7 @@
 //     reorder events of one device (pinned by tests/golden/ref_multidev.npz)
 #include <map>
 #include <mutex>
+#include <thread>
 
 #include "sgpu_tracesim.cuh"
 
@@ -155,23 +156,28 @@ __global__ void SG_SIM_BOUNDS trace_sim_kernel(const SimParams P) {
 
 // ------------------------------------------------------------------ launch
 
-// Group counters for dynamic scheduling, one per (device, stream): launches
+// Work counters for dynamic scheduling, one per (device, stream): launches
 // on one stream are ordered, so the host knows each counter's value at the
-// start of the next launch (it advances by exactly n_groups + warps).
-// Allocated once per device as a pool; streams take slots round robin.
+// start of the next launch (it advances by exactly the work items + one
+// failing fetch per warp).  The base is advanced when the launch is reserved,
+// under the lock, so concurrent callers on one stream stay consistent.  A
+// pool per device; streams take slots round robin (a reused slot's previous
+// stream has been idle for kWorkSlots new streams); the per-thread default
+// stream is keyed by thread as well.
 namespace {
 constexpr int kWorkSlots = 512;
 struct WorkPool {
     unsigned long long* ctr = nullptr;
     uint64_t base[kWorkSlots] = {};
-    std::map<cudaStream_t, int> slot;
+    bool dead[kWorkSlots] = {};
+    std::map<std::pair<cudaStream_t, std::thread::id>, int> slot;
     int next = 0;
 };
 std::mutex g_work_mu;
 std::map<int, WorkPool> g_work;
 }  // namespace
 
-cudaError_t work_reserve(cudaStream_t stream, SimParams& p, int* slot) {
+cudaError_t work_reserve(cudaStream_t stream, SimParams& p, uint64_t items, int* slot) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -182,28 +188,38 @@ cudaError_t work_reserve(cudaStream_t stream, SimParams& p, int* slot) {
         if (e == cudaSuccess) e = cudaMemset(w.ctr, 0, kWorkSlots * sizeof(unsigned long long));
         if (e != cudaSuccess) { w.ctr = nullptr; return e; }
     }
-    auto it = w.slot.find(stream);
+    const auto key = std::make_pair(stream, stream == cudaStreamPerThread ? std::this_thread::get_id()
+                                                                           : std::thread::id());
+    auto it = w.slot.find(key);
     int s;
     if (it == w.slot.end()) {
-        s = w.next;
-        w.next = (w.next + 1) % kWorkSlots;
-        // a reused slot's previous stream has been idle for kWorkSlots new streams
+        int tries = 0;
+        do {
+            s = w.next;
+            w.next = (w.next + 1) % kWorkSlots;
+        } while (w.dead[s] && ++tries < kWorkSlots);
+        if (w.dead[s]) return cudaErrorLaunchOutOfResources;
         for (auto i = w.slot.begin(); i != w.slot.end();) i = i->second == s ? w.slot.erase(i) : std::next(i);
-        w.slot[stream] = s;
+        w.slot[key] = s;
     } else {
         s = it->second;
     }
     p.work = w.ctr + s;
     p.work_base = w.base[s];
+    w.base[s] += items;
     *slot = s;
     return cudaSuccess;
 }
 
-void work_commit(int slot, uint64_t n) {
+void work_abort(int slot) {
+    // the launch did not happen: the slot's counter no longer matches its
+    // base; retire it (its stream gets a fresh slot next time)
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_work_mu);
-    g_work[dev].base[slot] += n;
+    WorkPool& w = g_work[dev];
+    w.dead[slot] = true;
+    for (auto i = w.slot.begin(); i != w.slot.end();) i = i->second == slot ? w.slot.erase(i) : std::next(i);
 }
 
 
@@ -269,11 +285,11 @@ static cudaError_t launch_t(const SimParams& p, cudaStream_t stream, int* grid_o
     if (grid_out) *grid_out = (int)grid;
     SimParams q = p;
     int slot = 0;
-    err = work_reserve(stream, q, &slot);
+    err = work_reserve(stream, q, p.n_traces + grid * wpb, &slot);
     if (err != cudaSuccess) return err;
     kern<<<(unsigned)grid, wpb * 32, smem, stream>>>(q);
     err = cudaGetLastError();
-    if (err == cudaSuccess) work_commit(slot, p.n_traces + grid * wpb);
+    if (err != cudaSuccess) work_abort(slot);
     return err;
 }
 

@@ -356,3 +356,39 @@ def test_work_counters_across_streams_and_sizes(cuda):
             g, e, st = O.simulate_burst(apps, cfg.cap_mib, pol.value)
             np.testing.assert_array_equal(res.ticks("end")[pi].reshape(e.shape), e, err_msg=f"launch {i}")
             np.testing.assert_array_equal(res.stats()[pi].view(np.uint8), st.view(np.uint8))
+
+
+def test_work_counters_concurrent_host_threads(cuda):
+    """Launches from several host threads at once, two of them sharing one
+    stream: the work-counter bases are reserved under a lock, so every
+    launch still covers each of its traces exactly once."""
+    import threading
+    cfg = CONFIGS["C2"]
+    shared = torch.cuda.Stream()
+    streams = [shared, shared, torch.cuda.Stream(), torch.cuda.Stream()]
+    cases = []
+    for i in range(4):
+        apps = as_u32x4(generate(dataclasses.replace(cfg.gen, seed=300 + i), 0, 500 + 37 * i))
+        cases.append((apps, to_dev(apps, cuda)))
+    results = [[] for _ in range(4)]
+
+    def work(k):
+        torch.cuda.set_device(cuda)
+        for _ in range(6):
+            with torch.cuda.stream(streams[k]):
+                r = B.simulate_batch(cases[k][1], ("mmu", "pfifo"), cfg.cap_mib, stream=streams[k])
+            streams[k].synchronize()
+            results[k].append((r.ticks("end"), r.stats()))
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for k in range(4):
+        apps = cases[k][0]
+        for pi, pol in enumerate(("mmu", "pfifo")):
+            _, e, st = O.simulate_burst(apps, cfg.cap_mib, pol)
+            for end, stats in results[k]:
+                np.testing.assert_array_equal(end[pi].reshape(e.shape), e)
+                np.testing.assert_array_equal(stats[pi].view(np.uint8), st.view(np.uint8))
