@@ -569,11 +569,16 @@ static inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
 // Lane path eligibility: T0 ticks mode, no event log, <= 256 apps per trace.
 // By default traces of <= 128 apps take it (measured on one B200: C4, 128
-// apps, 2.07e7 vs 1.41e7 trace-sims/s on the warp kernel); 256-app traces
-// are faster on the warp kernel (C3: 2.7e6 vs 4.5e5) unless `forced`.
+// apps, 4 policies: 4.1e7 vs 1.4e7 trace-sims/s on the warp kernel);
+// 256-app traces are faster on the warp kernel (C3: 3.4e6 vs 4.5e5) unless
+// `forced`.
 bool lane_eligible(const SimParams& p, bool program_mode, bool f64, bool forced) {
-    return !program_mode && !f64 && p.events == nullptr && p.n_pad <= (forced ? 256u : 128u) &&
-           p.npol * p.ndev <= 32;
+    if (program_mode || f64 || p.events != nullptr || p.npol * p.ndev > 32) return false;
+    if (forced) return p.n_pad <= 256u;
+    // one simulation per 128-app trace leaves 7 of 8 lanes of a trace slot
+    // idle: the warp kernel is faster there (C4 shape, 1 policy: 38-59 vs
+    // 98 ms per 1M traces)
+    return p.n_pad <= 64u || (p.n_pad <= 128u && p.npol * p.ndev >= 2);
 }
 
 template <int K>
@@ -616,7 +621,10 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
     const uint32_t N = p.n_pad;
     const uint32_t NW = (N + 63u) / 64u;
     L.lpt = p.npol * p.ndev;
-    L.G = 32u / L.lpt;
+    // at most 8 traces per warp: the shared slot of a trace is what limits
+    // residency, so fewer simulations per trace (npol * ndev < 4) leave lanes
+    // idle rather than multiply the warp's shared memory
+    L.G = min(32u / L.lpt, 8u);
     L.need_cls = 0;
     for (uint32_t i = 0; i < p.npol; i++) {
         const uint32_t pol = (p.policy_list >> (4 * i)) & 0xFu;
