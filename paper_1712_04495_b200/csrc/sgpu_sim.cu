@@ -250,8 +250,8 @@ void sim_layout(SimParams& p, bool program_mode, bool f64) {
     o = align16(o + N * 2u);
     p.off_held = o;
     o = align16(o + (program_mode ? N * 4u : 0u));
-    p.off_pc = o;  // T0: waiting entries per priority (256 x u16)
-    o = align16(o + (program_mode ? 0u : 512u));
+    p.off_pc = o;  // T0: waiting entries per priority (256 x u16) + their queue chunks (256 x u32)
+    o = align16(o + (program_mode ? 0u : 512u + 1024u));
     p.off_bar = o;
     o = align16(o + 16u);
     p.warp_bytes = o;

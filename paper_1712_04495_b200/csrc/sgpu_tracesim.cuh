@@ -197,6 +197,7 @@ struct TraceSim {
     uint16_t* s_st;
     int32_t* s_held;
     uint16_t* s_pc;           // T0 priority kinds: waiting entries per priority
+    uint32_t* s_pcm;          // T0 priority kinds: queue chunks holding waiters of each priority
     // trace / policy
     uint32_t n, cap;
     bool prio_pol, mmu;
@@ -228,6 +229,7 @@ struct TraceSim {
         s_st = reinterpret_cast<uint16_t*>(ws + p.off_st);
         s_held = reinterpret_cast<int32_t*>(ws + p.off_held);
         s_pc = reinterpret_cast<uint16_t*>(ws + p.off_pc);
+        s_pcm = reinterpret_cast<uint32_t*>(ws + p.off_pc + 512);
     }
 
     // harness.py:505-508: a push takes the next counter value
@@ -336,13 +338,17 @@ struct TraceSim {
             }
             uint32_t granted = 0;
             bool stop = false;
-            for (uint32_t a = active; a && !stop; a &= a - 1) {
+            // priority kinds: only the chunks holding waiters of class `top`
+            const uint32_t chunks = (PSET && prio_pol) ? active & s_pcm[top] : active;
+            uint32_t drained_chunks = 0;  // chunks left without a `top` waiter
+            for (uint32_t a = chunks; a && !stop; a &= a - 1) {
                 const uint32_t j = __ffs(a) - 1;
                 uint32_t rem = __shfl_sync(FULL, qm_lane, j);
                 const uint64_t e = s_q[32 * j + lane];
                 const uint32_t mib = (uint32_t)e;
                 const uint32_t app_l = q_app(e);
                 if (prio_pol) rem &= __ballot_sync(FULL, q_prio(e) == top);
+                const uint32_t top_waiting = rem;
                 const bool cand = (rem >> lane) & 1u;
                 uint32_t gm = 0;
                 if (!mmu) {
@@ -378,6 +384,7 @@ struct TraceSim {
                     counter += g;
                     granted += g;
                     if (lane == j) qm_lane &= ~gm;
+                    if ((top_waiting & ~gm) == 0) drained_chunks |= 1u << j;
                 }
             }
             if (granted) {
@@ -390,7 +397,10 @@ struct TraceSim {
                 if (PSET && prio_pol) {  // every grant of the round was of priority `top`
                     const uint32_t left = s_pc[top] - granted;
                     __syncwarp();
-                    if (lane == 0) s_pc[top] = (uint16_t)left;
+                    if (lane == 0) {
+                        s_pc[top] = (uint16_t)left;
+                        s_pcm[top] &= ~drained_chunks;
+                    }
                     __syncwarp();
                     if (left == 0 && lane == (top >> 5)) pm_lane &= ~(1u << (top & 31u));
                 }
@@ -522,7 +532,10 @@ struct TraceSim {
                     if (lane == (qtail >> 5)) qm_lane |= 1u << (qtail & 31);
                     if (PSET && prio_pol) {
                         const uint32_t p = f.w & 0xFFu;
-                        if (lane == 0) s_pc[p] += 1;
+                        if (lane == 0) {
+                            s_pc[p] += 1;
+                            s_pcm[p] |= 1u << (qtail >> 5);
+                        }
                         if (lane == (p >> 5)) pm_lane |= 1u << (p & 31u);
                         __syncwarp();
                     }
@@ -655,7 +668,7 @@ struct TraceSim {
         pm_lane = 0;
         if constexpr (!PROG && PSET) {
             if (prio_pol) {
-                for (uint32_t i = lane; i < 128; i += 32) reinterpret_cast<uint32_t*>(s_pc)[i] = 0;
+                for (uint32_t i = lane; i < 384; i += 32) reinterpret_cast<uint32_t*>(s_pc)[i] = 0;
                 __syncwarp();
             }
         }
