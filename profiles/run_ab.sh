@@ -1,5 +1,5 @@
 # A/B on one GPU: gpu tests on the in-tree build, then the kernel-only bench
-# line of the in-tree build against build_ab/libsgpu_old.so (previous commit),
+# line of the in-tree build against build_ab/libsgpu_old.so (profiles/build_ab_lib.sh),
 # interleaved N_AB times (default 3), with each run's per-step K1 times.
 set -x
 mkdir -p gpurun_out
