@@ -570,7 +570,7 @@ static inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 // Lane path eligibility: T0 ticks mode, no event log, <= 256 apps per trace.
 // By default traces of <= 128 apps take it (measured on one B200: C4, 128
 // apps, 4 policies: 4.1e7 vs 1.4e7 trace-sims/s on the warp kernel);
-// 256-app traces are faster on the warp kernel (C3: 3.4e6 vs 4.5e5) unless
+// 256-app traces are faster on the warp kernel (C3: 3.6e6 vs 1.3e6) unless
 // `forced`.
 bool lane_eligible(const SimParams& p, bool program_mode, bool f64, bool forced) {
     if (program_mode || f64 || p.events != nullptr || p.npol * p.ndev > 32) return false;

@@ -392,3 +392,18 @@ def test_work_counters_concurrent_host_threads(cuda):
             for end, stats in results[k]:
                 np.testing.assert_array_equal(end[pi].reshape(e.shape), e)
                 np.testing.assert_array_equal(stats[pi].view(np.uint8), st.view(np.uint8))
+
+
+@pytest.mark.parametrize("n", [24, 64, 128])
+def test_many_priority_classes(n, cuda):
+    """More distinct priorities per trace than the lane kernel keeps class
+    sets for (8): those traces take the in-kernel exact fallback; priorities
+    up to 255 exercise the warp kernel's full presence set."""
+    rng = np.random.default_rng(n)
+    apps = np.zeros((96, n, 4), np.uint32)
+    apps[..., 0] = rng.integers(0, 200, apps.shape[:2])
+    apps[..., 1] = rng.integers(1, 30_000, apps.shape[:2])
+    apps[..., 2] = rng.integers(1, 100, apps.shape[:2])
+    levels = rng.choice([4, 9, 16, 256], size=96)
+    apps[..., 3] = (rng.integers(0, 1 << 30, apps.shape[:2]) % levels[:, None]).astype(np.uint32)
+    check_against_oracle(apps, (60_000,), cuda)
