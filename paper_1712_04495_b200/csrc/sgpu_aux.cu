@@ -111,10 +111,20 @@ __global__ void __launch_bounds__(256)
 trace_gen_kernel(const sg_gen_params p, uint64_t trace_begin, uint64_t n_traces, uint64_t k0,
                  uint4* __restrict__ out) {
     const uint64_t total = n_traces * p.apps_per_trace;
+    // (trace, app) of element g: 32-bit division while g fits (all BASELINE
+    // shapes; 64-bit division is a long emulated sequence)
+    const bool narrow = total <= 0xFFFFFFFFull;
     for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
          g += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t t = g / p.apps_per_trace;
-        const uint64_t app = g - t * p.apps_per_trace;
+        uint64_t t, app;
+        if (narrow) {
+            const uint32_t t32 = (uint32_t)g / p.apps_per_trace;
+            t = t32;
+            app = (uint32_t)g - t32 * p.apps_per_trace;
+        } else {
+            t = g / p.apps_per_trace;
+            app = g - t * p.apps_per_trace;
+        }
         const uint64_t kt = mix64(k0 ^ (trace_begin + t));
         const uint64_t ha = mix64(kt ^ ((app << 3) | 0));
         const uint64_t hm = mix64(kt ^ ((app << 3) | 1));
@@ -141,7 +151,7 @@ trace_gen_kernel(const sg_gen_params p, uint64_t trace_begin, uint64_t n_traces,
         } else {
             prio = (uint32_t)((hp * p.prio_levels) >> 32);
         }
-        const uint32_t dev = (uint32_t)(app % p.ndev);
+        const uint32_t dev = (uint32_t)app % p.ndev;
         out[g] = make_uint4(arrival, uniform_u32(hm, p.mem_lo, p.mem_hi),
                             uniform_u32(hb, p.busy_lo, p.busy_hi), prio | (dev << 8));
     }
