@@ -116,7 +116,7 @@ struct LaneSim {
     uint32_t maxh, grants, pops;
     // incremental grant_waiters state (fit-table path): one select_grants
     // step per loop iteration while `gs` (harness.py:545-558)
-    bool gs;
+    bool gs, ginit;          // granting / the next step starts a round
     uint32_t clsmask;        // priority classes with waiting entries (bit c: class c, top = 0)
     uint32_t gc, gbud, gb0, gg;
     uint64_t gcand[NW], grem[NW];  // unscanned candidates / waiting members of the round's class
@@ -267,6 +267,12 @@ struct LaneSim {
         gg = 0;
     }
     SG_HD void grant_step() {
+        // a round starts inside its first step: one code site for init_round
+        // whether the round follows a free or a drained class
+        if (ginit) {
+            ginit = false;
+            init_round();
+        }
         uint64_t t[NW];
         fit_set(fit_rank(gbud), t);
         if constexpr (NW == 1) {
@@ -334,8 +340,8 @@ struct LaneSim {
         // (harness.py:547-550); otherwise the next round is empty
         if (prio_pol && gg && drained) {
             clsmask &= ~(1u << gc);
-            if (clsmask) init_round();
-            else gs = false;
+            gs = clsmask != 0;  // the next class has waiters: its round starts next step
+            ginit = gs;
         } else {
             gs = false;
         }
@@ -344,7 +350,8 @@ struct LaneSim {
         bool any = false;
 #pragma unroll
         for (uint32_t w = 0; w < NW; w++) any = any || mask[w] != 0;
-        if (any) init_round();
+        gs = any;
+        ginit = any;
     }
 
     // longer traces: scan the candidates in queue order
@@ -463,7 +470,7 @@ struct LaneSim {
         I = 0;
         busy_level = holders = 0;
         maxh = grants = pops = 0;
-        gs = false;
+        gs = ginit = false;
         clsmask = 0;
         // initial pops at t = 0: apps without a cpu step run inline, in index
         // order, each in its own virtual counter block
