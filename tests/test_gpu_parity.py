@@ -407,3 +407,18 @@ def test_many_priority_classes(n, cuda):
     levels = rng.choice([4, 9, 16, 256], size=96)
     apps[..., 3] = (rng.integers(0, 1 << 30, apps.shape[:2]) % levels[:, None]).astype(np.uint32)
     check_against_oracle(apps, (60_000,), cuda)
+
+
+@pytest.mark.parametrize("pols", [("mmu",), ("fifo", "pfifo"), ("mmu", "pfifo", "pmmu")])
+def test_host_pipeline_policy_subsets(pols, cuda):
+    """Host-buffer pipeline with 1-3 policies (grants then all derived on the
+    host, or copied for npol // 4 of them) against the device path."""
+    cfg = CONFIGS["C2"]
+    apps = as_u32x4(generate(dataclasses.replace(cfg.gen, seed=41), 0, 3000))
+    dres = run(apps, pols, cfg.cap_mib, cuda)
+    pin = B.pinned_apps(*apps.shape[:2])
+    pin[...] = apps
+    host = B.simulate_batch_host(pin, pols, cfg.cap_mib, chunk_traces=700)
+    np.testing.assert_array_equal(host.grant, dres.ticks("grant"))
+    np.testing.assert_array_equal(host.end, dres.ticks("end"))
+    np.testing.assert_array_equal(host.stats.view(np.uint8), dres.stats().view(np.uint8))
