@@ -215,16 +215,16 @@ class HostBuffers:
 
     def d2h_bytes(self) -> int:
         """Bytes the host pipeline copies device -> host per call.  With both
-        tick arrays requested, the grants of the first npol // 4 policies are
-        copied and the others derived on the host from the end ticks and the
-        inputs (grant = end - busy), crossing no bus (sg_simulate_batch_host,
-        csrc/sgpu_abi.cu; SGPU_GRANT_DMA overrides the split there and here)."""
+        tick arrays requested, the grants are derived on the host from the end
+        ticks and the inputs (grant = end - busy) and cross no bus
+        (sg_simulate_batch_host, csrc/sgpu_abi.cu; SGPU_GRANT_DMA=k copies the
+        first k policies' grants instead, there and here)."""
         n = sum(a.nbytes for a in (self.end, self.stats, self.mem_pct, self.dev_pct) if a is not None)
         if self.grant is not None:
             npol = self.grant.shape[0]
             n_dma = npol
             if self.end is not None:
-                n_dma = npol // 4
+                n_dma = 0
                 env = os.environ.get("SGPU_GRANT_DMA")
                 if env is not None and int(env) >= 0:
                     n_dma = min(int(env), npol)

@@ -259,9 +259,11 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
     const bool host_grant = out->grant != nullptr && out->end != nullptr;
     // With both tick arrays requested, the grants of policies [0, n_dma) are
     // copied from the device and those of [n_dma, npol) derived by host
-    // threads: the split balances PCIe time against host-memory traffic
-    // ("End to end").  SGPU_GRANT_DMA overrides.
-    uint32_t n_dma = host_grant ? s.npol / 4 : s.npol;
+    // threads.  Deriving all of them measured best on two of three boxes
+    // (36.6-37.2 vs 38.6 ms per C2 step; the third favoured copying one
+    // policy): the pipeline is host-memory bound ("End to end").
+    // SGPU_GRANT_DMA overrides.
+    uint32_t n_dma = host_grant ? 0u : s.npol;
     if (const char* ev = getenv("SGPU_GRANT_DMA")) {
         const int v = atoi(ev);
         if (host_grant && v >= 0) n_dma = (uint32_t)v < s.npol ? (uint32_t)v : s.npol;
