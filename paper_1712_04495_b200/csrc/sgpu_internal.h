@@ -34,7 +34,8 @@ struct SimParams {
     uint32_t* event_counts;
     // per-warp shared-memory layout (bytes)
     uint32_t off_app, off_sub, off_idx, off_key, off_kc, off_q, off_grant, off_end, off_st, off_held,
-        off_pc, off_bar, warp_bytes;
+        off_pc, off_steps, off_bar, warp_bytes;
+    uint32_t steps_cap;             // program mode: steps of one trace kept in shared memory
     // dynamic scheduling: work item = atomicAdd(work, 1) - work_base
     unsigned long long* work;
     uint64_t work_base;

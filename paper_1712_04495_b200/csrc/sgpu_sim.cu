@@ -53,7 +53,6 @@ __global__ void SG_SIM_BOUNDS trace_sim_kernel(const SimParams P) {
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
-    const uint32_t wpb = blockDim.x >> 5;
     uint8_t* ws = smem + (size_t)warp * P.warp_bytes;
     uint64_t* bar = reinterpret_cast<uint64_t*>(ws + P.off_bar);
     const uint32_t buf_bytes = P.n_pad * 16u;
@@ -106,6 +105,7 @@ __global__ void SG_SIM_BOUNDS trace_sim_kernel(const SimParams P) {
         uint32_t na;
         trace_range(t, a0, na);
         const uint32_t b = PROG ? 0u : (iter & 1u);
+        bool steps_cached = false;
         if constexpr (!PROG) {
             mbar_wait(&bar[b], (iter >> 1) & 1u);
             __syncwarp();
@@ -113,10 +113,20 @@ __global__ void SG_SIM_BOUNDS trace_sim_kernel(const SimParams P) {
         } else {
             uint4* dst = reinterpret_cast<uint4*>(ws + P.off_app);
             const uint32_t s0 = P.step_offsets[0];
+            // the trace's steps go to shared memory when they fit: the step
+            // fetch is on every event's critical path
+            const uint32_t t0s = P.step_offsets[a0] - s0, t1s = P.step_offsets[a0 + na] - s0;
+            steps_cached = t1s - t0s <= P.steps_cap;
+            const uint32_t rel = steps_cached ? t0s : 0u;
             for (uint32_t i = lane; i < na; i += 32) {
                 const uint32_t sb = P.step_offsets[a0 + i] - s0;
                 const uint32_t se = P.step_offsets[a0 + i + 1] - s0;
-                dst[i] = make_uint4(sb, se - sb, 0u, P.apps[a0 + i].attr);
+                dst[i] = make_uint4(sb - rel, se - sb, 0u, P.apps[a0 + i].attr);
+            }
+            if (steps_cached) {
+                uint4* s_steps = reinterpret_cast<uint4*>(ws + P.off_steps);
+                for (uint32_t j = lane; j < t1s - t0s; j += 32)
+                    s_steps[j] = __ldg(reinterpret_cast<const uint4*>(P.steps) + t0s + j);
             }
             __syncwarp();
         }
@@ -141,6 +151,7 @@ __global__ void SG_SIM_BOUNDS trace_sim_kernel(const SimParams P) {
             }
             for (uint32_t p = 0; p < P.npol; p++) {
                 TraceSim<TM, K, PROG> sim(P, lane, ws, sub);
+                if (PROG && steps_cached) sim.s_steps = reinterpret_cast<const uint4*>(ws + P.off_steps);
                 const uint64_t slot = (uint64_t)p * P.n_traces + t;
                 sg_event* evs = P.events ? P.events + slot * P.ev_cap : nullptr;
                 sim.run(nd, (P.policy_list >> (4 * p)) & 0xFu, cap_d, evs);
@@ -252,6 +263,9 @@ void sim_layout(SimParams& p, bool program_mode, bool f64) {
     o = align16(o + (program_mode ? N * 4u : 0u));
     p.off_pc = o;  // T0: waiting entries per priority (256 x u16) + their queue chunks (256 x u32)
     o = align16(o + (program_mode ? 0u : 512u + 1024u));
+    p.off_steps = o;  // program mode: the trace's steps, when they fit (8 per app slot)
+    p.steps_cap = program_mode ? 8u * N : 0u;
+    o = align16(o + p.steps_cap * 16u);
     p.off_bar = o;
     o = align16(o + 16u);
     p.warp_bytes = o;

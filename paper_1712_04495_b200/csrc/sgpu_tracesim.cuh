@@ -198,6 +198,7 @@ struct TraceSim {
     int32_t* s_held;
     uint16_t* s_pc;           // T0 priority kinds: waiting entries per priority
     uint32_t* s_pcm;          // T0 priority kinds: queue chunks holding waiters of each priority
+    const uint4* s_steps = nullptr;  // program mode: the trace's steps in shared memory (else global)
     // trace / policy
     uint32_t n, cap;
     bool prio_pol, mmu;
@@ -584,7 +585,7 @@ struct TraceSim {
                 emit(now, app, SG_EV_END, 0);
                 break;
             }
-            const uint4 stp = __ldg(reinterpret_cast<const uint4*>(P.steps) + f.x + pc);
+            const uint4 stp = s_steps ? s_steps[f.x + pc] : __ldg(reinterpret_cast<const uint4*>(P.steps) + f.x + pc);
             const uint32_t op = stp.x, mib = stp.y;
             const uint64_t dur = ((uint64_t)stp.w << 32) | stp.z;
             if (op == SG_OP_CPU || op == SG_OP_BUSY) {  // harness.py:514-520
@@ -644,7 +645,7 @@ struct TraceSim {
         const uint4 f = s_app[i];
         if constexpr (PROG) {
             if (f.y == 0) return false;
-            const uint4 st = __ldg(reinterpret_cast<const uint4*>(P.steps) + f.x);
+            const uint4 st = s_steps ? s_steps[f.x] : __ldg(reinterpret_cast<const uint4*>(P.steps) + f.x);
             dur = ((uint64_t)st.w << 32) | st.z;
             return st.x == SG_OP_CPU;
         } else {
