@@ -29,12 +29,11 @@ import json
 import math
 import struct
 from dataclasses import dataclass, field
-from fractions import Fraction
 
 import numpy as np
 
 from . import _lib
-from .batch import STEP_DTYPE, simulate_batch
+from .batch import STATS_DTYPE, STATS_F64_DTYPE, STEP_DTYPE, simulate_batch
 from .device import MIB, DeviceSpec, parse_device_config
 from .errors import SchemaError, SgpuUnavailable
 from .policy import PolicyKind
@@ -198,11 +197,12 @@ def _tick_grid(durations: list[float], cap_mib: int):
     memory integral < 2^53).  None => use float64 mode."""
     if not durations:
         return 10
-    fr = [Fraction(d) for d in durations]
-    e = max(f.denominator.bit_length() - 1 for f in fr)
+    # a finite double is num / 2^k exactly (float.as_integer_ratio)
+    fr = [float(d).as_integer_ratio() for d in durations]
+    e = max(den.bit_length() - 1 for _, den in fr)
     if e > 62:
         return None
-    total = sum(int(f * (1 << e)) for f in fr)
+    total = sum(num << (e - (den.bit_length() - 1)) for num, den in fr)
     if total >= 0xFFFFFFFE or cap_mib * total >= (1 << 53):
         return None
     return e
@@ -237,7 +237,8 @@ def encode_spec(spec: WorkloadSpec) -> EncodedTrace:
         for op, arg in flat:
             if op in (_lib.OP_CPU, _lib.OP_BUSY):
                 if mode == _lib.TIME_TICKS:
-                    dur = int(Fraction(arg) * (1 << e))
+                    num, den = float(arg).as_integer_ratio()
+                    dur = num << (e - (den.bit_length() - 1))
                 else:
                     dur = struct.unpack("<Q", struct.pack("<d", float(arg)))[0]
                 rows.append((op, 0, dur))
@@ -273,14 +274,19 @@ def run_encoded(enc: EncodedTrace, policy) -> dict:
     res = simulate_batch(apps_t, (policy,), enc.cap_mib, steps=steps_t, step_offsets=offs_t,
                          time_mode=enc.time_mode, tick_log2=enc.tick_log2,
                          events_per_trace=ev_cap)
-    stats = res.stats()[0, 0, 0]
-    count = int(res.event_counts[0, 0].item())
-    ev = res.events[0, 0, :min(count, ev_cap)].cpu().numpy().copy().view(
+    # one device->host round trip for every output of the trace
+    pct = torch.stack([res.mem_pct[0, 0, 0], res.dev_pct[0, 0, 0]])
+    host = [t.to("cpu", non_blocking=True) for t in (res.stats_raw, res.event_counts[0, 0], res.events[0, 0], pct)]
+    torch.cuda.current_stream(dev).synchronize()
+    raw = host[0].numpy()
+    dt = STATS_F64_DTYPE if res.time_mode == _lib.TIME_F64 else STATS_DTYPE
+    stats = np.ascontiguousarray(raw).view(dt).reshape(raw.shape[:3])[0, 0, 0]
+    count = int(host[1])
+    ev = host[2][:min(count, ev_cap)].numpy().copy().view(
         np.dtype([("t", "<u8"), ("app", "<u2"), ("kind", "u1"), ("dev", "u1"),
                   ("mib", "<u4")])).reshape(-1)
     return {"stats": stats, "events": ev, "count": count, "ev_cap": ev_cap,
-            "mem_pct": float(res.mem_pct[0, 0, 0].item()),
-            "dev_pct": float(res.dev_pct[0, 0, 0].item())}
+            "mem_pct": float(host[3][0]), "dev_pct": float(host[3][1])}
 
 
 def _time_of(enc: EncodedTrace, raw: int) -> float:
