@@ -49,10 +49,12 @@ namespace sg {
 constexpr uint32_t kLaneClassMasks = 64;    // class masks per warp, split over its trace slots
 constexpr int kLaneWarpsPerBlock = 2;      // two warps share a block's 1 KB smem reservation
 // Resident two-warp blocks per SM the register allocation is sized for.
-// Nine (18 warps) caps registers at 96 per thread: a win for 128-app traces
-// (C4: 3.46e7 -> 4.13e7 trace-sims/s), a small loss at 64 apps (C2: 18.13
-// -> 18.30 ms), where eight blocks keep 118 registers (one-box A/B).
-template <int K> struct LaneMinBlocks { static constexpr int v = K == 2 ? 8 : 9; };
+// Nine (18 warps) caps registers at 96 per thread: a small loss at 64 apps
+// (C2: 18.13 -> 18.30 ms), where eight blocks keep ~114 registers.  At 128
+// apps shared memory allows five blocks, so registers are left free up to
+// that (C4: 3.96e7 -> 4.03e7 trace-sims/s against the 96-register build;
+// one-box A/Bs).
+template <int K> struct LaneMinBlocks { static constexpr int v = K == 2 ? 8 : K == 4 ? 5 : 9; };
 struct LaneParams {
     SimParams sp;          // inputs/outputs + the fallback TraceSim layout (off_* relative to the warp region)
     uint32_t G;            // traces per warp (32 / lpt)
