@@ -10,7 +10,9 @@ on 8 simulated devices), where the CPU oracle cannot check every trace:
 * size-independent invariants hold on every record: every app is granted
   and ends (requests fit the device), grants per device = apps on that
   device, busy union <= makespan, memory integral <= capacity x makespan,
-  makespan >= the device's last arrival.
+  makespan >= the device's last arrival;
+* and C2 in full: every one of its 1,048,576 traces x 4 policies against
+  the oracle.
 """
 
 import numpy as np
@@ -80,3 +82,22 @@ def test_full_size(cname, cuda, monkeypatch):
         assert (r["mem_integral"] <= cap[None, :] * r["makespan"].astype(np.uint64)).all()
         assert (r["makespan"].astype(np.int64) >= last_arr).all()
     assert int((lane.grant == -1).sum()) == 0 and int((lane.end == -1).sum()) == 0
+
+
+def test_c2_every_trace_against_oracle(cuda, monkeypatch):
+    """C2 at its full BASELINE size: all 1,048,576 traces x 4 policies of the
+    default engine against the oracle (C restatement, all host cores),
+    every grant / end tick and every statistics record."""
+    cfg = CONFIGS["C2"]
+    n = cfg.n_traces
+    monkeypatch.delenv("SGPU_K1", raising=False)
+    apps_t = B.generate_traces(cfg.gen, 0, n, device=0)
+    res = B.simulate_batch(apps_t, cfg.policies, cfg.cap_mib)
+    torch.cuda.synchronize()
+    apps = apps_t.cpu().numpy().view(np.uint32)
+    grant, end, st = res.ticks("grant"), res.ticks("end"), res.stats()
+    for pi, pol in enumerate(res.policies):
+        g, e, s = O.simulate_burst(apps, cfg.cap_mib, pol.value)
+        assert np.array_equal(grant[pi].reshape(g.shape), g), pol
+        assert np.array_equal(end[pi].reshape(e.shape), e), pol
+        assert np.array_equal(st[pi].view(np.uint8), s.view(np.uint8)), pol
