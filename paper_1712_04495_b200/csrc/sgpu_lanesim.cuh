@@ -134,7 +134,8 @@ struct LaneSim {
     }
 
     // ------------------------------------------------- busy-end heap
-    // 4-ary min-heap of at most 21 keys (root + 4 + 16): every sift is at
+    // 4-ary min-heap of at most kLaneHeapN = 20 keys (depth 2: root + 4 + 16
+    // slots): every sift is at
     // most two levels, unrolled and predicated, and the four child loads of a
     // level are independent
     SG_HD void push(uint32_t t, uint32_t q) {
