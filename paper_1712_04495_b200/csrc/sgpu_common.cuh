@@ -11,6 +11,25 @@ namespace sg {
 
 constexpr uint32_t FULL = 0xFFFFFFFFu;
 
+// Dynamic work distribution (K1 kernels): ctr[0] hands out work items one
+// warp at a time; ctr[1] counts warps that have made their failing fetch.
+// The last warp of the launch resets both, so every launch - and every
+// replay of a captured CUDA graph - starts from zero.  Warp-collective.
+__device__ __forceinline__ uint64_t work_fetch(unsigned long long* ctr, uint32_t lane) {
+    unsigned long long v = 0;
+    if (lane == 0) v = atomicAdd(ctr, 1ull);
+    return (uint64_t)__shfl_sync(FULL, v, 0);
+}
+__device__ __forceinline__ void work_done(unsigned long long* ctr, uint32_t lane) {
+    if (lane == 0) {
+        const unsigned long long warps = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+        if (atomicAdd(ctr + 1, 1ull) == warps - 1) {  // no fetch of this launch is left
+            atomicExch(ctr, 0ull);
+            atomicExch(ctr + 1, 0ull);
+        }
+    }
+}
+
 __device__ __forceinline__ uint32_t lane_id() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%laneid;" : "=r"(r));

@@ -36,16 +36,13 @@ struct SimParams {
     uint32_t off_app, off_sub, off_idx, off_key, off_kc, off_q, off_grant, off_end, off_st, off_held,
         off_pc, off_steps, off_bar, warp_bytes;
     uint32_t steps_cap;             // program mode: steps of one trace kept in shared memory
-    // dynamic scheduling: work item = atomicAdd(work, 1) - work_base
+    // dynamic scheduling: work[0] hands out work items, work[1] counts the
+    // warps that are done; the last warp of a launch resets both
     unsigned long long* work;
-    uint64_t work_base;
 };
 
-// Work counter of `stream` on the current device for a launch that will
-// consume `items` counter values (work items + one failing fetch per warp):
-// sets p.work / p.work_base; call work_abort() if the launch then fails.
-cudaError_t work_reserve(cudaStream_t stream, SimParams& p, uint64_t items, int* slot);
-void work_abort(int slot);
+// The work counters of `stream` on the current device (sets p.work).
+cudaError_t work_counters(cudaStream_t stream, SimParams& p);
 
 // Shared-memory layout for one warp simulating traces of up to n_pad apps.
 void sim_layout(SimParams& p, bool program_mode, bool f64);

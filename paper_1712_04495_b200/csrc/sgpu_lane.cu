@@ -480,13 +480,8 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, LaneMinBlocks<K>::v) 
     const uint32_t ndev = P.ndev;
     // groups are handed out by one atomic counter (each warp takes the next
     // group when it finishes one): no tail of warps with more groups than
-    // others.  Every warp makes exactly one fetch past the end, so a launch
-    // advances the counter by n_groups + warps (tracked on the host).
-    auto fetch = [&]() -> uint64_t {
-        unsigned long long v = 0;
-        if (lane == 0) v = atomicAdd(P.work, 1ull);
-        return (uint64_t)__shfl_sync(FULL, v, 0) - P.work_base;
-    };
+    // others (sgpu_common.cuh work_fetch / work_done)
+    auto fetch = [&]() -> uint64_t { return work_fetch(P.work, lane); };
 
     // lane -> (slot, device, policy slot)
     const uint32_t g = lane / L.lpt;
@@ -564,6 +559,7 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, LaneMinBlocks<K>::v) 
         __syncwarp();
         grp = next;
     }
+    work_done(P.work, lane);
 }
 
 static inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
@@ -608,13 +604,10 @@ static cudaError_t launch_lane_t(LaneParams& L, cudaStream_t stream, int* grid_o
     if (need < grid) grid = need;
     if (grid == 0) grid = 1;
     if (grid_out) *grid_out = (int)grid;
-    int slot = 0;
-    err = work_reserve(stream, L.sp, groups + grid * wpb, &slot);
+    err = work_counters(stream, L.sp);
     if (err != cudaSuccess) return err;
     kern<<<(unsigned)grid, wpb * 32, smem, stream>>>(L);
-    err = cudaGetLastError();
-    if (err != cudaSuccess) work_abort(slot);
-    return err;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_out) {

@@ -59,11 +59,7 @@ __global__ void SG_SIM_BOUNDS trace_sim_kernel(const SimParams P) {
 
     // traces are handed out by one atomic counter (sgpu_internal.h
     // work_reserve); each warp makes exactly one fetch past the end
-    auto fetch = [&]() -> uint64_t {
-        unsigned long long v = 0;
-        if (lane == 0) v = atomicAdd(P.work, 1ull);
-        return (uint64_t)__shfl_sync(FULL, v, 0) - P.work_base;
-    };
+    auto fetch = [&]() -> uint64_t { return work_fetch(P.work, lane); };
 
     auto trace_range = [&](uint64_t t, uint64_t& a0, uint32_t& na) {
         if (P.trace_offsets) {
@@ -163,24 +159,21 @@ __global__ void SG_SIM_BOUNDS trace_sim_kernel(const SimParams P) {
         t = next;
         iter++;
     }
+    work_done(P.work, lane);
 }
 
 // ------------------------------------------------------------------ launch
 
-// Work counters for dynamic scheduling, one per (device, stream): launches
-// on one stream are ordered, so the host knows each counter's value at the
-// start of the next launch (it advances by exactly the work items + one
-// failing fetch per warp).  The base is advanced when the launch is reserved,
-// under the lock, so concurrent callers on one stream stay consistent.  A
-// pool per device; streams take slots round robin (a reused slot's previous
-// stream has been idle for kWorkSlots new streams); the per-thread default
-// stream is keyed by thread as well.
+// Work counters for dynamic scheduling, one pair per (device, stream): the
+// kernels reset them at the end of every launch (sgpu_common.cuh
+// work_done), and launches on one stream are ordered, so a stream's pair is
+// always zero when its next launch starts.  A pool per device; streams take
+// slots round robin (a reused slot's previous stream has been idle for
+// kWorkSlots new streams); the per-thread default stream is keyed by thread.
 namespace {
 constexpr int kWorkSlots = 512;
 struct WorkPool {
     unsigned long long* ctr = nullptr;
-    uint64_t base[kWorkSlots] = {};
-    bool dead[kWorkSlots] = {};
     std::map<std::pair<cudaStream_t, std::thread::id>, int> slot;
     int next = 0;
 };
@@ -188,15 +181,15 @@ std::mutex g_work_mu;
 std::map<int, WorkPool> g_work;
 }  // namespace
 
-cudaError_t work_reserve(cudaStream_t stream, SimParams& p, uint64_t items, int* slot) {
+cudaError_t work_counters(cudaStream_t stream, SimParams& p) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lk(g_work_mu);
     WorkPool& w = g_work[dev];
     if (!w.ctr) {
-        e = cudaMalloc(&w.ctr, kWorkSlots * sizeof(unsigned long long));
-        if (e == cudaSuccess) e = cudaMemset(w.ctr, 0, kWorkSlots * sizeof(unsigned long long));
+        e = cudaMalloc(&w.ctr, 2 * kWorkSlots * sizeof(unsigned long long));
+        if (e == cudaSuccess) e = cudaMemset(w.ctr, 0, 2 * kWorkSlots * sizeof(unsigned long long));
         if (e != cudaSuccess) { w.ctr = nullptr; return e; }
     }
     const auto key = std::make_pair(stream, stream == cudaStreamPerThread ? std::this_thread::get_id()
@@ -204,35 +197,16 @@ cudaError_t work_reserve(cudaStream_t stream, SimParams& p, uint64_t items, int*
     auto it = w.slot.find(key);
     int s;
     if (it == w.slot.end()) {
-        int tries = 0;
-        do {
-            s = w.next;
-            w.next = (w.next + 1) % kWorkSlots;
-        } while (w.dead[s] && ++tries < kWorkSlots);
-        if (w.dead[s]) return cudaErrorLaunchOutOfResources;
+        s = w.next;
+        w.next = (w.next + 1) % kWorkSlots;
         for (auto i = w.slot.begin(); i != w.slot.end();) i = i->second == s ? w.slot.erase(i) : std::next(i);
         w.slot[key] = s;
     } else {
         s = it->second;
     }
-    p.work = w.ctr + s;
-    p.work_base = w.base[s];
-    w.base[s] += items;
-    *slot = s;
+    p.work = w.ctr + 2 * s;
     return cudaSuccess;
 }
-
-void work_abort(int slot) {
-    // the launch did not happen: the slot's counter no longer matches its
-    // base; retire it (its stream gets a fresh slot next time)
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lk(g_work_mu);
-    WorkPool& w = g_work[dev];
-    w.dead[slot] = true;
-    for (auto i = w.slot.begin(); i != w.slot.end();) i = i->second == slot ? w.slot.erase(i) : std::next(i);
-}
-
 
 static inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
@@ -298,13 +272,10 @@ static cudaError_t launch_t(const SimParams& p, cudaStream_t stream, int* grid_o
     if (grid == 0) grid = 1;
     if (grid_out) *grid_out = (int)grid;
     SimParams q = p;
-    int slot = 0;
-    err = work_reserve(stream, q, p.n_traces + grid * wpb, &slot);
+    err = work_counters(stream, q);
     if (err != cudaSuccess) return err;
     kern<<<(unsigned)grid, wpb * 32, smem, stream>>>(q);
-    err = cudaGetLastError();
-    if (err != cudaSuccess) work_abort(slot);
-    return err;
+    return cudaGetLastError();
 }
 
 template <class TM, bool PROG>

@@ -422,3 +422,29 @@ def test_host_pipeline_policy_subsets(pols, cuda):
     np.testing.assert_array_equal(host.grant, dres.ticks("grant"))
     np.testing.assert_array_equal(host.end, dres.ticks("end"))
     np.testing.assert_array_equal(host.stats.view(np.uint8), dres.stats().view(np.uint8))
+
+
+def test_cuda_graph_replay(cuda):
+    """K1 launched inside a captured CUDA graph and replayed on new inputs:
+    the work counters reset at the end of every launch, so each replay
+    covers every trace again."""
+    cfg = CONFIGS["C2"]
+    n = 5000
+    apps_t = B.generate_traces(cfg.gen, 0, n, device=0)
+    B.simulate_batch(apps_t, POLICIES, cfg.cap_mib)  # warm-up: kernel attributes, counter pool
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        res = B.simulate_batch(apps_t, POLICIES, cfg.cap_mib, stream=s)
+    for k in range(3):
+        fresh = B.generate_traces(dataclasses.replace(cfg.gen, seed=900 + k), 0, n, device=0)
+        apps_t.copy_(fresh)
+        g.replay()
+        torch.cuda.synchronize()
+        apps = apps_t.cpu().numpy().view(np.uint32)
+        st = res.stats()
+        for pi, pol in enumerate(res.policies):
+            gr, e, sref = O.simulate_burst(apps, cfg.cap_mib, pol.value)
+            np.testing.assert_array_equal(res.ticks("end")[pi].reshape(e.shape), e, err_msg=f"replay {k}")
+            np.testing.assert_array_equal(st[pi].view(np.uint8), sref.view(np.uint8))
