@@ -338,10 +338,10 @@ def test_host_pipeline_cases(case, cuda):
 
 
 def test_work_counters_across_streams_and_sizes(cuda):
-    """Dynamic scheduling hands out work items from one counter per stream
-    whose base the host tracks launch by launch: many launches of varying
-    size, interleaved over several streams (and both engines, via the
-    fixture), must each cover every trace exactly once."""
+    """Dynamic scheduling hands out work items from one counter per stream,
+    reset by the last warp of each launch: many launches of varying size,
+    interleaved over several streams (and both engines, via the fixture),
+    must each cover every trace exactly once."""
     cfg = CONFIGS["C2"]
     streams = [torch.cuda.Stream() for _ in range(3)]
     rng = np.random.default_rng(11)
@@ -360,8 +360,8 @@ def test_work_counters_across_streams_and_sizes(cuda):
 
 def test_work_counters_concurrent_host_threads(cuda):
     """Launches from several host threads at once, two of them sharing one
-    stream: the work-counter bases are reserved under a lock, so every
-    launch still covers each of its traces exactly once."""
+    stream (whose launches the stream orders, so its counter is back at zero
+    when each starts): every launch covers each of its traces exactly once."""
     import threading
     cfg = CONFIGS["C2"]
     shared = torch.cuda.Stream()
