@@ -6,8 +6,9 @@
 
 A "step" simulates the configuration's whole per-GPU trace batch (default C2:
 1M traces x 64 apps) under every policy of the configuration (C2: all four),
-i.e. one launch of K1 trace_sim + one of K2 stats_reduce (+ the cross-GPU
-aggregate all-reduce for N > 1).  The unit is one trace simulated under one
+i.e. one K1 trace_sim (on the lane engine: the main launch + the 64-bit-key
+retry launch, which finds nothing to do on C2) + one K2 stats_reduce (+ the
+cross-GPU aggregate all-reduce for N > 1).  The unit is one trace simulated under one
 policy.  Scaling is weak: every rank simulates its own contiguous trace-id
 shard of the configured size, generated on its GPU before timing.
 
@@ -361,6 +362,8 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     launches = 0
+    # K1 (lane engine: main pass + 64-bit-key retry pass) + K2 stats_reduce
+    k1_launches = B.k1_launches(cfg.gen.apps_per_trace, npol, cfg.ndev)
 
     def step(i=None):
         nonlocal launches
@@ -370,7 +373,7 @@ def main():
         if i is not None:
             ev[i][1].record(stream)
         agg = B.reduce_stats(res.stats_raw, stream=stream)
-        launches += 2
+        launches += k1_launches + 1
         if ws > 1:
             agg = PAR.allreduce_aggregate(agg)
         return res, agg

@@ -20,12 +20,15 @@ __device__ __forceinline__ uint64_t work_fetch(unsigned long long* ctr, uint32_t
     if (lane == 0) v = atomicAdd(ctr, 1ull);
     return (uint64_t)__shfl_sync(FULL, v, 0);
 }
-__device__ __forceinline__ void work_done(unsigned long long* ctr, uint32_t lane) {
+// reset_list: also reset the deferred-list count ctr[2] (every warp of this
+// launch read it before it counted itself done)
+__device__ __forceinline__ void work_done(unsigned long long* ctr, uint32_t lane, bool reset_list = false) {
     if (lane == 0) {
         const unsigned long long warps = (unsigned long long)gridDim.x * (blockDim.x >> 5);
         if (atomicAdd(ctr + 1, 1ull) == warps - 1) {  // no fetch of this launch is left
             atomicExch(ctr, 0ull);
             atomicExch(ctr + 1, 0ull);
+            if (reset_list) atomicExch(ctr + 2, 0ull);
         }
     }
 }

@@ -37,12 +37,20 @@ struct SimParams {
         off_pc, off_steps, off_bar, warp_bytes;
     uint32_t steps_cap;             // program mode: steps of one trace kept in shared memory
     // dynamic scheduling: work[0] hands out work items, work[1] counts the
-    // warps that are done; the last warp of a launch resets both
+    // warps that are done; the last warp of a launch resets both.  work[2]
+    // counts the entries of `retry` (lane kernel: traces deferred to the
+    // 64-bit-key pass), reset by the last warp of that pass.
     unsigned long long* work;
+    uint32_t* retry;
 };
 
-// The work counters of `stream` on the current device (sets p.work).
-cudaError_t work_counters(cudaStream_t stream, SimParams& p);
+// The work counters of `stream` on the current device (sets p.work) and,
+// when retry_cap > 0, a deferred-trace list of that many entries that stays
+// valid for work on `stream` (sets p.retry).  Inside a stream capture the list
+// is a graph allocation (*retry_owned = true): the caller frees it on the
+// stream after its last use.
+cudaError_t work_counters(cudaStream_t stream, SimParams& p, uint64_t retry_cap = 0,
+                          bool* retry_owned = nullptr);
 
 // Shared-memory layout for one warp simulating traces of up to n_pad apps.
 void sim_layout(SimParams& p, bool program_mode, bool f64);

@@ -37,11 +37,16 @@
 //    (bucket lookup), and the next first fit is the lowest bit of
 //    mask & class & T above the last grant.
 //
-// Lanes that cannot take this path (heap or FIFO capacity exceeded, too many
-// priority classes, or a trace whose times could leave the 32-bit tick
-// range) are re-simulated by the whole warp with the exact warp-per-trace
-// TraceSim (sgpu_tracesim.cuh) right after, in the same kernel: no host
-// round trip, no extra buffers.
+// 32-bit event keys when every time of the group's traces fits, else 64-bit
+// keys, whose heap holds kLaneHeapW events in the same 2.5 KB region.  Two
+// launches per batch: a trace whose 64-bit-key lanes overflow that heap is
+// appended to a deferred list and re-simulated by the second (retry) pass
+// with a kLaneHeapN-event 64-bit heap (a 5 KB region, lower occupancy); on
+// C2's 32-bit-key traces that pass finds nothing to do.  Lanes that still
+// cannot take the lane path (heap or FIFO capacity exceeded, too many
+// priority classes, times near the 32-bit tick range) are re-simulated by
+// the whole warp with the exact warp-per-trace TraceSim (sgpu_tracesim.cuh)
+// right after, in the same kernel.
 #include "sgpu_lanesim.cuh"
 
 namespace sg {
@@ -55,6 +60,12 @@ constexpr int kLaneWarpsPerBlock = 2;      // two warps share a block's 1 KB sme
 // that (C4: 3.96e7 -> 4.03e7 trace-sims/s against the 96-register build;
 // one-box A/Bs).
 template <int K> struct LaneMinBlocks { static constexpr int v = K == 2 ? 8 : K == 4 ? 5 : 9; };
+// With few traces per warp (npol * ndev >= 8, e.g. C5's 8 devices x 4
+// policies) shared memory allows more blocks and registers limit residency:
+// a 64-app variant capped for ten blocks (<= 96 registers) is used there.
+constexpr int kLaneHiBlocks2 = 10;
+// The 64-bit-key retry pass: a 5 KB heap per warp, so fewer resident blocks.
+template <int K> struct LaneMinBlocksR { static constexpr int v = K == 2 ? 6 : K == 4 ? 4 : 7; };
 struct LaneParams {
     SimParams sp;          // inputs/outputs + the fallback TraceSim layout (off_* relative to the warp region)
     uint32_t G;            // traces per warp (32 / lpt)
@@ -214,14 +225,14 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
         }
     }
     uint32_t fail = __any_sync(FULL, big) ? 1u : 0u;
+    bsum = __reduce_add_sync(FULL, bsum);
     uint32_t amax = 0;
 #pragma unroll
     for (int k = 0; k < K; k++) amax = max(amax, key[k] != kInf ? (uint32_t)(key[k] >> 10) : 0u);
     amax = __reduce_max_sync(FULL, amax);
-    bsum = __reduce_add_sync(FULL, bsum);
     // every event time is <= max arrival + busy sum: 32-bit keys suffice
-    // when that stays below 2^(32 - TS) (LaneKey)
-    const bool narrow = (uint64_t)amax + bsum < (1ull << (32u - LaneKey<K, true>::TS));
+    // when that stays below LaneKey::LIM
+    const bool narrow = (uint64_t)amax + bsum < LaneKey<K, true>::LIM;
     warp_sort_keys<K>(key, ndev == 1 && amax < (1u << 22), lane);  // device bits sit above bit 41
     __syncwarp();
     // SoA records in arrival order
@@ -432,8 +443,9 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
 }
 
 // One lane's simulation of (trace t, device d, policy slot pslot) from the
-// staged slot g.  Returns false if the lane must be re-run by the fallback.
-template <int K, bool NARROW>
+// staged slot g with a heap of HW 64-bit keys (or kLaneHeapN 32-bit keys).
+// Returns false if the lane must be re-run (retry pass / fallback).
+template <int K, bool NARROW, uint32_t HW = kLaneHeapW>
 __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const uint16_t* meta, uint32_t g,
                                          uint32_t d, uint32_t pslot, uint32_t policy, uint32_t cap_d,
                                          uint64_t t, uint32_t lane) {
@@ -447,7 +459,7 @@ __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const
     uint64_t a0;
     uint32_t na_unused;
     lane_trace_range(P, t, a0, na_unused);
-    LaneSim<K, NARROW> sim(P);
+    LaneSim<K, NARROW, HW> sim(P);
     sim.s_a = reinterpret_cast<const uint32_t*>(ws + L.off_a) + g * SS::S32;
     sim.s_mem = reinterpret_cast<const uint32_t*>(ws + L.off_mem) + g * SS::S32;
     sim.s_bw = reinterpret_cast<const uint32_t*>(ws + L.off_bw) + g * SS::S32;
@@ -461,7 +473,7 @@ __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const
     if (L.need_cls) { c0 = meta[meta_cls(ndev, d)]; c1 = meta[meta_cls(ndev, d + 1)]; }
     sim.s_cm = reinterpret_cast<const uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW) + c0 * NW;
     sim.ncls = c1 - c0;
-    sim.heap = reinterpret_cast<typename LaneSim<K, NARROW>::Key*>(ws + L.off_fb) + lane;
+    sim.heap = reinterpret_cast<typename LaneSim<K, NARROW, HW>::Key*>(ws + L.off_fb) + lane;
     sim.fifo = reinterpret_cast<uint32_t*>(ws + L.off_fifo) + lane;
     sim.out_base = (uint64_t)pslot * P.n_apps_total + a0;
     if (!sim.run(na, s0, s1, z, policy, cap_d)) return false;
@@ -469,14 +481,22 @@ __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const
     return true;
 }
 
-template <int K>
-__global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, LaneMinBlocks<K>::v) trace_sim_lane_kernel(const LaneParams L) {
+// Main pass (RETRY = false): every trace in order.  A trace whose 64-bit-key
+// lanes overflow their heap (kLaneHeapW events) is appended to P.retry.
+// Retry pass: the traces of P.retry (count P.work[2]) with 64-bit keys and a
+// heap of kLaneHeapN events in a larger warp region.  Other failed lanes
+// (32-bit-key heap or wake FIFO full, staging limits) are re-run in-kernel
+// by the warp-per-trace fallback.
+template <int K, bool RETRY, int MB>
+__global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, MB) trace_sim_lane_kernel(const LaneParams L) {
     const SimParams& P = L.sp;
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
     uint8_t* ws = smem + (size_t)warp * L.warp_bytes;
-    const uint64_t n_groups = (P.n_traces + L.G - 1) / L.G;
+    const uint64_t n_items = RETRY ? *reinterpret_cast<volatile unsigned long long*>(P.work + 2) : P.n_traces;
+    const uint64_t n_groups = (n_items + L.G - 1) / L.G;
+    auto trace_of = [&](uint64_t i) -> uint64_t { return RETRY ? (uint64_t)P.retry[i] : i; };
     const uint32_t ndev = P.ndev;
     // groups are handed out by one atomic counter (each warp takes the next
     // group when it finishes one): no tail of warps with more groups than
@@ -498,27 +518,45 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, LaneMinBlocks<K>::v) 
     while (grp < n_groups) {
         const uint64_t next = fetch();
         const uint64_t t0 = grp * L.G;
-        const uint32_t gcount = (uint32_t)min((uint64_t)L.G, P.n_traces - t0);
-        for (uint32_t s = 0; s < gcount; s++) stage_trace<K>(L, ws, s, t0 + s, lane);
+        const uint32_t gcount = (uint32_t)min((uint64_t)L.G, n_items - t0);
+        for (uint32_t s = 0; s < gcount; s++) stage_trace<K>(L, ws, s, trace_of(t0 + s), lane);
         // warm L2 with the next group's records while this one simulates
-        if (next < n_groups && !P.trace_offsets) {
+        if (!RETRY && next < n_groups && !P.trace_offsets) {
             const uint64_t nt0 = next * L.G;
             const uint64_t nb = min((uint64_t)L.G, P.n_traces - nt0) * P.apps_per_trace * 16u;
             const uint8_t* base = reinterpret_cast<const uint8_t*>(P.apps + nt0 * P.apps_per_trace);
             for (uint64_t off = (uint64_t)lane * 128u; off < nb; off += 32u * 128u) prefetch_l2(base + off);
         }
 
-        bool fail = false;
+        bool fail = false, defer = false;
         const uint16_t* meta = reinterpret_cast<const uint16_t*>(ws + L.off_meta) + g * L.meta_stride;
+        const uint64_t my_t = trace_of(t0 + min(g, gcount - 1));
         // 32-bit event keys when every trace of the group allows them (warp-uniform)
-        const bool narrow = __all_sync(FULL, g >= gcount || meta[2] != 0);
+        const bool narrow = !RETRY && __all_sync(FULL, g >= gcount || meta[2] != 0);
         if (g < gcount) {
             if (meta[1])
                 fail = true;
+            else if (RETRY)
+                fail = !lane_run<K, false, kLaneHeapN>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane);
             else if (narrow)
-                fail = !lane_run<K, true>(L, ws, meta, g, d, pslot, policy, cap_d, t0 + g, lane);
+                fail = !lane_run<K, true>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane);
             else
-                fail = !lane_run<K, false>(L, ws, meta, g, d, pslot, policy, cap_d, t0 + g, lane);
+                defer = !lane_run<K, false>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane);
+        }
+        if (!RETRY) {
+            // a trace with a failed lane goes to the retry pass whole: one
+            // entry per trace, appended by its slot's first lane
+            const uint32_t any = __ballot_sync(FULL, defer);
+            const uint32_t smask = L.lpt >= 32u ? ~0u : (1u << L.lpt) - 1u;
+            const bool dslot = ((any >> (g * L.lpt)) & smask) != 0 && g < gcount;
+            fail = fail && !dslot;  // the retry pass re-runs every lane of a deferred trace
+            const uint32_t dm = __ballot_sync(FULL, dslot && rem == 0);
+            if (dm) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(P.work + 2, (unsigned long long)__popc(dm));
+                base = __shfl_sync(FULL, base, 0);
+                if (dm >> lane & 1u) P.retry[base + __popc(dm & lanemask_lt())] = (uint32_t)my_t;
+            }
         }
         __syncwarp();
         // exact fallback: the whole warp re-simulates each failed lane
@@ -528,7 +566,7 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, LaneMinBlocks<K>::v) 
             const uint32_t frem = fl - fg * L.lpt;
             const uint32_t fd = frem / P.npol;
             const uint32_t fp = frem - fd * P.npol;
-            const uint64_t t = t0 + fg;
+            const uint64_t t = trace_of(t0 + fg);
             uint64_t a0;
             uint32_t na;
             lane_trace_range(P, t, a0, na);
@@ -559,7 +597,7 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, LaneMinBlocks<K>::v) 
         __syncwarp();
         grp = next;
     }
-    work_done(P.work, lane);
+    work_done(P.work, lane, RETRY);
 }
 
 static inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
@@ -579,9 +617,9 @@ bool lane_eligible(const SimParams& p, bool program_mode, bool f64, bool forced)
     return p.n_pad <= 64u || (p.n_pad <= 128u && p.npol * p.ndev >= 2);
 }
 
-template <int K>
+template <int K, bool RETRY, int MB>
 static cudaError_t launch_lane_t(LaneParams& L, cudaStream_t stream, int* grid_out) {
-    auto kern = trace_sim_lane_kernel<K>;
+    auto kern = trace_sim_lane_kernel<K, RETRY, MB>;
     const uint32_t wpb = kLaneWarpsPerBlock;
     const size_t smem = (size_t)L.warp_bytes * wpb;
     if (smem > 227u * 1024u) return cudaErrorInvalidConfiguration;
@@ -604,35 +642,37 @@ static cudaError_t launch_lane_t(LaneParams& L, cudaStream_t stream, int* grid_o
     if (need < grid) grid = need;
     if (grid == 0) grid = 1;
     if (grid_out) *grid_out = (int)grid;
-    err = work_counters(stream, L.sp);
-    if (err != cudaSuccess) return err;
     kern<<<(unsigned)grid, wpb * 32, smem, stream>>>(L);
     return cudaGetLastError();
 }
 
-cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_out) {
-    LaneParams L;
-    L.sp = p;
-    const uint32_t N = p.n_pad;
-    const uint32_t NW = (N + 63u) / 64u;
-    L.lpt = p.npol * p.ndev;
-    // at most 8 traces per warp: the shared slot of a trace is what limits
-    // residency, so fewer simulations per trace (npol * ndev < 4) leave lanes
-    // idle rather than multiply the warp's shared memory
-    L.G = min(32u / L.lpt, 8u);
-    L.need_cls = 0;
-    for (uint32_t i = 0; i < p.npol; i++) {
-        const uint32_t pol = (p.policy_list >> (4 * i)) & 0xFu;
-        if (pol >= SG_POLICY_PFIFO) L.need_cls = 1;
+template <int K>
+static cudaError_t launch_lane_k(LaneParams& L, LaneParams& R, cudaStream_t stream, int* grid_out) {
+    cudaError_t err;
+    // blocks per SM that shared memory allows (228 KB, 1 KB reserved per block)
+    const uint32_t smem_blocks = 233472u / (L.warp_bytes * kLaneWarpsPerBlock + 1024u);
+    if constexpr (K == 2) {
+        if (smem_blocks >= (uint32_t)kLaneHiBlocks2)
+            err = launch_lane_t<K, false, kLaneHiBlocks2>(L, stream, grid_out);
+        else
+            err = launch_lane_t<K, false, LaneMinBlocks<K>::v>(L, stream, grid_out);
+    } else {
+        err = launch_lane_t<K, false, LaneMinBlocks<K>::v>(L, stream, grid_out);
     }
-    L.need_tbl = N <= 128 ? 1u : 0u;  // all kinds use the fit table (one or two mask words)
-    L.cm_per_trace = max(kLaneClassMasks / L.G, 8u);
-    // per-warp region: busy-end heaps / staging scratch; the fallback
+    if (err == cudaSuccess) err = launch_lane_t<K, true, LaneMinBlocksR<K>::v>(R, stream, nullptr);
+    return err;
+}
+
+// Per-warp shared-memory layout of the lane kernel; `heap_bytes` is the
+// busy-end heap region of the warp's 32 lanes.
+static void lane_layout(LaneParams& L, uint32_t heap_bytes) {
+    const uint32_t N = L.sp.n_pad;
+    const uint32_t NW = (N + 63u) / 64u;
+    // the heaps and the staging scratch share one region; the fallback
     // TraceSim overlays the whole warp region once the group's lanes are done
-    sim_layout(L.sp, false, false);
-    const uint32_t fb = max(max(kLaneHeapN * 32u * 4u, kLaneHeapW * 32u * 8u), N * 16u);
+    const uint32_t fb = max(heap_bytes, N * 16u);
     const uint32_t S32 = N + 1, POR = N + 4, LTB = kLtBuckets + 12, T4 = (N / 4 + 1) * NW;  // SlotStride<N>
-    L.meta_stride = meta_u16(p.ndev);
+    L.meta_stride = meta_u16(L.sp.ndev);
     uint32_t o = 0;
     L.off_a = o;
     o = align16(o + L.G * S32 * 4u);
@@ -656,13 +696,44 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
     o = align16(o + fb);
     L.warp_bytes = max(o, align16(L.sp.warp_bytes));
     if (const char* pad = getenv("SGPU_LANE_SMEM_PAD")) L.warp_bytes += align16((uint32_t)atoi(pad));  // occupancy experiments
-    switch (N / 32) {
-        case 1: return launch_lane_t<1>(L, stream, grid_out);
-        case 2: return launch_lane_t<2>(L, stream, grid_out);
-        case 4: return launch_lane_t<4>(L, stream, grid_out);
-        case 8: return launch_lane_t<8>(L, stream, grid_out);
-        default: return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_out) {
+    if (p.n_traces > 0xFFFFFFFFull) return cudaErrorInvalidValue;  // 32-bit deferred-trace ids
+    LaneParams L;
+    L.sp = p;
+    const uint32_t N = p.n_pad;
+    L.lpt = p.npol * p.ndev;
+    // at most 8 traces per warp: the shared slot of a trace is what limits
+    // residency, so fewer simulations per trace (npol * ndev < 4) leave lanes
+    // idle rather than multiply the warp's shared memory
+    L.G = min(32u / L.lpt, 8u);
+    L.need_cls = 0;
+    for (uint32_t i = 0; i < p.npol; i++) {
+        const uint32_t pol = (p.policy_list >> (4 * i)) & 0xFu;
+        if (pol >= SG_POLICY_PFIFO) L.need_cls = 1;
     }
+    L.need_tbl = N <= 128 ? 1u : 0u;  // all kinds use the fit table (one or two mask words)
+    L.cm_per_trace = max(kLaneClassMasks / L.G, 8u);
+    sim_layout(L.sp, false, false);
+    bool owned = false;
+    cudaError_t err = work_counters(stream, L.sp, p.n_traces, &owned);
+    if (err != cudaSuccess) return err;
+    LaneParams R = L;
+    lane_layout(L, max(kLaneHeapN * 32u * 4u, kLaneHeapW * 32u * 8u));
+    lane_layout(R, kLaneHeapN * 32u * 8u);
+    switch (N / 32) {
+        case 1: err = launch_lane_k<1>(L, R, stream, grid_out); break;
+        case 2: err = launch_lane_k<2>(L, R, stream, grid_out); break;
+        case 4: err = launch_lane_k<4>(L, R, stream, grid_out); break;
+        case 8: err = launch_lane_k<8>(L, R, stream, grid_out); break;
+        default: err = cudaErrorInvalidValue;
+    }
+    if (owned) {
+        const cudaError_t e2 = cudaFreeAsync(L.sp.retry, stream);
+        if (err == cudaSuccess) err = e2;
+    }
+    return err;
 }
 
 }  // namespace sg

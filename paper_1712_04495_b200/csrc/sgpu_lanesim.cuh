@@ -31,8 +31,8 @@ inline int __ffs(int x) { return __builtin_ffs(x); }
 
 namespace sg {
 
-constexpr uint32_t kLaneHeapN = 20;         // busy-end heap slots per lane, 32-bit keys: 4-ary, depth 2
-constexpr uint32_t kLaneHeapW = 10;         // the same region with 64-bit keys
+constexpr uint32_t kLaneHeapN = 20;         // busy-end heap slots per lane: 4-ary, depth 2
+constexpr uint32_t kLaneHeapW = 10;         // the same 2.5 KB region with 64-bit keys (main pass)
 constexpr uint32_t kLaneFifoWords = 2;      // wake FIFO: 4 app positions per u32 word
 constexpr uint32_t kLaneFifo = 4 * kLaneFifoWords;
 constexpr uint64_t kInf = ~0ull;
@@ -58,17 +58,20 @@ template <int K> struct LogN { static constexpr uint32_t v = K == 1 ? 5 : K == 2
 
 // Event keys (t, virtual counter, position).  NARROW: one u32, t << (2 LOGN
 // + 1) | counter << LOGN | q, usable when every event time of the trace is
-// below 2^(31 - 2 LOGN) (arrival max + busy sum, checked at staging): each
-// app pushes at most one busy end, so the counter of the initial pop of app i
-// is i and later pushes count up from N (< 2N).  Wide: one u64, t << 32 |
-// counter << 8 | q with the block counters described above.
-template <int K, bool NARROW> struct LaneKey {
+// below LIM = 2^(31 - 2 LOGN) - 1 (arrival max + busy sum, checked at
+// staging; time(INF) = LIM stays above every event time, which the wake-up
+// test relies on).  Each app pushes at most one busy end, so the counter of
+// the initial pop of app i is i and later pushes count up from N (< 2N).
+// Wide: one u64, t << 32 | counter << 8 | q with the block counters
+// described above.  HW: heap capacity with 64-bit keys.
+template <int K, bool NARROW, uint32_t HW = kLaneHeapW> struct LaneKey {
     static constexpr uint32_t LOGN = LogN<K>::v;
     using T = typename std::conditional<NARROW, uint32_t, uint64_t>::type;
     static constexpr uint32_t QB = NARROW ? LOGN : 8u;
     static constexpr uint32_t TS = NARROW ? 2u * LOGN + 1u : 32u;
     static constexpr T INF = (T)~(T)0;
-    static constexpr uint32_t HCAP = NARROW ? kLaneHeapN : kLaneHeapW;
+    static constexpr uint32_t HCAP = NARROW ? kLaneHeapN : HW;
+    static constexpr uint32_t LIM = NARROW ? (1u << (32u - TS)) - 1u : ~0u;
     static SG_HD T make(uint32_t t, uint32_t c, uint32_t q) {
         return ((T)t << TS) | ((T)c << QB) | (T)q;
     }
@@ -79,13 +82,13 @@ template <int K, bool NARROW> struct LaneKey {
     static SG_HD uint32_t c_base(uint32_t n) { return NARROW ? 32u * K : n << LOGN; }
 };
 
-template <int K, bool NARROW>
+template <int K, bool NARROW, uint32_t HW = kLaneHeapW>
 struct LaneSim {
     static constexpr uint32_t N = 32u * K;
     static constexpr uint32_t NW = (N + 63u) / 64u;  // queue mask words
     static constexpr uint32_t LOGN = LogN<K>::v;
     static constexpr bool TBL = K <= 4;              // fit table (one or two mask words)
-    using KY = LaneKey<K, NARROW>;
+    using KY = LaneKey<K, NARROW, HW>;
     using Key = typename KY::T;
 
     const SimParams& P;
@@ -559,7 +562,7 @@ struct LaneSim {
             }
             if (fail) return false;
         }
-        return true;
+        return !fail;  // a resumed waiter's push can fail just before the queue runs dry
     }
 
 #ifdef __CUDACC__

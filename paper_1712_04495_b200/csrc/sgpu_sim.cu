@@ -30,9 +30,11 @@
 //   * traces with several simulated devices run as per-device sub-traces: the
 //     devices share only the global push counter, whose interleaving cannot
 //     reorder events of one device (pinned by tests/golden/ref_multidev.npz)
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <thread>
+#include <vector>
 
 #include "sgpu_tracesim.cuh"
 
@@ -176,20 +178,22 @@ struct WorkPool {
     unsigned long long* ctr = nullptr;
     std::map<std::pair<cudaStream_t, std::thread::id>, int> slot;
     int next = 0;
+    std::vector<std::pair<uint32_t*, uint64_t>> retry = std::vector<std::pair<uint32_t*, uint64_t>>(kWorkSlots);
 };
+constexpr int kWorkWords = 4;  // u64 counters per slot
 std::mutex g_work_mu;
 std::map<int, WorkPool> g_work;
 }  // namespace
 
-cudaError_t work_counters(cudaStream_t stream, SimParams& p) {
+cudaError_t work_counters(cudaStream_t stream, SimParams& p, uint64_t retry_cap, bool* retry_owned) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lk(g_work_mu);
     WorkPool& w = g_work[dev];
     if (!w.ctr) {
-        e = cudaMalloc(&w.ctr, 2 * kWorkSlots * sizeof(unsigned long long));
-        if (e == cudaSuccess) e = cudaMemset(w.ctr, 0, 2 * kWorkSlots * sizeof(unsigned long long));
+        e = cudaMalloc(&w.ctr, kWorkWords * kWorkSlots * sizeof(unsigned long long));
+        if (e == cudaSuccess) e = cudaMemset(w.ctr, 0, kWorkWords * kWorkSlots * sizeof(unsigned long long));
         if (e != cudaSuccess) { w.ctr = nullptr; return e; }
     }
     const auto key = std::make_pair(stream, stream == cudaStreamPerThread ? std::this_thread::get_id()
@@ -204,7 +208,38 @@ cudaError_t work_counters(cudaStream_t stream, SimParams& p) {
     } else {
         s = it->second;
     }
-    p.work = w.ctr + 2 * s;
+    p.work = w.ctr + kWorkWords * s;
+    p.retry = nullptr;
+    if (retry_owned) *retry_owned = false;
+    if (retry_cap == 0) return cudaSuccess;
+    auto& rb = w.retry[s];
+    if (rb.second < retry_cap) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        e = cudaStreamIsCapturing(stream, &cs);
+        if (e != cudaSuccess) return e;
+        if (cs != cudaStreamCaptureStatusNone) {
+            // inside a capture: a graph-owned list, freed by the same graph
+            if (!retry_owned) return cudaErrorInvalidValue;
+            uint32_t* b = nullptr;
+            e = cudaMallocAsync(reinterpret_cast<void**>(&b), retry_cap * 4u, stream);
+            if (e != cudaSuccess) return e;
+            p.retry = b;
+            *retry_owned = true;
+            return cudaSuccess;
+        }
+        // grow: work already queued on the stream may still read the old list
+        if (rb.first) {
+            e = cudaStreamSynchronize(stream);
+            if (e == cudaSuccess) e = cudaFree(rb.first);
+            if (e != cudaSuccess) return e;
+            rb = {nullptr, 0};
+        }
+        const uint64_t c = std::max<uint64_t>(retry_cap, 1u << 16);
+        e = cudaMalloc(&rb.first, c * 4u);
+        if (e != cudaSuccess) { rb = {nullptr, 0}; return e; }
+        rb.second = c;
+    }
+    p.retry = rb.first;
     return cudaSuccess;
 }
 

@@ -8,4 +8,4 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
 cat gpurun_out/bench.json
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/b_ncu.log 2>&1; echo "ncu list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:trace_sim_lane -s 3 -c 1 -o gpurun_out/lane_full python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/lane_full.log 2>&1; echo "ncu full rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:trace_sim_lane_kernelILi2ELb0 -s 3 -c 1 -o gpurun_out/lane_full python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/lane_full.log 2>&1; echo "ncu full rc=$?"

@@ -5,7 +5,9 @@
 // Staging (arrival order, fit table, class masks) is rebuilt here from its
 // definition in sgpu_lane.cu's stage_trace, single device.
 //
-// stdin, per case:  n policy cap narrow(0|1)  then n lines: arrival mem busy prio
+// stdin, per case:  n policy cap keys  then n lines: arrival mem busy prio
+//   keys: 1 = 32-bit keys, 0 = 64-bit keys with the main pass's heap
+//   (kLaneHeapW), 2 = 64-bit keys with the retry pass's heap (kLaneHeapN)
 // stdout, per case: ok T B I grants pops maxh unfinished  grant_0 end_0 ... (app order)
 #include <cstdio>
 #include <cstring>
@@ -15,12 +17,12 @@
 
 using namespace sg;
 
-template <int K, bool NAR>
+template <int K, bool NAR, uint32_t HW = kLaneHeapW>
 static void run_case(int n, uint32_t policy, uint32_t cap, const std::vector<uint32_t>& A,
                      const std::vector<uint32_t>& M, const std::vector<uint32_t>& Bz,
                      const std::vector<uint32_t>& Pr) {
     constexpr uint32_t N = 32u * K;
-    using Sim = LaneSim<K, NAR>;
+    using Sim = LaneSim<K, NAR, HW>;
     constexpr uint32_t NW = Sim::NW;
     // arrival order: (arrival, index)
     std::vector<int> ord(n);
@@ -111,13 +113,16 @@ int main() {
         for (int i = 0; i < n; i++)
             if (scanf("%u %u %u %u", &A[i], &M[i], &Bz[i], &Pr[i]) != 4) return 1;
         if (n <= 32) {
-            if (narrow) run_case<1, true>(n, policy, cap, A, M, Bz, Pr);
+            if (narrow == 1) run_case<1, true>(n, policy, cap, A, M, Bz, Pr);
+            else if (narrow == 2) run_case<1, false, kLaneHeapN>(n, policy, cap, A, M, Bz, Pr);
             else run_case<1, false>(n, policy, cap, A, M, Bz, Pr);
         } else if (n <= 64) {
-            if (narrow) run_case<2, true>(n, policy, cap, A, M, Bz, Pr);
+            if (narrow == 1) run_case<2, true>(n, policy, cap, A, M, Bz, Pr);
+            else if (narrow == 2) run_case<2, false, kLaneHeapN>(n, policy, cap, A, M, Bz, Pr);
             else run_case<2, false>(n, policy, cap, A, M, Bz, Pr);
         } else {
-            if (narrow) run_case<4, true>(n, policy, cap, A, M, Bz, Pr);
+            if (narrow == 1) run_case<4, true>(n, policy, cap, A, M, Bz, Pr);
+            else if (narrow == 2) run_case<4, false, kLaneHeapN>(n, policy, cap, A, M, Bz, Pr);
             else run_case<4, false>(n, policy, cap, A, M, Bz, Pr);
         }
         fflush(stdout);

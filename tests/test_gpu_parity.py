@@ -201,6 +201,27 @@ def test_lane_fallback_tick_range(cuda):
     check_against_oracle(apps, (1000,), cuda)
 
 
+@pytest.mark.parametrize("n,ndev", [(32, 1), (64, 1), (100, 1), (128, 1), (64, 2)])
+def test_lane_retry_pass(n, ndev, cuda):
+    """Traces that need 64-bit event keys (arrival max + busy sum past
+    LaneKey::LIM) with 6..26 apps busy at once: those whose 64-bit-key lanes
+    overflow the main pass's 10-event heap are re-simulated by the second
+    launch (20-event heap), the busiest ones again by the warp fallback,
+    mixed in one batch with traces that keep 32-bit keys."""
+    rng = np.random.default_rng(40 + n + ndev)
+    nt = 240
+    apps = np.zeros((nt, n, 4), dtype=np.uint32)
+    apps[:, :, 0] = rng.integers(0, 64, (nt, n))
+    conc = np.linspace(6, 26, nt).astype(np.uint32)
+    apps[:, :, 1] = (1000 // conc)[:, None]
+    apps[:, :, 2] = rng.integers(1 << 14, 1 << 16, (nt, n))      # 64-bit keys
+    apps[::5, :, 2] = rng.integers(1, 64, (len(apps[::5]), n))    # 32-bit keys
+    apps[:, :, 3] = rng.integers(0, 3, (nt, n))
+    if ndev > 1:
+        apps[:, :, 3] |= (np.arange(n) % ndev).astype(np.uint32)[None, :] << 8
+    check_against_oracle(apps, (1000,) * ndev, cuda)
+
+
 def test_wide_sort_keys(cuda):
     """Arrivals >= 2^22 and requests >= 2^24 MiB take the 64-bit key sorts of
     the lane kernel's staging (narrow 32-bit sorts otherwise)."""
@@ -424,11 +445,16 @@ def test_host_pipeline_policy_subsets(pols, cuda):
     np.testing.assert_array_equal(host.stats.view(np.uint8), dres.stats().view(np.uint8))
 
 
-def test_cuda_graph_replay(cuda):
+@pytest.mark.parametrize("tick_scale", [1, 256])
+def test_cuda_graph_replay(tick_scale, cuda):
     """K1 launched inside a captured CUDA graph and replayed on new inputs:
     the work counters reset at the end of every launch, so each replay
-    covers every trace again."""
+    covers every trace again.  At tick scale 256 the traces need 64-bit
+    event keys: the retry launch and its graph-owned deferred list run in
+    every replay."""
     cfg = CONFIGS["C2"]
+    cfg = dataclasses.replace(cfg, gen=dataclasses.replace(
+        cfg.gen, arr_hi=4095 * tick_scale, busy_hi=2048 * tick_scale, busy_lo=tick_scale))
     n = 5000
     apps_t = B.generate_traces(cfg.gen, 0, n, device=0)
     B.simulate_batch(apps_t, POLICIES, cfg.cap_mib)  # warm-up: kernel attributes, counter pool

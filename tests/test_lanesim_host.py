@@ -36,10 +36,12 @@ def lanesim(tmp_path_factory):
     return exe
 
 
-def run_host(exe, apps, pol, cap, narrow):
+def run_host(exe, apps, pol, cap, keys):
+    """keys: 1 / True = 32-bit, 0 / False = 64-bit (main-pass heap),
+    2 = 64-bit (retry-pass heap)."""
     lines = []
     for tr in apps:
-        lines.append(f"{len(tr)} {CODES[pol]} {cap} {int(narrow)}")
+        lines.append(f"{len(tr)} {CODES[pol]} {cap} {int(keys)}")
         lines.extend(" ".join(str(int(x)) for x in (r[0], r[1], r[2], r[3] & 0xFF)) for r in tr)
     out = subprocess.run([exe], input="\n".join(lines) + "\n", capture_output=True, text=True,
                          check=True).stdout.split("\n")
@@ -64,11 +66,24 @@ def check(exe, apps, pol, cap, narrow, min_checked):
     return checked
 
 
-def narrow_ok(apps, n):
-    """The kernel's staging rule for 32-bit keys (sgpu_lane.cu stage_trace)."""
+def narrow_lim(n):
+    """LaneKey<K, true>::LIM: every event time of a 32-bit-key lane stays below it."""
     logn = 5 if n <= 32 else 6 if n <= 64 else 7
+    return (1 << (31 - 2 * logn)) - 1
+
+
+def narrow_mask(apps, n):
+    """Per trace, the kernel's staging rule for 32-bit keys (sgpu_lane.cu
+    stage_trace): arrival max + busy sum below LaneKey::LIM."""
     a = apps.astype(np.uint64)
-    return bool(np.all(a[..., 0].max(axis=1) + a[..., 2].sum(axis=1) < (1 << (31 - 2 * logn))))
+    return a[..., 0].max(axis=1) + a[..., 2].sum(axis=1) < narrow_lim(n)
+
+
+def narrow_ok(apps, n):
+    return bool(np.all(narrow_mask(apps, n)))
+
+
+WIDE, NARROW, WIDE_RETRY = 0, 1, 2   # lanesim_host key modes
 
 
 @pytest.mark.parametrize("pol", POLICIES)
@@ -76,9 +91,58 @@ def test_lanesim_c2_traces(lanesim, pol):
     cfg = CONFIGS["C2"]
     apps = as_u32x4(generate(cfg.gen, 123_456, 150))
     assert narrow_ok(apps, 64)
-    check(lanesim, apps, pol, cfg.cap_mib[0], True, 150)
-    # 64-bit keys: 10 heap slots, so the busiest traces decline to the fallback
-    check(lanesim, apps, pol, cfg.cap_mib[0], False, 1)
+    check(lanesim, apps, pol, cfg.cap_mib[0], NARROW, 150)
+    # 64-bit keys: the main pass's 10-slot heap declines the busiest traces
+    # to the retry pass, whose 20-slot heap takes them all
+    check(lanesim, apps, pol, cfg.cap_mib[0], WIDE, 1)
+    check(lanesim, apps, pol, cfg.cap_mib[0], WIDE_RETRY, 150)
+
+
+@pytest.mark.parametrize("pol", POLICIES)
+@pytest.mark.parametrize("n", [32, 64, 128])
+def test_lanesim_narrow_limit_boundary(lanesim, pol, n):
+    """A holder ending near LaneKey::LIM with a waiter behind it whose busy
+    step is 0 or 1 (the waiter's wake-up is the last event): every trace the
+    staging rule admits to 32-bit keys, up to the tightest one (arrival max
+    + busy sum = LIM - 1), matches the oracle; 64-bit keys take them all."""
+    lim = narrow_lim(n)
+    traces = []
+    for end in range(lim - 5, lim + 2):
+        for wb in (0, 1):
+            tr = np.zeros((n, 4), np.uint32)
+            tr[0] = (1000, 10, end - 1000, 0)   # holder: the whole device (busy < 2^21)
+            tr[1] = (1001, 10, wb, 0)           # waiter, granted at the holder's end
+            traces.append(tr)
+    apps = np.stack(traces)
+    ok = narrow_mask(apps, n)
+    a = apps.astype(np.int64)
+    assert (a[ok, :, 0].max(axis=1) + a[ok, :, 2].sum(axis=1)).max() == lim - 1
+    check(lanesim, apps[ok], pol, 10, NARROW, int(ok.sum()))
+    check(lanesim, apps, pol, 10, WIDE, len(apps))
+
+
+@pytest.mark.parametrize("pol", POLICIES)
+@pytest.mark.parametrize("n", [32, 64, 128])
+def test_lanesim_wide_heap_overflow(lanesim, pol, n):
+    """11..20 busy apps at once overflow the main pass's 64-bit heap (10
+    events) but not the retry pass's (20); more overflow both (the kernel's
+    warp fallback runs those)."""
+    rng = np.random.default_rng(900 + n)
+    nt = 120
+    apps = np.zeros((nt, n, 4), np.uint32)
+    apps[..., 0] = rng.integers(0, 64, (nt, n))
+    conc = np.linspace(6, 26, nt).astype(int)                 # target concurrency per trace
+    apps[..., 1] = (1000 // conc)[:, None]
+    apps[..., 2] = rng.integers(500, 900, (nt, n))
+    apps[..., 3] = rng.integers(0, 3, (nt, n))
+    wide = run_host(lanesim, apps, pol, 1000, WIDE)
+    retry = run_host(lanesim, apps, pol, 1000, WIDE_RETRY)
+    d_wide = np.array([v[0] == 0 for v in wide])
+    d_retry = np.array([v[0] == 0 for v in retry])
+    assert not np.any(d_retry & ~d_wide)                      # a bigger heap never declines more
+    assert np.sum(d_wide & ~d_retry) >= 10 and np.sum(~d_wide) >= 10
+    check(lanesim, apps, pol, 1000, WIDE, int((~d_wide).sum()))
+    check(lanesim, apps, pol, 1000, WIDE_RETRY, int((~d_retry).sum()))
 
 
 def random_edge_traces(rng, n_traces, n, cap):
@@ -100,8 +164,9 @@ def test_lanesim_edge_shapes(lanesim, pol, n):
     rng = np.random.default_rng(1000 + n)
     cap = 1000
     apps = random_edge_traces(rng, 300, n, cap)
-    check(lanesim, apps, pol, cap, True, 250)
-    check(lanesim, apps, pol, cap, False, 10 if n <= 64 else 0)
+    check(lanesim, apps, pol, cap, NARROW, 250)
+    check(lanesim, apps, pol, cap, WIDE, 10 if n <= 64 else 0)
+    check(lanesim, apps, pol, cap, WIDE_RETRY, 250)
 
 
 @pytest.mark.parametrize("pol", POLICIES)
@@ -115,14 +180,22 @@ def test_lanesim_near_capacity(lanesim, pol, n):
     apps[..., 1] = rng.integers(46_080, cap + 1, (100, n))
     apps[..., 2] = rng.integers(1, 2049, (100, n))
     apps[..., 3] = rng.integers(0, 4, (100, n))
-    check(lanesim, apps, pol, cap, narrow_ok(apps, n), 100)
+    ok = narrow_mask(apps, n)
+    if ok.any():
+        check(lanesim, apps[ok], pol, cap, NARROW, int(ok.sum()))
+    check(lanesim, apps, pol, cap, WIDE, 100)
+    check(lanesim, apps, pol, cap, WIDE_RETRY, 100)
 
 
 @pytest.mark.parametrize("pol", POLICIES)
 def test_lanesim_c4_traces(lanesim, pol):
     cfg = CONFIGS["C4"]
     apps = as_u32x4(generate(cfg.gen, 7_000, 40))
-    check(lanesim, apps, pol, cfg.cap_mib[0], narrow_ok(apps, 128), 40)
+    ok = narrow_mask(apps, 128)
+    assert 0 < ok.sum() < len(ok)   # C4 mixes 32- and 64-bit-key traces
+    check(lanesim, apps[ok], pol, cfg.cap_mib[0], NARROW, int(ok.sum()))
+    check(lanesim, apps, pol, cfg.cap_mib[0], WIDE, 40)
+    check(lanesim, apps, pol, cfg.cap_mib[0], WIDE_RETRY, 40)
 
 
 def test_header_is_shared_with_the_kernel():
