@@ -233,6 +233,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
     // every event time is <= max arrival + busy sum: 32-bit keys suffice
     // when that stays below LaneKey::LIM
     const bool narrow = (uint64_t)amax + bsum < LaneKey<K, true>::LIM;
+    bool wide_big = false;  // 64-bit keys and more than kLaneHeapW apps can be busy at once
     warp_sort_keys<K>(key, ndev == 1 && amax < (1u << 22), lane);  // device bits sit above bit 41
     __syncwarp();
     // SoA records in arrival order
@@ -418,6 +419,27 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
         }
         // buckets above the largest request (all ranks valid) -> N
         for (uint32_t j = bcarry + lane; j < kLtBuckets; j += 32u) s_lt[j] = (uint8_t)N;
+        if (!narrow && ndev == 1) {
+            // busy apps at once <= apps without a request + the most requests
+            // that fit the device together (the k smallest): ranks whose
+            // prefix sum of sorted requests is <= cap.  Above the main
+            // pass's 64-bit heap, the trace goes to the retry pass directly.
+            uint64_t run = 0;
+            uint32_t fit = 0;
+#pragma unroll
+            for (int k = 0; k < K; k++) {
+                uint64_t v = mk[k] != kInf ? (mk[k] >> 8) : (uint64_t)0xFFFFFFFFu;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint64_t u = shfl_up_u64(v, o);
+                    if (lane >= (uint32_t)o) v += u;
+                }
+                v += run;
+                fit += __popc(__ballot_sync(FULL, v <= P.cap[0]));
+                run = __shfl_sync(FULL, (uint32_t)v, 31) | ((uint64_t)__shfl_sync(FULL, (uint32_t)(v >> 32), 31) << 32);
+            }
+            wide_big = fit > kLaneHeapW;
+        }
         if (lane < NW) s_t4[lane] = 0ull;
         if (lane == 0) {
             uint32_t* prm = reinterpret_cast<uint32_t*>(s_lt + kLtBuckets);
@@ -435,7 +457,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
     if (lane == 0) {
         meta[0] = (uint16_t)na;
         meta[1] = (uint16_t)fail;
-        meta[2] = narrow ? 1u : 0u;
+        meta[2] = narrow ? 1u : wide_big ? 2u : 0u;  // 32-bit keys / 64-bit, retry pass / 64-bit
         meta[meta_dev(0)] = 0;
         meta[meta_cls(ndev, 0)] = 0;
     }
@@ -532,7 +554,7 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, MB) trace_sim_lane_ke
         const uint16_t* meta = reinterpret_cast<const uint16_t*>(ws + L.off_meta) + g * L.meta_stride;
         const uint64_t my_t = trace_of(t0 + min(g, gcount - 1));
         // 32-bit event keys when every trace of the group allows them (warp-uniform)
-        const bool narrow = !RETRY && __all_sync(FULL, g >= gcount || meta[2] != 0);
+        const bool narrow = !RETRY && __all_sync(FULL, g >= gcount || meta[2] == 1);
         if (g < gcount) {
             if (meta[1])
                 fail = true;
@@ -540,6 +562,8 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, MB) trace_sim_lane_ke
                 fail = !lane_run<K, false, kLaneHeapN>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane);
             else if (narrow)
                 fail = !lane_run<K, true>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane);
+            else if (meta[2] == 2)
+                defer = true;
             else
                 defer = !lane_run<K, false>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane);
         }
