@@ -364,6 +364,8 @@ def main():
     launches = 0
     # K1 (lane engine: main pass + 64-bit-key retry pass) + K2 stats_reduce
     k1_launches = B.k1_launches(cfg.gen.apps_per_trace, npol, cfg.ndev)
+    k1_kernel = {"lane": "trace_sim_lane_kernel", "warp": "trace_sim_kernel"}[
+        B.k1_engine(cfg.gen.apps_per_trace, npol, cfg.ndev)]
 
     def step(i=None):
         nonlocal launches
@@ -494,7 +496,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch",
                          "traffic_source": TRAFFIC_SOURCE if traffic else None, "peak_source": peak_src,
-                         "kernel": os.environ.get("SGPU_K1_NAME", "trace_sim_lane_kernel"), "alg_bytes_per_launch": alg_bytes,
+                         "kernel": k1_kernel, "alg_bytes_per_launch": alg_bytes,
                          "mean_launch_ms": mean_k * 1000.0,
                          # what bounds this kernel instead: issue slots (the ncu capture above)
                          "issue_active_frac": issue_pct / 100.0 if issue_pct else None},

@@ -283,21 +283,27 @@ def simulate_batch_host(apps: np.ndarray, policies: Iterable = ("fifo",), cap_mi
                       out.stats, out.mem_pct if want_pct else None, out.dev_pct if want_pct else None)
 
 
-def k1_launches(apps_per_trace: int, n_policies: int, ndev: int = 1) -> int:
-    """Kernel launches of one T0 simulate_batch call: two on the lane engine
-    (the main pass + the 64-bit-key retry pass, sgpu_lane.cu
-    launch_sim_lane), one on the warp engine.  Mirrors the default engine
-    choice of sgpu_lane.cu lane_eligible and the SGPU_K1 override."""
+def k1_engine(apps_per_trace: int, n_policies: int, ndev: int = 1) -> str:
+    """K1 engine of a T0 simulate_batch call: "lane" (trace_sim_lane) or
+    "warp" (trace_sim).  Mirrors the default choice of sgpu_lane.cu
+    lane_eligible and the SGPU_K1 override."""
     n_pad = 32
     while n_pad < apps_per_trace:
         n_pad *= 2
     eng = os.environ.get("SGPU_K1", "")
-    if eng == "warp":
-        return 1
+    if eng == "warp" or n_policies * ndev > 32:
+        return "warp"
     lane = n_pad <= 64 or (n_pad <= 128 and n_policies * ndev >= 2)
     if eng == "lane":
         lane = n_pad <= 256
-    return 2 if lane and n_policies * ndev <= 32 else 1
+    return "lane" if lane else "warp"
+
+
+def k1_launches(apps_per_trace: int, n_policies: int, ndev: int = 1) -> int:
+    """Kernel launches of one T0 simulate_batch call: two on the lane engine
+    (the main pass + the 64-bit-key retry pass, sgpu_lane.cu
+    launch_sim_lane), one on the warp engine."""
+    return 2 if k1_engine(apps_per_trace, n_policies, ndev) == "lane" else 1
 
 
 def reduce_stats(stats_raw, stream=None) -> dict:

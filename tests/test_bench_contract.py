@@ -27,3 +27,23 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
     assert d["config"]["workload"].startswith("C2")
+
+
+def test_k1_engine_and_launch_count(monkeypatch):
+    """bench.py's gpu_launches and roofline kernel name follow the engine
+    sg_simulate_batch picks (sgpu_lane.cu lane_eligible)."""
+    sys.path.insert(0, ROOT)
+    from paper_1712_04495_b200 import batch as B
+    from paper_1712_04495_b200.tracegen import CONFIGS
+    monkeypatch.delenv("SGPU_K1", raising=False)
+    want = {"C2": "lane", "C3": "warp", "C4": "lane", "C5": "lane"}
+    for c, eng in want.items():
+        cfg = CONFIGS[c]
+        assert B.k1_engine(cfg.gen.apps_per_trace, len(cfg.policies), cfg.ndev) == eng, c
+        assert B.k1_launches(cfg.gen.apps_per_trace, len(cfg.policies), cfg.ndev) == (2 if eng == "lane" else 1)
+    assert B.k1_engine(128, 1) == "warp"          # one policy at 128 apps: the warp kernel is faster
+    assert B.k1_engine(20, 4, 9) == "warp"        # more than 32 simulations per trace
+    monkeypatch.setenv("SGPU_K1", "warp")
+    assert B.k1_engine(64, 4) == "warp" and B.k1_launches(64, 4) == 1
+    monkeypatch.setenv("SGPU_K1", "lane")
+    assert B.k1_engine(256, 2) == "lane"
