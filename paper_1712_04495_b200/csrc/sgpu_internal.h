@@ -46,11 +46,10 @@ struct SimParams {
 
 // The work counters of `stream` on the current device (sets p.work) and,
 // when retry_cap > 0, a deferred-trace list of that many entries that stays
-// valid for work on `stream` (sets p.retry).  Inside a stream capture the list
-// is a graph allocation (*retry_owned = true): the caller frees it on the
-// stream after its last use.
-cudaError_t work_counters(cudaStream_t stream, SimParams& p, uint64_t retry_cap = 0,
-                          bool* retry_owned = nullptr);
+// valid for work on `stream` (sets p.retry).  Inside a stream capture both
+// are one graph allocation at p.work (*owned = true): the caller frees it
+// on the stream after its last launch.
+cudaError_t work_counters(cudaStream_t stream, SimParams& p, uint64_t retry_cap, bool* owned);
 
 // Shared-memory layout for one warp simulating traces of up to n_pad apps.
 void sim_layout(SimParams& p, bool program_mode, bool f64);

@@ -754,7 +754,7 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
         default: err = cudaErrorInvalidValue;
     }
     if (owned) {
-        const cudaError_t e2 = cudaFreeAsync(L.sp.retry, stream);
+        const cudaError_t e2 = cudaFreeAsync(L.sp.work, stream);
         if (err == cudaSuccess) err = e2;
     }
     return err;

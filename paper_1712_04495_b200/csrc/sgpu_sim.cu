@@ -185,9 +185,28 @@ std::mutex g_work_mu;
 std::map<int, WorkPool> g_work;
 }  // namespace
 
-cudaError_t work_counters(cudaStream_t stream, SimParams& p, uint64_t retry_cap, bool* retry_owned) {
+cudaError_t work_counters(cudaStream_t stream, SimParams& p, uint64_t retry_cap, bool* owned) {
+    if (owned) *owned = false;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaError_t e = cudaStreamIsCapturing(stream, &cs);
+    if (e != cudaSuccess) return e;
+    if (cs != cudaStreamCaptureStatusNone) {
+        // inside a capture: counters and list are graph allocations (zeroed
+        // by a memset node at every replay), so a replay never shares them
+        // with the capturing stream's later work or with another replay
+        if (!owned) return cudaErrorInvalidValue;
+        void* b = nullptr;
+        e = cudaMallocAsync(&b, kWorkWords * sizeof(unsigned long long) + retry_cap * 4u, stream);
+        if (e != cudaSuccess) return e;
+        e = cudaMemsetAsync(b, 0, kWorkWords * sizeof(unsigned long long), stream);
+        if (e != cudaSuccess) return e;
+        p.work = static_cast<unsigned long long*>(b);
+        p.retry = retry_cap ? reinterpret_cast<uint32_t*>(p.work + kWorkWords) : nullptr;
+        *owned = true;
+        return cudaSuccess;
+    }
     int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
+    e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lk(g_work_mu);
     WorkPool& w = g_work[dev];
@@ -210,23 +229,9 @@ cudaError_t work_counters(cudaStream_t stream, SimParams& p, uint64_t retry_cap,
     }
     p.work = w.ctr + kWorkWords * s;
     p.retry = nullptr;
-    if (retry_owned) *retry_owned = false;
     if (retry_cap == 0) return cudaSuccess;
     auto& rb = w.retry[s];
     if (rb.second < retry_cap) {
-        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        e = cudaStreamIsCapturing(stream, &cs);
-        if (e != cudaSuccess) return e;
-        if (cs != cudaStreamCaptureStatusNone) {
-            // inside a capture: a graph-owned list, freed by the same graph
-            if (!retry_owned) return cudaErrorInvalidValue;
-            uint32_t* b = nullptr;
-            e = cudaMallocAsync(reinterpret_cast<void**>(&b), retry_cap * 4u, stream);
-            if (e != cudaSuccess) return e;
-            p.retry = b;
-            *retry_owned = true;
-            return cudaSuccess;
-        }
         // grow: work already queued on the stream may still read the old list
         if (rb.first) {
             e = cudaStreamSynchronize(stream);
@@ -307,10 +312,16 @@ static cudaError_t launch_t(const SimParams& p, cudaStream_t stream, int* grid_o
     if (grid == 0) grid = 1;
     if (grid_out) *grid_out = (int)grid;
     SimParams q = p;
-    err = work_counters(stream, q);
+    bool owned = false;
+    err = work_counters(stream, q, 0, &owned);
     if (err != cudaSuccess) return err;
     kern<<<(unsigned)grid, wpb * 32, smem, stream>>>(q);
-    return cudaGetLastError();
+    err = cudaGetLastError();
+    if (owned) {
+        const cudaError_t e2 = cudaFreeAsync(q.work, stream);
+        if (err == cudaSuccess) err = e2;
+    }
+    return err;
 }
 
 template <class TM, bool PROG>

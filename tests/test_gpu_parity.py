@@ -474,3 +474,33 @@ def test_cuda_graph_replay(tick_scale, cuda):
             gr, e, sref = O.simulate_burst(apps, cfg.cap_mib, pol.value)
             np.testing.assert_array_equal(res.ticks("end")[pi].reshape(e.shape), e, err_msg=f"replay {k}")
             np.testing.assert_array_equal(st[pi].view(np.uint8), sref.view(np.uint8))
+
+
+def test_cuda_graph_replay_beside_its_capture_stream(cuda):
+    """A captured K1 launch owns its work counters and deferred list (graph
+    allocations, zeroed by a memset node at every replay), so replays on
+    another stream interleaved with new K1 work on the capturing stream each
+    simulate their whole batch.  (torch's blocking streams serialise the two
+    here; the separation is by construction, sgpu_sim.cu work_counters.)"""
+    cfg = CONFIGS["C2"]
+    n = 20000
+    a_graph = B.generate_traces(cfg.gen, 0, n, device=0)
+    a_live = B.generate_traces(dataclasses.replace(cfg.gen, seed=77), 0, n, device=0)
+    B.simulate_batch(a_graph, POLICIES, cfg.cap_mib)
+    torch.cuda.synchronize()
+    s, t = torch.cuda.Stream(), torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        res_g = B.simulate_batch(a_graph, POLICIES, cfg.cap_mib, stream=s)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        with torch.cuda.stream(t):
+            g.replay()
+        res_live = B.simulate_batch(a_live, POLICIES, cfg.cap_mib, stream=s)
+    torch.cuda.synchronize()
+    for apps_t, res in ((a_graph, res_g), (a_live, res_live)):
+        apps = apps_t.cpu().numpy().view(np.uint32)
+        for pi, pol in enumerate(res.policies):
+            _, e, sref = O.simulate_burst(apps, cfg.cap_mib, pol.value)
+            np.testing.assert_array_equal(res.ticks("end")[pi].reshape(e.shape), e)
+            np.testing.assert_array_equal(res.stats()[pi].view(np.uint8), sref.view(np.uint8))
