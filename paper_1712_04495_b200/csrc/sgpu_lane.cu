@@ -504,7 +504,8 @@ __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const
 }
 
 // Main pass (RETRY = false): every trace in order.  A trace whose 64-bit-key
-// lanes overflow their heap (kLaneHeapW events) is appended to P.retry.
+// lanes overflow their heap (kLaneHeapW events), or could (its staged
+// busy-app bound exceeds kLaneHeapW: meta[2] == 2), is appended to P.retry.
 // Retry pass: the traces of P.retry (count P.work[2]) with 64-bit keys and a
 // heap of kLaneHeapN events in a larger warp region.  Other failed lanes
 // (32-bit-key heap or wake FIFO full, staging limits) are re-run in-kernel
