@@ -628,13 +628,15 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, MB) trace_sim_lane_ke
 static inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
 
-// Lane path eligibility: T0 ticks mode, no event log, <= 256 apps per trace.
+// Lane path eligibility: T0 ticks mode, no event log, <= 256 apps per trace,
+// < 2^32 traces.
 // By default traces of <= 128 apps take it (measured on one B200: C4, 128
 // apps, 4 policies: 4.1e7 vs 1.4e7 trace-sims/s on the warp kernel);
 // 256-app traces are faster on the warp kernel (C3: 3.6e6 vs 1.3e6) unless
 // `forced`.
 bool lane_eligible(const SimParams& p, bool program_mode, bool f64, bool forced) {
     if (program_mode || f64 || p.events != nullptr || p.npol * p.ndev > 32) return false;
+    if (p.n_traces > 0xFFFFFFFFull) return false;  // deferred-trace ids are 32-bit
     if (forced) return p.n_pad <= 256u;
     // one simulation per 128-app trace leaves 7 of 8 lanes of a trace slot
     // idle: the warp kernel is faster there (C4 shape, 1 policy: 38-59 vs
