@@ -127,6 +127,26 @@ def test_golden_multidev(cuda):
         np.testing.assert_array_equal(st[pi]["unfinished"], ints[..., 2])
 
 
+@pytest.mark.parametrize("n,ndev,pols", [(128, 8, POLICIES), (100, 4, POLICIES), (128, 2, ("pmmu",)),
+                                          (40, 8, ("fifo", "pfifo")), (64, 3, POLICIES)])
+def test_multidev_lane_shapes(n, ndev, pols, cuda):
+    """Multi-device traces at the lane kernel's shape limits: 128 apps x 8
+    devices x 4 policies (32 lanes per trace, one trace per warp), 100 apps
+    over 4 devices, one policy on 2 devices, 8 devices x 2 policies, an odd
+    device count; random device per app, per-device capacities."""
+    rng = np.random.default_rng(300 + n + ndev)
+    nt = 400
+    apps = np.zeros((nt, n, 4), dtype=np.uint32)
+    apps[:, :, 0] = rng.integers(0, 3000, (nt, n))
+    apps[:, :, 1] = rng.integers(0, 700, (nt, n))
+    apps[:, :, 2] = rng.integers(0, 900, (nt, n))
+    prio = rng.integers(0, 4, (nt, n)).astype(np.uint32)
+    dev = rng.integers(0, ndev, (nt, n)).astype(np.uint32)
+    apps[:, :, 3] = prio | (dev << 8)
+    caps = tuple(int(c) for c in rng.integers(600, 2000, ndev))
+    check_against_oracle(apps, caps, cuda, policies=pols)
+
+
 # ------------------------------------------------------------ oracle, seeded
 
 @pytest.mark.parametrize("cname,nt", [("C2", 3000), ("C3", 300), ("C4", 2000), ("C5", 1500)])
