@@ -75,7 +75,7 @@ struct LaneParams {
     uint32_t cm_per_trace; // class-mask capacity of one trace slot
     uint32_t meta_stride;  // u16 per trace slot of the meta array
     // per-warp shared-memory layout (bytes)
-    uint32_t off_a, off_mem, off_bw, off_por, off_lt, off_tbl, off_cm, off_meta, off_fifo, off_fb,
+    uint32_t off_a, off_mem, off_bw, off_por, off_lt, off_tbl, off_cm, off_meta, off_fb,
         warp_bytes;
 };
 
@@ -496,7 +496,6 @@ __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const
     sim.s_cm = reinterpret_cast<const uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW) + c0 * NW;
     sim.ncls = c1 - c0;
     sim.heap = reinterpret_cast<typename LaneSim<K, NARROW, HW>::Key*>(ws + L.off_fb) + lane;
-    sim.fifo = reinterpret_cast<uint32_t*>(ws + L.off_fifo) + lane;
     sim.out_base = (uint64_t)pslot * P.n_apps_total + a0;
     if (!sim.run(na, s0, s1, z, policy, cap_d)) return false;
     sim.finish(((uint64_t)pslot * P.n_traces + t) * P.ndev + d, s1 - s0);
@@ -717,8 +716,6 @@ static void lane_layout(LaneParams& L, uint32_t heap_bytes) {
     o = align16(o + (L.need_cls ? L.G * (L.cm_per_trace * NW) * 8u : 0u));
     L.off_meta = o;
     o = align16(o + L.G * L.meta_stride * 2u);
-    L.off_fifo = o;
-    o = align16(o + kLaneFifoWords * 32u * 4u);
     L.off_fb = o;
     o = align16(o + fb);
     L.warp_bytes = max(o, align16(L.sp.warp_bytes));

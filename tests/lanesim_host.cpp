@@ -73,7 +73,6 @@ static void run_case(int n, uint32_t policy, uint32_t cap, const std::vector<uin
             for (uint32_t w = 0; w < NW; w++) s_t4[((r + 1) >> 2) * NW + w] = T[w];
     }
     std::vector<uint64_t> heap(32 * 32, 0);  // column 0 of the [slot][lane] layout
-    std::vector<uint32_t> fifo(32 * kLaneFifoWords, 0);
     std::vector<uint32_t> grant(n, SG_NEVER), end(n, SG_NEVER);
     SimParams P{grant.data(), end.data()};
     Sim sim(P);
@@ -89,7 +88,6 @@ static void run_case(int n, uint32_t policy, uint32_t cap, const std::vector<uin
     sim.s_cm = s_cm.data();
     sim.ncls = (uint32_t)pl.size();
     sim.heap = reinterpret_cast<typename Sim::Key*>(heap.data());
-    sim.fifo = fifo.data();
     sim.out_base = 0;
     if (!sim.run((uint32_t)n, 0, (uint32_t)n, z, policy, cap)) { printf("0\n"); return; }
     uint32_t unf = 0;
