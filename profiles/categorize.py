@@ -13,7 +13,7 @@ CSRC = "paper_1712_04495_b200/csrc/"
 MARKS = {
     "sgpu_lanesim.cuh": [
         (r"struct LaneKey", "keys/helpers"), (r"SG_HD void push\(", "heap push"), (r"SG_HD Key min_child\(", "heap pop"),
-        (r"SG_HD void pop\(", "heap pop"), (r"SG_HD uint8_t\* fifo_slot\(", "wake fifo"), (r"SG_HD void enqueue\(", "queue mask"),
+        (r"SG_HD void pop\(", "heap pop"), (r"SG_HD uint32_t fifo_get\(", "wake fifo"), (r"SG_HD void enqueue\(", "queue mask"),
         (r"SG_HD uint32_t fit_rank\(", "fit_rank/fit_set"), (r"SG_HD void grant_one\(", "grant (scan path)"),
         (r"SG_HD void init_round\(", "grant round init"), (r"SG_HD void grant_step\(", "grant step"),
         (r"SG_HD void end_round\(", "grant round end"), (r"SG_HD void grant_waiters_tbl\(", "grant round init"),
