@@ -82,11 +82,11 @@ struct LaneParams {
 // Per-trace-slot strides (in elements) of the shared arrays.  The u32
 // record arrays hold N entries + the s_mem[N] sentinel; an odd stride skews
 // the slots of a warp onto different banks.
-template <uint32_t N> struct SlotStride {
+template <uint32_t N, uint32_t FS> struct SlotStride {
     static constexpr uint32_t S32 = N + 1;          // u32 record arrays
     static constexpr uint32_t POR = N + 4;          // rank -> position (u8) + 4 sentinels
     static constexpr uint32_t LTB = kLtBuckets + 12;  // rank lookup: u8 buckets + 3 u32 params
-    static constexpr uint32_t T4 = (N / 4 + 1) * ((N + 63) / 64);  // fit table at every 4th rank (NW words)
+    static constexpr uint32_t T4 = (N / FS + 1) * ((N + 63) / 64);  // fit table (NW words per entry)
 };
 
 // meta per trace slot (u16), for ndev devices: [0] n, [1] fail (big times /
@@ -189,8 +189,8 @@ __device__ __forceinline__ uint32_t dev_scan_incl(uint32_t v, uint32_t lane) {
 
 // Stage trace t into slot g (scratch: the warp's fb region): SoA records in
 // (device, arrival, index) order, class masks of each device's priority
-// classes (highest first), the fit table.  Warp-collective.
-template <int K>
+// classes (highest first), the fit table (every FS-th rank).  Warp-collective.
+template <int K, uint32_t FS>
 __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, uint32_t g, uint64_t t,
                                             uint32_t lane) {
     const SimParams& P = L.sp;
@@ -200,7 +200,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
     uint32_t na;
     lane_trace_range(P, t, a0, na);
     uint4* raw = reinterpret_cast<uint4*>(ws + L.off_fb);
-    using SS = SlotStride<N>;
+    using SS = SlotStride<N, FS>;
     uint32_t* s_a = reinterpret_cast<uint32_t*>(ws + L.off_a) + g * SS::S32;
     uint32_t* s_mem = reinterpret_cast<uint32_t*>(ws + L.off_mem) + g * SS::S32;
     uint32_t* s_bw = reinterpret_cast<uint32_t*>(ws + L.off_bw) + g * SS::S32;
@@ -405,7 +405,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
                     if (lane >= (uint32_t)o) v |= u;
                 }
                 v |= carry[w];
-                if ((r & 3u) == 3u) s_t4[((r + 1) >> 2) * NW + w] = v;
+                if ((r + 1u) % FS == 0) s_t4[((r + 1) / FS) * NW + w] = v;
                 carry[w] = __shfl_sync(FULL, (uint32_t)v, 31) |
                            ((uint64_t)__shfl_sync(FULL, (uint32_t)(v >> 32), 31) << 32);
             }
@@ -467,21 +467,21 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
 // One lane's simulation of (trace t, device d, policy slot pslot) from the
 // staged slot g with a heap of HW 64-bit keys (or kLaneHeapN 32-bit keys).
 // Returns false if the lane must be re-run (retry pass / fallback).
-template <int K, bool NARROW, uint32_t HW = kLaneHeapW>
+template <int K, uint32_t FS, bool NARROW, uint32_t HW = kLaneHeapW>
 __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const uint16_t* meta, uint32_t g,
                                          uint32_t d, uint32_t pslot, uint32_t policy, uint32_t cap_d,
                                          uint64_t t, uint32_t lane) {
     const SimParams& P = L.sp;
     constexpr uint32_t N = 32u * K;
     constexpr uint32_t NW = (N + 63u) / 64u;
-    using SS = SlotStride<N>;
+    using SS = SlotStride<N, FS>;
     const uint32_t na = meta[0];
     const uint32_t ndev = P.ndev;
     const uint32_t s0 = meta[meta_dev(d)], s1 = meta[meta_dev(d + 1)], z = meta[meta_z(ndev, d)];
     uint64_t a0;
     uint32_t na_unused;
     lane_trace_range(P, t, a0, na_unused);
-    LaneSim<K, NARROW, HW> sim(P);
+    LaneSim<K, NARROW, HW, FS> sim(P);
     sim.s_a = reinterpret_cast<const uint32_t*>(ws + L.off_a) + g * SS::S32;
     sim.s_mem = reinterpret_cast<const uint32_t*>(ws + L.off_mem) + g * SS::S32;
     sim.s_bw = reinterpret_cast<const uint32_t*>(ws + L.off_bw) + g * SS::S32;
@@ -495,7 +495,7 @@ __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const
     if (L.need_cls) { c0 = meta[meta_cls(ndev, d)]; c1 = meta[meta_cls(ndev, d + 1)]; }
     sim.s_cm = reinterpret_cast<const uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW) + c0 * NW;
     sim.ncls = c1 - c0;
-    sim.heap = reinterpret_cast<typename LaneSim<K, NARROW, HW>::Key*>(ws + L.off_fb) + lane;
+    sim.heap = reinterpret_cast<typename LaneSim<K, NARROW, HW, FS>::Key*>(ws + L.off_fb) + lane;
     sim.out_base = (uint64_t)pslot * P.n_apps_total + a0;
     if (!sim.run(na, s0, s1, z, policy, cap_d)) return false;
     sim.finish(((uint64_t)pslot * P.n_traces + t) * P.ndev + d, s1 - s0);
@@ -509,7 +509,7 @@ __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const
 // heap of kLaneHeapN events in a larger warp region.  Other failed lanes
 // (32-bit-key heap or wake FIFO full, staging limits) are re-run in-kernel
 // by the warp-per-trace fallback.
-template <int K, bool RETRY, int MB>
+template <int K, bool RETRY, int MB, uint32_t FS>
 __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, MB) trace_sim_lane_kernel(const LaneParams L) {
     const SimParams& P = L.sp;
     extern __shared__ __align__(16) uint8_t smem[];
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, MB) trace_sim_lane_ke
         const uint64_t next = fetch();
         const uint64_t t0 = grp * L.G;
         const uint32_t gcount = (uint32_t)min((uint64_t)L.G, n_items - t0);
-        for (uint32_t s = 0; s < gcount; s++) stage_trace<K>(L, ws, s, trace_of(t0 + s), lane);
+        for (uint32_t s = 0; s < gcount; s++) stage_trace<K, FS>(L, ws, s, trace_of(t0 + s), lane);
         // warm L2 with the next group's records while this one simulates
         if (!RETRY && next < n_groups && !P.trace_offsets) {
             const uint64_t nt0 = next * L.G;
@@ -559,13 +559,13 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, MB) trace_sim_lane_ke
             if (meta[1])
                 fail = true;
             else if (RETRY)
-                fail = !lane_run<K, false, kLaneHeapN>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane);
+                fail = !lane_run<K, FS, false, kLaneHeapN>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane);
             else if (narrow)
-                fail = !lane_run<K, true>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane);
+                fail = !lane_run<K, FS, true>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane);
             else if (meta[2] == 2)
                 defer = true;
             else
-                defer = !lane_run<K, false>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane);
+                defer = !lane_run<K, FS, false>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane);
         }
         if (!RETRY) {
             // a trace with a failed lane goes to the retry pass whole: one
@@ -643,9 +643,9 @@ bool lane_eligible(const SimParams& p, bool program_mode, bool f64, bool forced)
     return p.n_pad <= 64u || (p.n_pad <= 128u && p.npol * p.ndev >= 2);
 }
 
-template <int K, bool RETRY, int MB>
+template <int K, bool RETRY, int MB, uint32_t FS>
 static cudaError_t launch_lane_t(LaneParams& L, cudaStream_t stream, int* grid_out) {
-    auto kern = trace_sim_lane_kernel<K, RETRY, MB>;
+    auto kern = trace_sim_lane_kernel<K, RETRY, MB, FS>;
     const uint32_t wpb = kLaneWarpsPerBlock;
     const size_t smem = (size_t)L.warp_bytes * wpb;
     if (smem > 227u * 1024u) return cudaErrorInvalidConfiguration;
@@ -672,32 +672,15 @@ static cudaError_t launch_lane_t(LaneParams& L, cudaStream_t stream, int* grid_o
     return cudaGetLastError();
 }
 
-template <int K>
-static cudaError_t launch_lane_k(LaneParams& L, LaneParams& R, cudaStream_t stream, int* grid_out) {
-    cudaError_t err;
-    // blocks per SM that shared memory allows (228 KB, 1 KB reserved per block)
-    const uint32_t smem_blocks = 233472u / (L.warp_bytes * kLaneWarpsPerBlock + 1024u);
-    if constexpr (K == 2) {
-        if (smem_blocks >= (uint32_t)kLaneHiBlocks2)
-            err = launch_lane_t<K, false, kLaneHiBlocks2>(L, stream, grid_out);
-        else
-            err = launch_lane_t<K, false, LaneMinBlocks<K>::v>(L, stream, grid_out);
-    } else {
-        err = launch_lane_t<K, false, LaneMinBlocks<K>::v>(L, stream, grid_out);
-    }
-    if (err == cudaSuccess) err = launch_lane_t<K, true, LaneMinBlocksR<K>::v>(R, stream, nullptr);
-    return err;
-}
-
 // Per-warp shared-memory layout of the lane kernel; `heap_bytes` is the
-// busy-end heap region of the warp's 32 lanes.
-static void lane_layout(LaneParams& L, uint32_t heap_bytes) {
+// busy-end heap region of the warp's 32 lanes, `fs` the fit-table stride.
+static void lane_layout(LaneParams& L, uint32_t heap_bytes, uint32_t fs) {
     const uint32_t N = L.sp.n_pad;
     const uint32_t NW = (N + 63u) / 64u;
     // the heaps and the staging scratch share one region; the fallback
     // TraceSim overlays the whole warp region once the group's lanes are done
     const uint32_t fb = max(heap_bytes, N * 16u);
-    const uint32_t S32 = N + 1, POR = N + 4, LTB = kLtBuckets + 12, T4 = (N / 4 + 1) * NW;  // SlotStride<N>
+    const uint32_t S32 = N + 1, POR = N + 4, LTB = kLtBuckets + 12, T4 = (N / fs + 1) * NW;  // SlotStride<N, fs>
     L.meta_stride = meta_u16(L.sp.ndev);
     uint32_t o = 0;
     L.off_a = o;
@@ -722,6 +705,33 @@ static void lane_layout(LaneParams& L, uint32_t heap_bytes) {
     if (const char* pad = getenv("SGPU_LANE_SMEM_PAD")) L.warp_bytes += align16((uint32_t)atoi(pad));  // occupancy experiments
 }
 
+// Main pass + retry pass.  The variant: at 64 apps with few traces per warp
+// (shared memory allows >= kLaneHiBlocks2 blocks with the 4-stride table)
+// the ten-block, 4-stride build; otherwise LaneMinBlocks with FitStride<K>.
+template <int K>
+static cudaError_t launch_lane_k(LaneParams& L, LaneParams& R, cudaStream_t stream, int* grid_out) {
+    const uint32_t HB = max(kLaneHeapN * 32u * 4u, kLaneHeapW * 32u * 8u);  // main pass heap region
+    const uint32_t HBR = kLaneHeapN * 32u * 8u;                          // retry pass: 64-bit keys
+    cudaError_t err;
+    if constexpr (K == 2) {
+        lane_layout(L, HB, 4u);
+        // blocks per SM that shared memory allows (228 KB, 1 KB reserved per block)
+        const uint32_t smem_blocks = 233472u / (L.warp_bytes * kLaneWarpsPerBlock + 1024u);
+        if (smem_blocks >= (uint32_t)kLaneHiBlocks2) {
+            lane_layout(R, HBR, 4u);
+            err = launch_lane_t<K, false, kLaneHiBlocks2, 4u>(L, stream, grid_out);
+            if (err == cudaSuccess) err = launch_lane_t<K, true, LaneMinBlocksR<K>::v, 4u>(R, stream, nullptr);
+            return err;
+        }
+    }
+    constexpr uint32_t FS = FitStride<K>::v;
+    lane_layout(L, HB, FS);
+    lane_layout(R, HBR, FS);
+    err = launch_lane_t<K, false, LaneMinBlocks<K>::v, FS>(L, stream, grid_out);
+    if (err == cudaSuccess) err = launch_lane_t<K, true, LaneMinBlocksR<K>::v, FS>(R, stream, nullptr);
+    return err;
+}
+
 cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_out) {
     if (p.n_traces > 0xFFFFFFFFull) return cudaErrorInvalidValue;  // 32-bit deferred-trace ids
     LaneParams L;
@@ -744,8 +754,6 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
     cudaError_t err = work_counters(stream, L.sp, p.n_traces, &owned);
     if (err != cudaSuccess) return err;
     LaneParams R = L;
-    lane_layout(L, max(kLaneHeapN * 32u * 4u, kLaneHeapW * 32u * 8u));
-    lane_layout(R, kLaneHeapN * 32u * 8u);
     switch (N / 32) {
         case 1: err = launch_lane_k<1>(L, R, stream, grid_out); break;
         case 2: err = launch_lane_k<2>(L, R, stream, grid_out); break;

@@ -34,6 +34,10 @@ namespace sg {
 constexpr uint32_t kLaneHeapN = 20;         // busy-end heap slots per lane: 4-ary, depth 2
 constexpr uint32_t kLaneHeapW = 10;         // the same 2.5 KB region with 64-bit keys (main pass)
 constexpr uint32_t kLaneFifo = 8;           // wake FIFO: 8 app positions, one byte each, in a u64 register
+// Fit table T[r] kept at every FS-th rank: every 2nd at <= 64 apps (one
+// extra position to OR in; fits C2's shared budget), every 4th above and in
+// the few-traces-per-warp variant (its staging is a larger share).
+template <int K> struct FitStride { static constexpr uint32_t v = K <= 2 ? 2u : 4u; };
 constexpr uint64_t kInf = ~0ull;
 constexpr uint32_t kLtBuckets = 128;        // rank-lookup buckets per trace
 constexpr uint32_t kBusyBits = 21;          // busy < 2^21 on this path; app index above it
@@ -81,7 +85,7 @@ template <int K, bool NARROW, uint32_t HW = kLaneHeapW> struct LaneKey {
     static SG_HD uint32_t c_base(uint32_t n) { return NARROW ? 32u * K : n << LOGN; }
 };
 
-template <int K, bool NARROW, uint32_t HW = kLaneHeapW>
+template <int K, bool NARROW, uint32_t HW = kLaneHeapW, uint32_t FSt = FitStride<K>::v>
 struct LaneSim {
     static constexpr uint32_t N = 32u * K;
     static constexpr uint32_t NW = (N + 63u) / 64u;  // queue mask words
@@ -98,7 +102,7 @@ struct LaneSim {
     const uint8_t* s_por;    // position of the r-th smallest request (N past the end)
     const uint8_t* s_lt;     // s_lt[j] = #requests in buckets < j
     uint32_t lt_lo, lt_hi, lt_scale;
-    const uint64_t* s_t4;    // T[4j] (NW words): positions of the 4j smallest requests
+    const uint64_t* s_t4;    // T[FS j] (NW words): positions of the FS j smallest requests
     const uint64_t* s_cm;    // class masks (NW words each) of this lane's device, top class first
     uint32_t ncls;
     // this lane's columns
@@ -220,18 +224,27 @@ struct LaneSim {
         while (s_mem[s_por[r]] <= budget) r += 1;  // s_mem[N] = ~0 ends the scan
         return r;
     }
-    // T[r]: positions of the r smallest requests = T[4 floor(r/4)] + up to 3
+    // T[r]: positions of the r smallest requests = T[FS floor(r/FS)] + the
+    // positions of the up to FS - 1 ranks after it
+    static constexpr uint32_t FS = FSt;
     SG_HD void fit_set(uint32_t r, uint64_t (&t)[NW]) const {
 #pragma unroll
-        for (uint32_t w = 0; w < NW; w++) t[w] = s_t4[(r >> 2) * NW + w];
-        const uint32_t pw = *reinterpret_cast<const uint32_t*>(s_por + (r & ~3u));
-        const uint32_t k = r & 3u;
-#pragma unroll
-        for (uint32_t j = 0; j < 3; j++) {
-            const uint32_t p = (pw >> (8u * j)) & 0xFFu;
+        for (uint32_t w = 0; w < NW; w++) t[w] = s_t4[(r / FS) * NW + w];
+        if constexpr (FS == 2) {
+            const uint32_t p = s_por[r & ~1u];
 #pragma unroll
             for (uint32_t w = 0; w < NW; w++)
-                if (k > j && (NW == 1 || w == (p >> 6))) t[w] |= 1ull << (p & 63u);
+                if ((r & 1u) && (NW == 1 || w == (p >> 6))) t[w] |= 1ull << (p & 63u);
+        } else {
+            const uint32_t pw = *reinterpret_cast<const uint32_t*>(s_por + (r & ~3u));
+            const uint32_t k = r & 3u;
+#pragma unroll
+            for (uint32_t j = 0; j < 3; j++) {
+                const uint32_t p = (pw >> (8u * j)) & 0xFFu;
+#pragma unroll
+                for (uint32_t w = 0; w < NW; w++)
+                    if (k > j && (NW == 1 || w == (p >> 6))) t[w] |= 1ull << (p & 63u);
+            }
         }
     }
     SG_HD void grant_one(uint32_t q, uint32_t m, uint32_t& budget, uint32_t& g) {

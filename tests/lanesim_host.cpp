@@ -22,7 +22,7 @@ static void run_case(int n, uint32_t policy, uint32_t cap, const std::vector<uin
                      const std::vector<uint32_t>& M, const std::vector<uint32_t>& Bz,
                      const std::vector<uint32_t>& Pr) {
     constexpr uint32_t N = 32u * K;
-    using Sim = LaneSim<K, NAR, HW>;
+    using Sim = LaneSim<K, NAR, HW>;  // fit table stride FitStride<K>
     constexpr uint32_t NW = Sim::NW;
     // arrival order: (arrival, index)
     std::vector<int> ord(n);
@@ -65,12 +65,13 @@ static void run_case(int n, uint32_t policy, uint32_t cap, const std::vector<uin
         while (r < (uint32_t)n && lt_bucket(s_mem[rk[r]] - mn, scale) + 1 <= j) r++;
         s_lt[j] = (uint8_t)r;
     }
-    std::vector<uint64_t> s_t4((N / 4 + 2) * NW, 0);
+    constexpr uint32_t FS = FitStride<K>::v;
+    std::vector<uint64_t> s_t4((N / FS + 2) * NW, 0);
     uint64_t T[NW] = {};
     for (uint32_t r = 0; r < N; r++) {
         if (r < (uint32_t)n) T[rk[r] >> 6] |= 1ull << (rk[r] & 63);
-        if ((r & 3) == 3)
-            for (uint32_t w = 0; w < NW; w++) s_t4[((r + 1) >> 2) * NW + w] = T[w];
+        if ((r + 1) % FS == 0)
+            for (uint32_t w = 0; w < NW; w++) s_t4[((r + 1) / FS) * NW + w] = T[w];
     }
     std::vector<uint64_t> heap(32 * 32, 0);  // column 0 of the [slot][lane] layout
     std::vector<uint32_t> grant(n, SG_NEVER), end(n, SG_NEVER);
