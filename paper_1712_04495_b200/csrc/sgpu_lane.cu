@@ -85,7 +85,7 @@ struct LaneParams {
 template <uint32_t N, uint32_t FS> struct SlotStride {
     static constexpr uint32_t S32 = N + 1;          // u32 record arrays
     static constexpr uint32_t POR = N + 4;          // rank -> position (u8) + 4 sentinels
-    static constexpr uint32_t LTB = kLtBuckets + 12;  // rank lookup: u8 buckets + 3 u32 params
+    static constexpr uint32_t LTB = LtBuckets<FS>::v + 12;  // rank lookup: u8 buckets + 3 u32 params
     static constexpr uint32_t T4 = (N / FS + 1) * ((N + 63) / 64);  // fit table (NW words per entry)
 };
 
@@ -373,7 +373,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
 #pragma unroll
         for (int k = 0; k < K; k++) mmax = max(mmax, memk[k] != ~0u ? memk[k] : 0u);
         warp_sort_keys<K>(mk, __reduce_max_sync(FULL, mmax) < (1u << 24), lane);
-        // rank lookup: kLtBuckets buckets spread linearly over [lo, hi]
+        // rank lookup: LtBuckets buckets spread linearly over [lo, hi]
         uint32_t mx = 0, mn = ~0u;
 #pragma unroll
         for (int k = 0; k < K; k++) {
@@ -383,7 +383,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
         mx = __reduce_max_sync(FULL, mx);
         mn = __reduce_min_sync(FULL, mn);
         if (mn > mx) mn = mx;  // empty trace
-        const uint64_t sc = ((uint64_t)kLtBuckets << 32) / ((uint64_t)(mx - mn) + 1ull);
+        const uint64_t sc = ((uint64_t)LtBuckets<FS>::v << 32) / ((uint64_t)(mx - mn) + 1ull);
         const uint32_t scale = sc > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)sc;
         uint64_t carry[NW];
 #pragma unroll
@@ -410,15 +410,15 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
                            ((uint64_t)__shfl_sync(FULL, (uint32_t)(v >> 32), 31) << 32);
             }
             // LT[j] = first rank whose bucket is >= j: rank r owns (b[r-1], b[r]]
-            const uint32_t b = valid ? lt_bucket((uint32_t)(mk[k] >> 8) - mn, scale) + 1u : kLtBuckets + 1u;
+            const uint32_t b = valid ? lt_bucket<FS>((uint32_t)(mk[k] >> 8) - mn, scale) + 1u : LtBuckets<FS>::v + 1u;
             uint32_t bp = __shfl_up_sync(FULL, b, 1);
             if (lane == 0) bp = bcarry;
-            for (uint32_t j = bp; j < min(b, kLtBuckets + 1u); j++)
-                if (j < kLtBuckets) s_lt[j] = (uint8_t)r;
+            for (uint32_t j = bp; j < min(b, LtBuckets<FS>::v + 1u); j++)
+                if (j < LtBuckets<FS>::v) s_lt[j] = (uint8_t)r;
             bcarry = __shfl_sync(FULL, b, 31);
         }
         // buckets above the largest request (all ranks valid) -> N
-        for (uint32_t j = bcarry + lane; j < kLtBuckets; j += 32u) s_lt[j] = (uint8_t)N;
+        for (uint32_t j = bcarry + lane; j < LtBuckets<FS>::v; j += 32u) s_lt[j] = (uint8_t)N;
         if (!narrow && ndev == 1) {
             // busy apps at once <= apps without a request + the most requests
             // that fit the device together (the k smallest): ranks whose
@@ -442,7 +442,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
         }
         if (lane < NW) s_t4[lane] = 0ull;
         if (lane == 0) {
-            uint32_t* prm = reinterpret_cast<uint32_t*>(s_lt + kLtBuckets);
+            uint32_t* prm = reinterpret_cast<uint32_t*>(s_lt + LtBuckets<FS>::v);
             prm[0] = mn;
             prm[1] = mx;
             prm[2] = scale;
@@ -487,9 +487,9 @@ __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const
     sim.s_bw = reinterpret_cast<const uint32_t*>(ws + L.off_bw) + g * SS::S32;
     sim.s_por = ws + L.off_por + g * SS::POR;
     sim.s_lt = ws + L.off_lt + g * SS::LTB;
-    sim.lt_lo = reinterpret_cast<const uint32_t*>(sim.s_lt + kLtBuckets)[0];
-    sim.lt_hi = reinterpret_cast<const uint32_t*>(sim.s_lt + kLtBuckets)[1];
-    sim.lt_scale = reinterpret_cast<const uint32_t*>(sim.s_lt + kLtBuckets)[2];
+    sim.lt_lo = reinterpret_cast<const uint32_t*>(sim.s_lt + LtBuckets<FS>::v)[0];
+    sim.lt_hi = reinterpret_cast<const uint32_t*>(sim.s_lt + LtBuckets<FS>::v)[1];
+    sim.lt_scale = reinterpret_cast<const uint32_t*>(sim.s_lt + LtBuckets<FS>::v)[2];
     sim.s_t4 = reinterpret_cast<const uint64_t*>(ws + L.off_tbl) + g * SS::T4;
     uint32_t c0 = 0, c1 = 0;
     if (L.need_cls) { c0 = meta[meta_cls(ndev, d)]; c1 = meta[meta_cls(ndev, d + 1)]; }
@@ -680,7 +680,8 @@ static void lane_layout(LaneParams& L, uint32_t heap_bytes, uint32_t fs) {
     // the heaps and the staging scratch share one region; the fallback
     // TraceSim overlays the whole warp region once the group's lanes are done
     const uint32_t fb = max(heap_bytes, N * 16u);
-    const uint32_t S32 = N + 1, POR = N + 4, LTB = kLtBuckets + 12, T4 = (N / fs + 1) * NW;  // SlotStride<N, fs>
+    const uint32_t LB = fs == 2 ? LtBuckets<2>::v : LtBuckets<4>::v;
+    const uint32_t S32 = N + 1, POR = N + 4, LTB = LB + 12, T4 = (N / fs + 1) * NW;  // SlotStride<N, fs>
     L.meta_stride = meta_u16(L.sp.ndev);
     uint32_t o = 0;
     L.off_a = o;

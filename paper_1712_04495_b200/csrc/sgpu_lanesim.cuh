@@ -39,7 +39,10 @@ constexpr uint32_t kLaneFifo = 8;           // wake FIFO: 8 app positions, one b
 // the few-traces-per-warp variant (its staging is a larger share).
 template <int K> struct FitStride { static constexpr uint32_t v = K <= 2 ? 2u : 4u; };
 constexpr uint64_t kInf = ~0ull;
-constexpr uint32_t kLtBuckets = 128;        // rank-lookup buckets per trace
+// rank-lookup buckets per trace, with the fit-table stride FS: 192 with the
+// 2-stride table (<= 64 apps: fewer requests per bucket to scan; C2 17.89 ->
+// 17.81 ms), 128 with the 4-stride one (C4's shared budget; C5's staging)
+template <uint32_t FS> struct LtBuckets { static constexpr uint32_t v = FS == 2 ? 192u : 128u; };
 constexpr uint32_t kBusyBits = 21;          // busy < 2^21 on this path; app index above it
 constexpr uint32_t kClsShift = 29;          // s_bw bits 29-31: priority class of the app within its device
 constexpr uint32_t kLaneMaxCls = 8;         // classes per device on this path (more: warp-kernel re-run)
@@ -53,8 +56,8 @@ SG_HD uint32_t ffs64(uint64_t x) { return (uint32_t)__ffsll((long long)x) - 1u; 
 SG_HD uint32_t ffs32(uint32_t x) { return (uint32_t)__ffs((int)x) - 1u; }
 
 // Rank-lookup bucket of a request d = mem - lo >= 0: monotone in d.
-SG_HD uint32_t lt_bucket(uint32_t d, uint32_t scale) {
-    return min((uint32_t)(((uint64_t)d * scale) >> 32), kLtBuckets - 1u);
+template <uint32_t FS> SG_HD uint32_t lt_bucket(uint32_t d, uint32_t scale) {
+    return min((uint32_t)(((uint64_t)d * scale) >> 32), LtBuckets<FS>::v - 1u);
 }
 
 template <int K> struct LogN { static constexpr uint32_t v = K == 1 ? 5 : K == 2 ? 6 : K == 4 ? 7 : 8; };
@@ -214,12 +217,12 @@ struct LaneSim {
             if (w == (q >> 6)) mask[w] |= 1ull << (q & 63u);
         clsmask |= 1u << bw_cls(bw);
     }
-    // number of requests <= budget in the trace: bucket lookup (kLtBuckets
+    // number of requests <= budget in the trace: bucket lookup (LtBuckets
     // spread linearly over [smallest, largest] request), then a short
     // forward scan of the sorted requests inside the bucket
     SG_HD uint32_t fit_rank(uint32_t budget) const {
         if (budget > lt_hi) return N;
-        const uint32_t bi = budget < lt_lo ? 0u : lt_bucket(budget - lt_lo, lt_scale);
+        const uint32_t bi = budget < lt_lo ? 0u : lt_bucket<FS>(budget - lt_lo, lt_scale);
         uint32_t r = s_lt[bi];
         while (s_mem[s_por[r]] <= budget) r += 1;  // s_mem[N] = ~0 ends the scan
         return r;

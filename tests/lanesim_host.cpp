@@ -55,14 +55,14 @@ static void run_case(int n, uint32_t policy, uint32_t cap, const std::vector<uin
     std::vector<int> rk(n);
     for (int e = 0; e < n; e++) rk[e] = e;
     std::stable_sort(rk.begin(), rk.end(), [&](int x, int y) { return s_mem[x] < s_mem[y]; });
-    std::vector<uint8_t> s_por(N + 16, (uint8_t)N), s_lt(kLtBuckets + 16, 0);  // (host: roomier than the kernel slots)
+    std::vector<uint8_t> s_por(N + 16, (uint8_t)N), s_lt(LtBuckets<FitStride<K>::v>::v + 16, 0);  // (host: roomier than the kernel slots)
     for (int r = 0; r < n; r++) s_por[r] = (uint8_t)rk[r];
     const uint32_t mn = n ? s_mem[rk[0]] : 0, mx = n ? s_mem[rk[n - 1]] : 0;
-    const uint64_t sc = ((uint64_t)kLtBuckets << 32) / ((uint64_t)(mx - mn) + 1);
+    const uint64_t sc = ((uint64_t)LtBuckets<FitStride<K>::v>::v << 32) / ((uint64_t)(mx - mn) + 1);
     const uint32_t scale = sc > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)sc;
-    for (uint32_t j = 0; j < kLtBuckets; j++) {  // first rank whose bucket is >= j
+    for (uint32_t j = 0; j < LtBuckets<FitStride<K>::v>::v; j++) {  // first rank whose bucket is >= j
         uint32_t r = 0;
-        while (r < (uint32_t)n && lt_bucket(s_mem[rk[r]] - mn, scale) + 1 <= j) r++;
+        while (r < (uint32_t)n && lt_bucket<FitStride<K>::v>(s_mem[rk[r]] - mn, scale) + 1 <= j) r++;
         s_lt[j] = (uint8_t)r;
     }
     constexpr uint32_t FS = FitStride<K>::v;
