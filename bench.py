@@ -4,11 +4,15 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
 
+`--gpus N` without a launcher (WORLD_SIZE unset) re-executes itself under
+torch.distributed.run with N ranks (one process per GPU, NCCL), so both
+launch forms measure N GPUs.
+
 A "step" simulates the configuration's whole per-GPU trace batch (default C2:
 1M traces x 64 apps) under every policy of the configuration (C2: all four),
 i.e. one K1 trace_sim (on the lane engine: the main launch + the 64-bit-key
 retry launch, which finds nothing to do on C2) + one K2 stats_reduce (+ the
-cross-GPU aggregate all-reduce for N > 1).  The unit is one trace simulated under one
+cross-GPU aggregate all-gather for N > 1).  The unit is one trace simulated under one
 policy.  Scaling is weak: every rank simulates its own contiguous trace-id
 shard of the configured size, generated on its GPU before timing.
 
@@ -244,6 +248,32 @@ def measured_traffic(config, traces_per_gpu):
     return int(t["dram_bytes_read"]) + int(t["dram_bytes_write"]), t.get("issue_active_pct")
 
 
+def cpu_model() -> str:
+    """lscpu's model name (reported with every CPU number)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or platform.machine()
+
+
+def relaunch_distributed(args) -> int:
+    """--gpus N > 1 outside a launcher: run this script as N ranks under
+    torch.distributed.run (127.0.0.1 rendezvous); rank 0 prints the line."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -285,8 +315,7 @@ def run_reference_arm(args, ws, rank):
                          "sample": f"{totals} trace-policy simulations of {args.config} "
                                    f"(memshare.harness.simulate, {args.steps} steps of "
                                    f"~{budget:.1f} s on {cores} processes)",
-                         "cpu": platform.processor() or platform.machine(),
-                         "python": platform.python_version()},
+                         "cpu": cpu_model(), "python": platform.python_version()},
         "e2e": {"value": value, "unit": "traces/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -321,6 +350,8 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: check the multi-rank flow with several ranks on one GPU")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(args)
     ws, rank, local = dist_env()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -426,8 +457,10 @@ def main():
     ms_per_step = elapsed_ms / args.steps
 
     # roofline of K1: algorithmic bytes per launch / mean launch duration
+    # (16 B/app in; per policy 8 B/app grant + end and, per (trace, device),
+    # the 32 B record + 16 B percentages + 8 B speed-up out)
     in_b = n * napp * 16
-    out_b = n * npol * (napp * 8 + cfg.ndev * (32 + 16))
+    out_b = n * npol * (napp * 8 + cfg.ndev * (32 + 16 + 8))
     alg_bytes = in_b + out_b
     mean_k = statistics.mean(kern_ms) / 1000.0
     peak, peak_src = hbm_peak()
@@ -471,14 +504,15 @@ def main():
                    "sample": f"{tot} trace-policy simulations of {args.config} traces "
                              f"[10M, ...) in {wall:.1f} s: memshare.harness.simulate "
                              f"(oracle/_ref) on {cores} processes",
-                   "python": platform.python_version()}
+                   "cpu": cpu_model(), "python": platform.python_version()}
         except Exception as exc:  # pragma: no cover - reported, not fatal
             cpu = {"value": None, "unit": "traces/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {exc!r}"}
         try:
             pr, pdt = cpu_port_rate(args.config, 20_000 if napp <= 64 else 5_000)
             cpu["port"] = {"value": pr, "unit": "traces/s", "cores": os.cpu_count(),
-                           "kind": "port", "sample": f"oracle/ C restatement, OpenMP, {pdt:.1f} s"}
+                           "kind": "port", "sample": f"oracle/ C restatement, OpenMP, {pdt:.1f} s",
+                           "cpu": cpu_model()}
         except Exception as exc:  # pragma: no cover
             cpu["port"] = {"value": None, "sample": f"unavailable: {exc!r}"}
 
@@ -498,6 +532,10 @@ def main():
                          "traffic_source": TRAFFIC_SOURCE if traffic else None, "peak_source": peak_src,
                          "kernel": k1_kernel, "alg_bytes_per_launch": alg_bytes,
                          "mean_launch_ms": mean_k * 1000.0,
+                         # outputs only (the inputs are generated on the device
+                         # before timing)
+                         "alg_bytes_outputs_only": out_b,
+                         "frac_outputs_only": out_b / mean_k / 1e9 / peak,
                          # what bounds this kernel instead: issue slots (the ncu capture above)
                          "issue_active_frac": issue_pct / 100.0 if issue_pct else None},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,

@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define SG_ABI_VERSION 1
+#define SG_ABI_VERSION 2
 
 /* Largest trace (apps per trace) one warp simulates. */
 #define SG_MAX_APPS 1024
@@ -70,7 +70,10 @@ enum sg_event_kind {
 /* Per-trace status bits (sg_trace_stats.status). */
 #define SG_ST_TICK_OVERFLOW   0x1u  /* an event time exceeded 2^32-2 ticks   */
 #define SG_ST_COUNTER_OVERFLOW 0x2u /* more than 2^22 heap pushes            */
-#define SG_ST_BAD_DEVICE      0x4u  /* app device index >= ndev              */
+#define SG_ST_BAD_DEVICE      0x4u  /* ndev > 1 and an app of the trace has a
+                                       device index >= ndev (it is simulated
+                                       on device 0); set on every record of
+                                       the trace                           */
 #define SG_ST_EVENT_OVERFLOW  0x8u  /* event log capacity exceeded           */
 #define SG_ST_ZERO_SPAN_LEVEL 0x10u /* T == 0 with memory still held: the
                                        reference integrates level * 1e-9 s;
@@ -119,6 +122,12 @@ typedef struct sg_batch {
     uint32_t cap_mib[SG_MAX_DEV];
     uint32_t time_mode;         /* sg_time_mode (F64 requires steps)         */
     int32_t tick_log2;          /* seconds per tick = 2^-tick_log2           */
+    /* With trace_offsets: the per-policy stride of grant/end, at least
+     * trace_offsets[n_traces] - trace_offsets[0] (the batch's app count).
+     * Passed by the caller so the call never reads device memory on the
+     * host: it stays asynchronous and graph-capturable.  Ignored without
+     * trace_offsets (the stride is then n_traces * apps_per_trace). */
+    uint64_t apps_total;
 } sg_batch;
 
 /* Per-(policy, trace, device) statistics, ticks mode, 32 B. */
@@ -171,6 +180,14 @@ typedef struct sg_out {
     uint32_t* event_counts;
     uint32_t events_per_trace;
     uint32_t reserved;
+    /* Optional per (policy, trace, device) speed-up vs sequential execution
+     * (ticks mode; NaN in F64 mode and for an empty sub-trace):
+     *   sum over apps of (cpu + busy) * time_scale / makespan_ms
+     * in the reference's float order (AppProfile.total_ms(),
+     * memshare/harness.py:61-62; pkg/tests/test_harness.py:119-126), i.e.
+     * (S * 1000 * 2^-tick_log2) / (max(T * 2^-tick_log2, 1e-9) * 1000) with
+     * S = sum of the sub-trace's cpu and busy ticks and T its makespan. */
+    double* speedup;
 } sg_out;
 
 #define SG_NEVER 0xFFFFFFFFu
@@ -219,7 +236,8 @@ typedef struct sg_gen_params {
 int sg_abi_version(void);
 const char* sg_last_error(void);
 
-/* Number of SMs and resident warps per SM the simulator will use. */
+/* Number of SMs, and resident warps per SM of the default K1 engine for a
+ * C2-shaped batch (64-app T0 traces, four policies, one device). */
 int sg_device_info(int cuda_device, int* sm_count, int* warps_per_sm);
 
 /* Device-pointer batch simulation (async on stream). */

@@ -136,3 +136,35 @@ def pct_from_stats(stats: np.ndarray, cap_mib, tick_log2: int = 10):
     busy_s = stats["busy"].astype(np.float64) * scale
     dev_pct = (100.0 * busy_s) / makespan_s
     return makespan_s * 1000.0, mem_pct, dev_pct
+
+
+def seq_ticks(apps: np.ndarray, ndev: int = 1) -> np.ndarray:
+    """Sequential makespan in ticks per (trace, device) of T0 traces:
+    sum of arrival + busy over the device's apps (AppProfile.total_ms() of
+    [Phase(cpu_ms=a), Phase(alloc, busy_ms=b, free)], harness.py:61-62).
+    Devices out of range count as device 0."""
+    a = np.ascontiguousarray(apps)
+    if a.dtype != np.uint32:
+        a = a.view(np.uint32).reshape(a.shape + (4,))
+    per_app = a[..., 0].astype(np.uint64) + a[..., 2].astype(np.uint64)
+    if ndev == 1:
+        return per_app.sum(axis=1, dtype=np.uint64)[:, None]
+    dev = (a[..., 3] >> 8) & 0xFF
+    dev = np.where(dev < ndev, dev, 0)
+    return np.stack([np.where(dev == d, per_app, 0).sum(axis=1, dtype=np.uint64)
+                     for d in range(ndev)], axis=1)
+
+
+def speedup_from(seq: np.ndarray, makespan: np.ndarray, napps: np.ndarray,
+                 tick_log2: int = 10) -> np.ndarray:
+    """Speed-up vs sequential, the reference's float order with cpu/busy ms =
+    ticks and time_scale = 1000 * 2^-tick_log2 (pkg/tests/test_harness.py:
+    119-126): (S * time_scale) / (max(T * 2^-tick_log2, 1e-9) * 1000.0);
+    NaN for an empty (sub-)trace."""
+    scale = 2.0 ** -tick_log2
+    seq_ms = np.asarray(seq, dtype=np.uint64).astype(np.float64) * (1000.0 * scale)
+    T = np.asarray(makespan)
+    span = np.where(T > 0, T.astype(np.float64) * scale, 1e-9)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        sp = seq_ms / (span * 1000.0)
+    return np.where(np.asarray(napps) > 0, sp, np.nan)

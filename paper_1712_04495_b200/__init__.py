@@ -19,7 +19,7 @@ from .device import MIB, DeviceSpec, load_device_spec, parse_device_config
 from .errors import MemshareError, ParseError, SchemaError, SgpuError, SgpuUnavailable
 from .policy import PolicyKind, select_grants, select_grants_batch
 from .harness import (AppProfile, DEFAULT_DEVICE, MetricsReport, Phase, TICK_MS, WorkloadSpec,
-                      builtin_profiles, simulate)
+                      builtin_profiles, sequential_ms, simulate, speedup_vs_sequential)
 from .batch import (BatchResult, HostBuffers, generate_traces, reduce_stats, simulate_batch,
                     simulate_batch_host)
 from .tracegen import CONFIGS, GenParams, generate
@@ -29,7 +29,7 @@ __all__ = [
     "MemshareError", "ParseError", "SchemaError", "SgpuError", "SgpuUnavailable",
     "PolicyKind", "select_grants", "select_grants_batch",
     "AppProfile", "DEFAULT_DEVICE", "MetricsReport", "Phase", "TICK_MS", "WorkloadSpec",
-    "builtin_profiles", "simulate",
+    "builtin_profiles", "simulate", "sequential_ms", "speedup_vs_sequential",
     "BatchResult", "HostBuffers", "generate_traces", "reduce_stats", "simulate_batch",
     "simulate_batch_host", "CONFIGS", "GenParams", "generate",
 ]

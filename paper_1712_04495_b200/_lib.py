@@ -17,7 +17,7 @@ from .errors import SgpuError, SgpuUnavailable
 HERE = os.path.dirname(os.path.abspath(__file__))
 # SGPU_LIB: developer override (A/B builds of the same ABI); default in-tree
 LIB_PATH = os.environ.get("SGPU_LIB") or os.path.join(HERE, "libsgpu.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 MAX_APPS = 1024
 MAX_DEV = 8
 
@@ -47,13 +47,13 @@ class SgBatch(ctypes.Structure):
     _fields_ = [("n_traces", U64), ("trace_offsets", P), ("apps_per_trace", U32),
                 ("max_apps", U32), ("apps", P), ("steps", P), ("step_offsets", P),
                 ("policy_mask", U32), ("ndev", U32), ("cap_mib", U32 * MAX_DEV),
-                ("time_mode", U32), ("tick_log2", ctypes.c_int32)]
+                ("time_mode", U32), ("tick_log2", ctypes.c_int32), ("apps_total", U64)]
 
 
 class SgOut(ctypes.Structure):
     _fields_ = [("grant", P), ("end", P), ("stats", P), ("mem_pct", P), ("dev_pct", P),
                 ("events", P), ("event_counts", P), ("events_per_trace", U32),
-                ("reserved", U32)]
+                ("reserved", U32), ("speedup", P)]
 
 
 class SgGenParams(ctypes.Structure):

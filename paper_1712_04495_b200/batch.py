@@ -16,6 +16,10 @@ Layouts (include/sgpu.h):
   grant/end   (n_policies, total_apps) uint32 ticks (0xFFFFFFFF = never)
   stats       (n_policies, n_traces, ndev) STATS_DTYPE records (32 B)
   mem/dev pct (n_policies, n_traces, ndev) float64, reference op order
+  speedup     (n_policies, n_traces, ndev) float64: sequential / concurrent
+              makespan, sum(total_ms) * time_scale / makespan_ms in the
+              reference's float order (harness.py:61-62,
+              pkg/tests/test_harness.py:119-126), ticks mode
 """
 
 from __future__ import annotations
@@ -82,6 +86,7 @@ class BatchResult:
     dev_pct: object
     events: object = None  # (npol, n_traces, events_per_trace, 4) int32 or None
     event_counts: object = None
+    speedup: object = None  # (npol, n_traces, ndev) float64 or None
 
     def stats(self) -> np.ndarray:
         """Per-(policy, trace, device) statistics as a numpy structured array."""
@@ -102,14 +107,17 @@ def simulate_batch(apps, policies: Iterable = ("fifo",), cap_mib=184_320, *,
                    trace_offsets=None, max_apps: Optional[int] = None,
                    steps=None, step_offsets=None, time_mode: int = _lib.TIME_TICKS,
                    tick_log2: int = 10, want_ticks: bool = True, want_pct: bool = True,
-                   events_per_trace: int = 0, stream=None) -> BatchResult:
+                   want_speedup: bool = True, events_per_trace: int = 0,
+                   apps_total: Optional[int] = None, stream=None) -> BatchResult:
     """Simulate every trace under every requested policy on the GPU.
 
     apps: CUDA int32/uint32 tensor (n_traces, n_apps, 4), or (total_apps, 4)
     with `trace_offsets` (CUDA int64, n_traces + 1).  In step-program mode
     `steps` (CUDA int32 (n_steps, 4) = STEP_DTYPE records) and
     `step_offsets` (CUDA int32, total_apps + 1) define each app's program;
-    apps[..., 3] still carries prio | device << 8.
+    apps[..., 3] still carries prio | device << 8.  With `trace_offsets`,
+    `apps_total` (= offsets[-1] - offsets[0]) and `max_apps` avoid a device
+    read on the host; the call is then asynchronous and graph-capturable.
     """
     torch = _torch()
     L = _lib.lib()
@@ -130,7 +138,9 @@ def simulate_batch(apps, policies: Iterable = ("fifo",), cap_mib=184_320, *,
         if trace_offsets.dtype != torch.int64:
             raise ValueError("trace_offsets must be int64")
         n_traces = int(trace_offsets.numel()) - 1
-        total_apps = int(apps.shape[0])
+        total_apps = int(apps.shape[0]) if apps_total is None else int(apps_total)
+        if total_apps > int(apps.shape[0]):
+            raise ValueError("apps_total exceeds the apps tensor")
         if max_apps is None:
             max_apps = int((trace_offsets[1:] - trace_offsets[:-1]).max().item()) if n_traces else 0
         napp = 0
@@ -148,9 +158,11 @@ def simulate_batch(apps, policies: Iterable = ("fifo",), cap_mib=184_320, *,
     stats = torch.empty((npol, n_traces, ndev, rec_words), dtype=torch.int32, device=dev)
     mem_pct = torch.empty((npol, n_traces, ndev), dtype=torch.float64, device=dev) if want_pct else None
     dev_pct = torch.empty_like(mem_pct) if want_pct else None
+    speedup = torch.empty((npol, n_traces, ndev), dtype=torch.float64, device=dev) if want_speedup else None
     events = counts = None
     if events_per_trace:
-        events = torch.empty((npol, n_traces, events_per_trace, 4), dtype=torch.int32, device=dev)
+        # zeroed: readers copy whole slices, of which the log fills event_counts
+        events = torch.zeros((npol, n_traces, events_per_trace, 4), dtype=torch.int32, device=dev)
         counts = torch.empty((npol, n_traces), dtype=torch.int32, device=dev)
 
     b = _lib.SgBatch()
@@ -167,9 +179,11 @@ def simulate_batch(apps, policies: Iterable = ("fifo",), cap_mib=184_320, *,
         b.cap_mib[i] = c
     b.time_mode = time_mode
     b.tick_log2 = tick_log2
+    b.apps_total = total_apps
     o = _lib.SgOut()
     o.grant, o.end, o.stats = _vp(grant), _vp(end), _vp(stats)
     o.mem_pct, o.dev_pct = _vp(mem_pct), _vp(dev_pct)
+    o.speedup = _vp(speedup)
     o.events, o.event_counts = _vp(events), _vp(counts)
     o.events_per_trace = events_per_trace
     if stream is None:
@@ -178,7 +192,7 @@ def simulate_batch(apps, policies: Iterable = ("fifo",), cap_mib=184_320, *,
         rc = L.sg_simulate_batch(ctypes.byref(b), ctypes.byref(o), ctypes.c_void_p(stream.cuda_stream))
     _lib.check(rc, "sg_simulate_batch")
     return BatchResult(ordered, n_traces, ndev, caps, time_mode, tick_log2, grant, end, stats,
-                       mem_pct, dev_pct, events, counts)
+                       mem_pct, dev_pct, events, counts, speedup)
 
 
 @dataclass
@@ -189,17 +203,15 @@ class HostResult:
     stats: np.ndarray             # (npol, n_traces, ndev) STATS_DTYPE
     mem_pct: Optional[np.ndarray]
     dev_pct: Optional[np.ndarray]
-
-    @property
-    def h2d_bytes(self) -> int:
-        return 0
+    speedup: Optional[np.ndarray] = None
+    h2d_bytes: int = 0            # input bytes the call copied host -> device
 
 
 class HostBuffers:
     """Pinned host output buffers for repeated simulate_batch_host calls."""
 
     def __init__(self, npol: int, n_traces: int, n_apps: int, ndev: int,
-                 want_ticks: bool = True, want_pct: bool = True):
+                 want_ticks: bool = True, want_pct: bool = True, want_speedup: bool = True):
         torch = _torch()
         pin = torch.cuda.is_available()
 
@@ -212,6 +224,7 @@ class HostBuffers:
             npol, n_traces, ndev)
         self.mem_pct = alloc((npol, n_traces, ndev), torch.float64) if want_pct else None
         self.dev_pct = alloc((npol, n_traces, ndev), torch.float64) if want_pct else None
+        self.speedup = alloc((npol, n_traces, ndev), torch.float64) if want_speedup else None
 
     def d2h_bytes(self) -> int:
         """Bytes the host pipeline copies device -> host per call.  With both
@@ -219,7 +232,8 @@ class HostBuffers:
         ticks and the inputs (grant = end - busy) and cross no bus
         (sg_simulate_batch_host, csrc/sgpu_abi.cu; SGPU_GRANT_DMA=k copies the
         first k policies' grants instead, there and here)."""
-        n = sum(a.nbytes for a in (self.end, self.stats, self.mem_pct, self.dev_pct) if a is not None)
+        n = sum(a.nbytes for a in (self.end, self.stats, self.mem_pct, self.dev_pct, self.speedup)
+                if a is not None)
         if self.grant is not None:
             npol = self.grant.shape[0]
             n_dma = npol
@@ -241,8 +255,8 @@ def pinned_apps(n_traces: int, n_apps: int) -> np.ndarray:
 
 def simulate_batch_host(apps: np.ndarray, policies: Iterable = ("fifo",), cap_mib=184_320, *,
                         device: int = 0, chunk_traces: int = 0, want_ticks: bool = True,
-                        want_pct: bool = True, out: Optional[HostBuffers] = None,
-                        tick_log2: int = 10) -> HostResult:
+                        want_pct: bool = True, want_speedup: bool = True,
+                        out: Optional[HostBuffers] = None, tick_log2: int = 10) -> HostResult:
     """Host-buffer simulation through the C ABI pipeline (sg_simulate_batch_host).
     apps: (n_traces, n_apps, 4) uint32 (pinned memory gives full copy speed)."""
     L = _lib.lib()
@@ -257,7 +271,8 @@ def simulate_batch_host(apps: np.ndarray, policies: Iterable = ("fifo",), cap_mi
     caps = _caps(cap_mib)
     n_traces, napp = a.shape[0], a.shape[1]
     if out is None:
-        out = HostBuffers(len(ordered), n_traces, napp, len(caps), want_ticks, want_pct)
+        out = HostBuffers(len(ordered), n_traces, napp, len(caps), want_ticks, want_pct, want_speedup)
+    want_speedup = want_speedup and out.speedup is not None
     b = _lib.SgBatch()
     b.n_traces = n_traces
     b.apps_per_trace = napp
@@ -277,10 +292,12 @@ def simulate_batch_host(apps: np.ndarray, policies: Iterable = ("fifo",), cap_mi
     o.grant, o.end, o.stats = p(out.grant if want_ticks else None), p(out.end if want_ticks else None), p(out.stats)
     o.mem_pct = p(out.mem_pct if want_pct else None)
     o.dev_pct = p(out.dev_pct if want_pct else None)
+    o.speedup = p(out.speedup if want_speedup else None)
     rc = L.sg_simulate_batch_host(ctypes.byref(b), ctypes.byref(o), int(device), int(chunk_traces))
     _lib.check(rc, "sg_simulate_batch_host")
     return HostResult(ordered, out.grant if want_ticks else None, out.end if want_ticks else None,
-                      out.stats, out.mem_pct if want_pct else None, out.dev_pct if want_pct else None)
+                      out.stats, out.mem_pct if want_pct else None, out.dev_pct if want_pct else None,
+                      out.speedup if want_speedup else None, int(a.nbytes))
 
 
 def k1_engine(apps_per_trace: int, n_policies: int, ndev: int = 1) -> str:

@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <chrono>
+#include <mutex>
 #include <thread>
 #include <immintrin.h>
 #include <vector>
@@ -82,7 +83,14 @@ int sg_device_info(int cuda_device, int* sm_count, int* warps_per_sm) {
     cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
     if (sm_count) *sm_count = sms;
-    if (warps_per_sm) *warps_per_sm = 0;
+    if (warps_per_sm) {
+        int cur = 0;
+        e = cudaGetDevice(&cur);
+        if (e == cudaSuccess && cur != cuda_device) e = cudaSetDevice(cuda_device);
+        if (e == cudaSuccess) e = sg::lane_warps_per_sm(warps_per_sm);
+        if (cur != cuda_device) cudaSetDevice(cur);
+        if (e != cudaSuccess) return cuda_fail(e, "lane kernel occupancy");
+    }
     return 0;
 }
 
@@ -117,6 +125,7 @@ static int simulate_device(const sg_batch* in, const sg_out* out, cudaStream_t s
     p.stats = out->stats;
     p.mem_pct = out->mem_pct;
     p.dev_pct = out->dev_pct;
+    p.speedup = out->speedup;
     p.events = out->events;
     p.event_counts = out->event_counts;
     sg::sim_layout(p, s.program, s.f64);
@@ -142,18 +151,10 @@ static int simulate_device(const sg_batch* in, const sg_out* out, cudaStream_t s
 
 int sg_simulate_batch(const sg_batch* in, const sg_out* out, void* stream) {
     if (!in) return fail(E_ARG, "null batch");
-    uint64_t n_apps_total;
-    if (in->trace_offsets) {
-        // the total is only needed as the per-policy output stride
-        uint64_t o[2] = {0, 0};
-        cudaError_t e = cudaMemcpy(&o[0], in->trace_offsets, 8, cudaMemcpyDeviceToHost);
-        if (e == cudaSuccess)
-            e = cudaMemcpy(&o[1], in->trace_offsets + in->n_traces, 8, cudaMemcpyDeviceToHost);
-        if (e != cudaSuccess) return cuda_fail(e, "reading trace_offsets");
-        n_apps_total = o[1] - o[0];
-    } else {
-        n_apps_total = in->n_traces * (uint64_t)in->apps_per_trace;
-    }
+    // the per-policy stride of grant/end: given by the caller for CSR
+    // batches (no device read on the host: the call stays asynchronous)
+    const uint64_t n_apps_total = in->trace_offsets ? in->apps_total
+                                                    : in->n_traces * (uint64_t)in->apps_per_trace;
     return simulate_device(in, out, static_cast<cudaStream_t>(stream), n_apps_total);
 }
 
@@ -281,26 +282,31 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
         sg_app* apps = nullptr;
         uint32_t *grant = nullptr, *end = nullptr;
         sg_trace_stats* stats = nullptr;
-        double *mem = nullptr, *dev = nullptr;
+        double *mem = nullptr, *dev = nullptr, *spd = nullptr;
     } B[NBUF];
     std::vector<HostChunk> chunks;
     // Pipeline buffers come from the device's stream-ordered memory pool
     // (cudaMallocAsync), kept cached between calls: repeated calls pay no
     // cudaMalloc/cudaFree or implicit device synchronisation.
-    static bool pool_tuned[64] = {false};
-    if (cuda_device >= 0 && cuda_device < 64 && !pool_tuned[cuda_device]) {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, cuda_device) == cudaSuccess) {
-            uint64_t keep = ~0ull;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    {
+        static std::mutex mu;
+        static bool pool_tuned[64] = {false};
+        std::lock_guard<std::mutex> lk(mu);
+        if (cuda_device >= 0 && cuda_device < 64 && !pool_tuned[cuda_device]) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, cuda_device) == cudaSuccess) {
+                uint64_t keep = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+            pool_tuned[cuda_device] = true;
         }
-        pool_tuned[cuda_device] = true;
     }
     auto cleanup = [&]() {
         for (auto& b : B) {
             if (!b.st) continue;
             cudaFreeAsync(b.apps, b.st); cudaFreeAsync(b.grant, b.st); cudaFreeAsync(b.end, b.st);
             cudaFreeAsync(b.stats, b.st); cudaFreeAsync(b.mem, b.st); cudaFreeAsync(b.dev, b.st);
+            cudaFreeAsync(b.spd, b.st);
             cudaStreamSynchronize(b.st);
             cudaStreamDestroy(b.st);
         }
@@ -314,6 +320,7 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
         if (e == cudaSuccess) e = cudaMallocAsync(&b.stats, st_b, b.st);
         if (e == cudaSuccess && want_pct) e = cudaMallocAsync(&b.mem, pct_b, b.st);
         if (e == cudaSuccess && want_pct) e = cudaMallocAsync(&b.dev, pct_b, b.st);
+        if (e == cudaSuccess && out->speedup) e = cudaMallocAsync(&b.spd, pct_b, b.st);
         if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "allocating pipeline buffers"); }
     }
     const uint64_t n_apps_total = N * napps;
@@ -338,6 +345,7 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
         co.stats = b.stats;
         co.mem_pct = out->mem_pct ? b.mem : nullptr;
         co.dev_pct = out->dev_pct ? b.dev : nullptr;
+        co.speedup = b.spd;
         rc = simulate_device(&cb, &co, b.st, na);
         if (rc) { cleanup(); return rc; }
         for (uint32_t p = 0; p < s.npol; p++) {
@@ -359,6 +367,9 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
             if (e == cudaSuccess && out->dev_pct)
                 e = cudaMemcpyAsync(out->dev_pct + hs, b.dev + dsrc, nt * ndev * 8,
                                     cudaMemcpyDeviceToHost, b.st);
+            if (e == cudaSuccess && out->speedup)
+                e = cudaMemcpyAsync(out->speedup + hs, b.spd + dsrc, nt * ndev * 8,
+                                    cudaMemcpyDeviceToHost, b.st);
             if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "D2H outputs"); }
         }
         if (derive) {
@@ -375,6 +386,12 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
         // grants of its contiguous share of every chunk's traces
         const bool avx2 = __builtin_cpu_supports("avx2");
         unsigned nthr = std::thread::hardware_concurrency();
+        // one process per GPU shares the host: each rank's pipeline takes its
+        // share of the cores (LOCAL_WORLD_SIZE, set by torch.distributed.run)
+        if (const char* lw = getenv("LOCAL_WORLD_SIZE")) {
+            const int n = atoi(lw);
+            if (n > 1) nthr = nthr / (unsigned)n;
+        }
         nthr = nthr == 0 ? 1 : (nthr > 16 ? 16 : nthr);
         if (const char* ev = getenv("SGPU_HOST_THREADS")) {  // tuning knob
             const int v = atoi(ev);

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include "../../include/sgpu.h"
@@ -30,6 +31,7 @@ struct SimParams {
     void* stats;
     double* mem_pct;
     double* dev_pct;
+    double* speedup;                // optional: per-record speed-up vs sequential (ticks mode)
     sg_event* events;
     uint32_t* event_counts;
     // per-warp shared-memory layout (bytes)
@@ -44,12 +46,31 @@ struct SimParams {
     uint32_t* retry;
 };
 
+// A lease on one stream's work counters (and deferred-trace list), from
+// work_counters() until work_release(), which the caller invokes after its
+// last launch using them.  Outside a capture the pool lock is held for the
+// whole lease, so no other host thread can grow the list or reassign the
+// slot between the lookup and the launches; the release records the slot's
+// last-use event, which a later owner of a recycled slot waits on.  Inside a
+// capture counters and list are one graph allocation, freed on the stream
+// by the release.
+struct WorkLease {
+    std::unique_lock<std::mutex> lk;
+    cudaEvent_t last_use = nullptr;
+    void* owned = nullptr;
+};
+
 // The work counters of `stream` on the current device (sets p.work) and,
 // when retry_cap > 0, a deferred-trace list of that many entries that stays
-// valid for work on `stream` (sets p.retry).  Inside a stream capture both
-// are one graph allocation at p.work (*owned = true): the caller frees it
-// on the stream after its last launch.
-cudaError_t work_counters(cudaStream_t stream, SimParams& p, uint64_t retry_cap, bool* owned);
+// valid for work on `stream` (sets p.retry).
+cudaError_t work_counters(cudaStream_t stream, SimParams& p, uint64_t retry_cap, WorkLease& lease);
+// End the lease after the launches; returns `err` or the first release error.
+cudaError_t work_release(cudaStream_t stream, WorkLease& lease, cudaError_t err);
+
+// Kernel attributes (dynamic shared memory, max-shared carveout) set once per
+// (kernel, device, smem) and the resulting resident blocks per SM, cached:
+// launches pay no attribute call or occupancy query.
+cudaError_t kernel_config(const void* kern, int threads, size_t smem, int* per_sm, int* sms);
 
 // Shared-memory layout for one warp simulating traces of up to n_pad apps.
 void sim_layout(SimParams& p, bool program_mode, bool f64);
@@ -62,6 +83,9 @@ cudaError_t launch_sim(const SimParams& p, bool program_mode, bool f64, cudaStre
 // (sgpu_lane.cu), with an in-kernel exact fallback to TraceSim.
 bool lane_eligible(const SimParams& p, bool program_mode, bool f64, bool forced);
 cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_out);
+// Resident warps per SM of the lane kernel for a C2-shaped batch (64 apps, 4
+// policies, 1 device) on the current device (sg_device_info).
+cudaError_t lane_warps_per_sm(int* warps);
 
 cudaError_t launch_reduce(const sg_trace_stats* stats, uint64_t count, sg_aggr* out,
                           cudaStream_t stream);

@@ -47,6 +47,8 @@
 // priority classes, times near the 32-bit tick range) are re-simulated by
 // the whole warp with the exact warp-per-trace TraceSim (sgpu_tracesim.cuh)
 // right after, in the same kernel.
+#include <cstring>
+
 #include "sgpu_lanesim.cuh"
 
 namespace sg {
@@ -97,6 +99,13 @@ __host__ __device__ constexpr uint32_t meta_dev(uint32_t d) { return 3u + d; }
 __host__ __device__ constexpr uint32_t meta_z(uint32_t ndev, uint32_t d) { return 4u + ndev + d; }
 __host__ __device__ constexpr uint32_t meta_cls(uint32_t ndev, uint32_t d) { return 4u + 2u * ndev + d; }
 __host__ __device__ constexpr uint32_t meta_u16(uint32_t ndev) { return (5u + 3u * ndev + 7u) & ~7u; }
+// ndev > 1 only (one spare u16 after the class bounds; ndev == 1 ignores the
+// device field): the trace holds an app with device index >= ndev
+__host__ __device__ constexpr uint32_t meta_baddev(uint32_t ndev) { return 5u + 3u * ndev; }
+static_assert(meta_baddev(2) < meta_u16(2) && meta_baddev(3) < meta_u16(3) && meta_baddev(4) < meta_u16(4) &&
+                  meta_baddev(5) < meta_u16(5) && meta_baddev(6) < meta_u16(6) && meta_baddev(7) < meta_u16(7) &&
+                  meta_baddev(8) < meta_u16(8),
+              "meta layout");
 
 __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
     const uint32_t lo = __shfl_xor_sync(FULL, (uint32_t)v, m);
@@ -208,7 +217,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
     const uint32_t ndev = P.ndev;
 
     uint64_t key[K];
-    bool big = false;
+    bool big = false, bad_dev = false;
     uint32_t bsum = 0;  // busy sum (each busy < 2^21 unless `big`)
 #pragma unroll
     for (int k = 0; k < K; k++) {
@@ -218,7 +227,10 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
             const uint4 f = ldg_stream(reinterpret_cast<const uint4*>(P.apps + a0) + i, l2_policy_evict_first());
             raw[i] = f;
             uint32_t dv = ndev > 1 ? (f.w >> 8) & 0xFFu : 0u;
-            if (dv >= ndev) dv = 0;
+            if (dv >= ndev) {  // simulated on device 0, flagged SG_ST_BAD_DEVICE
+                dv = 0;
+                bad_dev = true;
+            }
             key[k] = ((uint64_t)dv << 42) | ((uint64_t)f.x << 10) | i;
             big = big || f.x >= (1u << 31) || f.z >= (1u << kBusyBits);
             bsum += min(f.z, 1u << kBusyBits);
@@ -454,6 +466,10 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
         meta[meta_dev(lane + 1)] = (uint16_t)dincl;
         meta[meta_z(ndev, lane)] = (uint16_t)z_d;
     }
+    if (ndev > 1) {
+        bad_dev = __any_sync(FULL, bad_dev);
+        if (lane == 0) meta[meta_baddev(ndev)] = bad_dev ? 1u : 0u;
+    }
     if (lane == 0) {
         meta[0] = (uint16_t)na;
         meta[1] = (uint16_t)fail;
@@ -498,7 +514,13 @@ __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const
     sim.heap = reinterpret_cast<typename LaneSim<K, NARROW, HW, FS>::Key*>(ws + L.off_fb) + lane;
     sim.out_base = (uint64_t)pslot * P.n_apps_total + a0;
     if (!sim.run(na, s0, s1, z, policy, cap_d)) return false;
-    sim.finish(((uint64_t)pslot * P.n_traces + t) * P.ndev + d, s1 - s0);
+    // S = cpu + busy ticks of the lane's device range (arrival < 2^31 and
+    // busy < 2^21 on this path), only when the speed-up is requested
+    uint64_t seq = 0;
+    if (P.speedup)
+        for (uint32_t q = s0; q < s1; q++) seq += (uint64_t)sim.s_a[q] + bw_busy(sim.s_bw[q]);
+    const uint32_t st = ndev > 1 && meta[meta_baddev(ndev)] ? SG_ST_BAD_DEVICE : 0u;
+    sim.finish(((uint64_t)pslot * P.n_traces + t) * P.ndev + d, s1 - s0, st, seq);
     return true;
 }
 
@@ -602,10 +624,11 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, MB) trace_sim_lane_ke
             const uint4* sub = apps_s;
             const uint16_t* idx = nullptr;
             uint32_t nd = na;
+            bool bad_dev = false;
             if (ndev > 1) {
                 uint4* s_sub = reinterpret_cast<uint4*>(fb + P.off_sub);
                 uint16_t* s_idx = reinterpret_cast<uint16_t*>(fb + P.off_idx);
-                nd = build_subtrace(apps_s, na, fd, ndev, s_sub, s_idx, lane);
+                nd = build_subtrace(apps_s, na, fd, ndev, s_sub, s_idx, lane, bad_dev);
                 sub = s_sub;
                 idx = s_idx;
             }
@@ -615,6 +638,7 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, MB) trace_sim_lane_ke
                 if (fd == j) fcap = P.cap[j];
             TraceSim<TickTM, K, false, false> sim(P, lane, fb, sub);
             sim.run(nd, (P.policy_list >> (4 * fp)) & 0xFu, fcap, nullptr);
+            if (bad_dev) sim.status |= SG_ST_BAD_DEVICE;
             sim.finish(((uint64_t)fp * P.n_traces + t) * ndev + fd, (uint64_t)fp * P.n_apps_total + a0,
                        idx, nullptr);
         }
@@ -643,33 +667,45 @@ bool lane_eligible(const SimParams& p, bool program_mode, bool f64, bool forced)
     return p.n_pad <= 64u || (p.n_pad <= 128u && p.npol * p.ndev >= 2);
 }
 
+// Grid of one lane-kernel instantiation for L (cached attributes/occupancy).
 template <int K, bool RETRY, int MB, uint32_t FS>
-static cudaError_t launch_lane_t(LaneParams& L, cudaStream_t stream, int* grid_out) {
-    auto kern = trace_sim_lane_kernel<K, RETRY, MB, FS>;
+static cudaError_t lane_grid(const LaneParams& L, uint64_t* grid) {
     const uint32_t wpb = kLaneWarpsPerBlock;
     const size_t smem = (size_t)L.warp_bytes * wpb;
-    if (smem > 227u * 1024u) return cudaErrorInvalidConfiguration;
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int sms = 0, per_sm = 0;
+    const cudaError_t err = kernel_config(reinterpret_cast<const void*>(trace_sim_lane_kernel<K, RETRY, MB, FS>),
+                                          wpb * 32, smem, &per_sm, &sms);
     if (err != cudaSuccess) return err;
-    // all of the unified L1/shared array as shared memory: the occupancy the
-    // grid is sized for must not depend on the driver's carveout choice
-    err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared);
-    if (err != cudaSuccess) return err;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, smem);
-    if (err != cudaSuccess) return err;
-    if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const uint64_t groups = (L.sp.n_traces + L.G - 1) / L.G;
     const uint64_t need = (groups + wpb - 1) / wpb;
-    uint64_t grid = (uint64_t)sms * per_sm;
-    if (need < grid) grid = need;
-    if (grid == 0) grid = 1;
-    if (grid_out) *grid_out = (int)grid;
-    kern<<<(unsigned)grid, wpb * 32, smem, stream>>>(L);
-    return cudaGetLastError();
+    uint64_t g = (uint64_t)sms * per_sm;
+    if (need < g) g = need;
+    *grid = g == 0 ? 1 : g;
+    return cudaSuccess;
+}
+
+// Main pass + retry pass of one variant.  Both configurations are checked
+// before the main pass launches: a main pass whose retry pass cannot run
+// would leave its deferred-trace count behind.
+template <int K, int MB, int MBR, uint32_t FS>
+static cudaError_t launch_pair(LaneParams& L, LaneParams& R, cudaStream_t stream, int* grid_out) {
+    uint64_t gm = 0, gr = 0;
+    cudaError_t err = lane_grid<K, false, MB, FS>(L, &gm);
+    if (err == cudaSuccess) err = lane_grid<K, true, MBR, FS>(R, &gr);
+    if (err != cudaSuccess) return err;
+    if (grid_out) *grid_out = (int)gm;
+    const unsigned threads = kLaneWarpsPerBlock * 32;
+    trace_sim_lane_kernel<K, false, MB, FS><<<(unsigned)gm, threads, (size_t)L.warp_bytes * kLaneWarpsPerBlock, stream>>>(L);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+    trace_sim_lane_kernel<K, true, MBR, FS><<<(unsigned)gr, threads, (size_t)R.warp_bytes * kLaneWarpsPerBlock, stream>>>(R);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) {
+        // the main pass may have deferred traces: clear the count for the
+        // stream's next launch
+        cudaMemsetAsync(L.sp.work + 2, 0, sizeof(unsigned long long), stream);
+    }
+    return err;
 }
 
 // Per-warp shared-memory layout of the lane kernel; `heap_bytes` is the
@@ -713,24 +749,19 @@ template <int K>
 static cudaError_t launch_lane_k(LaneParams& L, LaneParams& R, cudaStream_t stream, int* grid_out) {
     const uint32_t HB = max(kLaneHeapN * 32u * 4u, kLaneHeapW * 32u * 8u);  // main pass heap region
     const uint32_t HBR = kLaneHeapN * 32u * 8u;                          // retry pass: 64-bit keys
-    cudaError_t err;
     if constexpr (K == 2) {
         lane_layout(L, HB, 4u);
         // blocks per SM that shared memory allows (228 KB, 1 KB reserved per block)
         const uint32_t smem_blocks = 233472u / (L.warp_bytes * kLaneWarpsPerBlock + 1024u);
         if (smem_blocks >= (uint32_t)kLaneHiBlocks2) {
             lane_layout(R, HBR, 4u);
-            err = launch_lane_t<K, false, kLaneHiBlocks2, 4u>(L, stream, grid_out);
-            if (err == cudaSuccess) err = launch_lane_t<K, true, LaneMinBlocksR<K>::v, 4u>(R, stream, nullptr);
-            return err;
+            return launch_pair<K, kLaneHiBlocks2, LaneMinBlocksR<K>::v, 4u>(L, R, stream, grid_out);
         }
     }
     constexpr uint32_t FS = FitStride<K>::v;
     lane_layout(L, HB, FS);
     lane_layout(R, HBR, FS);
-    err = launch_lane_t<K, false, LaneMinBlocks<K>::v, FS>(L, stream, grid_out);
-    if (err == cudaSuccess) err = launch_lane_t<K, true, LaneMinBlocksR<K>::v, FS>(R, stream, nullptr);
-    return err;
+    return launch_pair<K, LaneMinBlocks<K>::v, LaneMinBlocksR<K>::v, FS>(L, R, stream, grid_out);
 }
 
 cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_out) {
@@ -751,21 +782,45 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
     L.need_tbl = N <= 128 ? 1u : 0u;  // all kinds use the fit table (one or two mask words)
     L.cm_per_trace = max(kLaneClassMasks / L.G, 8u);
     sim_layout(L.sp, false, false);
-    bool owned = false;
-    cudaError_t err = work_counters(stream, L.sp, p.n_traces, &owned);
-    if (err != cudaSuccess) return err;
-    LaneParams R = L;
-    switch (N / 32) {
-        case 1: err = launch_lane_k<1>(L, R, stream, grid_out); break;
-        case 2: err = launch_lane_k<2>(L, R, stream, grid_out); break;
-        case 4: err = launch_lane_k<4>(L, R, stream, grid_out); break;
-        case 8: err = launch_lane_k<8>(L, R, stream, grid_out); break;
-        default: err = cudaErrorInvalidValue;
+    WorkLease lease;
+    cudaError_t err = work_counters(stream, L.sp, p.n_traces, lease);
+    if (err == cudaSuccess) {
+        LaneParams R = L;
+        switch (N / 32) {
+            case 1: err = launch_lane_k<1>(L, R, stream, grid_out); break;
+            case 2: err = launch_lane_k<2>(L, R, stream, grid_out); break;
+            case 4: err = launch_lane_k<4>(L, R, stream, grid_out); break;
+            case 8: err = launch_lane_k<8>(L, R, stream, grid_out); break;
+            default: err = cudaErrorInvalidValue;
+        }
     }
-    if (owned) {
-        const cudaError_t e2 = cudaFreeAsync(L.sp.work, stream);
-        if (err == cudaSuccess) err = e2;
-    }
+    return work_release(stream, lease, err);
+}
+
+cudaError_t lane_warps_per_sm(int* warps) {
+    SimParams p;
+    memset(&p, 0, sizeof(p));
+    p.n_traces = 1u << 20;
+    p.apps_per_trace = 64;
+    p.n_pad = 64;
+    p.npol = 4;
+    p.policy_list = 0x3210u;
+    p.ndev = 1;
+    LaneParams L;
+    L.sp = p;
+    L.lpt = 4;
+    L.G = 8;
+    L.need_cls = 1;
+    L.need_tbl = 1;
+    L.cm_per_trace = max(kLaneClassMasks / L.G, 8u);
+    sim_layout(L.sp, false, false);
+    const uint32_t HB = max(kLaneHeapN * 32u * 4u, kLaneHeapW * 32u * 8u);
+    lane_layout(L, HB, FitStride<2>::v);
+    int sms = 0, per_sm = 0;
+    const cudaError_t err = kernel_config(
+        reinterpret_cast<const void*>(trace_sim_lane_kernel<2, false, LaneMinBlocks<2>::v, FitStride<2>::v>),
+        kLaneWarpsPerBlock * 32, (size_t)L.warp_bytes * kLaneWarpsPerBlock, &per_sm, &sms);
+    *warps = err == cudaSuccess ? per_sm * kLaneWarpsPerBlock : 0;
     return err;
 }
 

@@ -52,6 +52,11 @@ SG_HD uint32_t bw_app(uint32_t bw) { return (bw >> kBusyBits) & 0xFFu; }
 SG_HD uint32_t bw_cls(uint32_t bw) { return bw >> kClsShift; }
 
 
+// Member arrays (mask, gcand, grem, the fit set) are only ever updated with
+// unconditional per-word selects: a predicated store `if (w == q >> 6)
+// m[w] |= ...` is merged by the compiler into one dynamically indexed store,
+// which moves the whole LaneSim (and a copy of the kernel parameters) to
+// local memory (K = 4: a 624-byte stack frame).
 SG_HD uint32_t ffs64(uint64_t x) { return (uint32_t)__ffsll((long long)x) - 1u; }
 SG_HD uint32_t ffs32(uint32_t x) { return (uint32_t)__ffs((int)x) - 1u; }
 
@@ -214,7 +219,7 @@ struct LaneSim {
     SG_HD void enqueue(uint32_t q, uint32_t bw) {
 #pragma unroll
         for (uint32_t w = 0; w < NW; w++)
-            if (w == (q >> 6)) mask[w] |= 1ull << (q & 63u);
+            mask[w] |= w == (q >> 6) ? 1ull << (q & 63u) : 0ull;  // unconditional: no indexed store
         clsmask |= 1u << bw_cls(bw);
     }
     // number of requests <= budget in the trace: bucket lookup (LtBuckets
@@ -237,7 +242,7 @@ struct LaneSim {
             const uint32_t p = s_por[r & ~1u];
 #pragma unroll
             for (uint32_t w = 0; w < NW; w++)
-                if ((r & 1u) && (NW == 1 || w == (p >> 6))) t[w] |= 1ull << (p & 63u);
+                t[w] |= (r & 1u) && (NW == 1 || w == (p >> 6)) ? 1ull << (p & 63u) : 0ull;
         } else {
             const uint32_t pw = *reinterpret_cast<const uint32_t*>(s_por + (r & ~3u));
             const uint32_t k = r & 3u;
@@ -246,14 +251,14 @@ struct LaneSim {
                 const uint32_t p = (pw >> (8u * j)) & 0xFFu;
 #pragma unroll
                 for (uint32_t w = 0; w < NW; w++)
-                    if (k > j && (NW == 1 || w == (p >> 6))) t[w] |= 1ull << (p & 63u);
+                    t[w] |= k > j && (NW == 1 || w == (p >> 6)) ? 1ull << (p & 63u) : 0ull;
             }
         }
     }
     SG_HD void grant_one(uint32_t q, uint32_t m, uint32_t& budget, uint32_t& g) {
 #pragma unroll
         for (uint32_t w = 0; w < NW; w++)
-            if (w == (q >> 6)) mask[w] &= ~(1ull << (q & 63u));
+            mask[w] &= w == (q >> 6) ? ~(1ull << (q & 63u)) : ~0ull;
         budget -= m;
         g += 1;
         wake(q);
@@ -329,10 +334,8 @@ struct LaneSim {
             const uint64_t bit = 1ull << (q & 63u);
 #pragma unroll
             for (uint32_t w = 0; w < NW; w++) {
-                if (w == qw) {
-                    mask[w] &= ~bit;
-                    grem[w] &= ~bit;
-                }
+                mask[w] &= w == qw ? ~bit : ~0ull;
+                grem[w] &= w == qw ? ~bit : ~0ull;
                 // continue above the granted position
                 gcand[w] &= w < qw ? 0ull : (w == qw ? ~((bit << 1) - 1ull) : ~0ull);
                 more = more || gcand[w] != 0;
@@ -583,7 +586,7 @@ struct LaneSim {
     }
 
 #ifdef __CUDACC__
-    SG_HD void finish(uint64_t srec, uint32_t nd) {
+    SG_HD void finish(uint64_t srec, uint32_t nd, uint32_t st, uint64_t seq) {
         uint32_t unf = 0;
 #pragma unroll
         for (uint32_t w = 0; w < NW; w++) {
@@ -596,7 +599,7 @@ struct LaneSim {
             }
         }
         store_tick_record(P, srec, nd, cap, last, mem_t, I, B, (int64_t)used, grants, pops + nd,
-                          maxh, unf, 0u);
+                          maxh, unf, st, seq);
     }
 #endif
 };

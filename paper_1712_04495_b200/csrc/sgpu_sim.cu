@@ -32,6 +32,7 @@
 //     reorder events of one device (pinned by tests/golden/ref_multidev.npz)
 #include <algorithm>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -140,10 +141,11 @@ __global__ void SG_SIM_BOUNDS trace_sim_kernel(const SimParams P) {
             const uint4* sub = apps_smem;
             const uint16_t* idx = nullptr;
             uint32_t nd = na;
+            bool bad_dev = false;
             if (P.ndev > 1) {
                 uint4* s_sub = reinterpret_cast<uint4*>(ws + P.off_sub);
                 uint16_t* s_idx = reinterpret_cast<uint16_t*>(ws + P.off_idx);
-                nd = build_subtrace(apps_smem, na, d, P.ndev, s_sub, s_idx, lane);
+                nd = build_subtrace(apps_smem, na, d, P.ndev, s_sub, s_idx, lane, bad_dev);
                 sub = s_sub;
                 idx = s_idx;
             }
@@ -153,6 +155,7 @@ __global__ void SG_SIM_BOUNDS trace_sim_kernel(const SimParams P) {
                 const uint64_t slot = (uint64_t)p * P.n_traces + t;
                 sg_event* evs = P.events ? P.events + slot * P.ev_cap : nullptr;
                 sim.run(nd, (P.policy_list >> (4 * p)) & 0xFu, cap_d, evs);
+                if (bad_dev) sim.status |= SG_ST_BAD_DEVICE;
                 sim.finish(slot * P.ndev + d, (uint64_t)p * P.n_apps_total + a0, idx,
                            P.event_counts ? P.event_counts + slot : nullptr);
             }
@@ -166,27 +169,29 @@ __global__ void SG_SIM_BOUNDS trace_sim_kernel(const SimParams P) {
 
 // ------------------------------------------------------------------ launch
 
-// Work counters for dynamic scheduling, one pair per (device, stream): the
+// Work counters for dynamic scheduling, one set per (device, stream): the
 // kernels reset them at the end of every launch (sgpu_common.cuh
-// work_done), and launches on one stream are ordered, so a stream's pair is
-// always zero when its next launch starts.  A pool per device; streams take
-// slots round robin (a reused slot's previous stream has been idle for
-// kWorkSlots new streams); the per-thread default stream is keyed by thread.
+// work_done), and launches on one stream are ordered, so a stream's set is
+// always zero when its next launch starts.  A pool per device; new streams
+// take slots round robin, and the per-thread default stream is keyed by
+// thread.  A recycled slot may still be in use by work its previous stream
+// has queued: the new owner's stream first waits on the slot's last-use
+// event (recorded by every lease's release), so the two never overlap.
 namespace {
 constexpr int kWorkSlots = 512;
+constexpr int kWorkWords = 4;  // u64 counters per slot
 struct WorkPool {
     unsigned long long* ctr = nullptr;
     std::map<std::pair<cudaStream_t, std::thread::id>, int> slot;
     int next = 0;
     std::vector<std::pair<uint32_t*, uint64_t>> retry = std::vector<std::pair<uint32_t*, uint64_t>>(kWorkSlots);
+    std::vector<cudaEvent_t> last_use = std::vector<cudaEvent_t>(kWorkSlots, nullptr);
 };
-constexpr int kWorkWords = 4;  // u64 counters per slot
 std::mutex g_work_mu;
 std::map<int, WorkPool> g_work;
 }  // namespace
 
-cudaError_t work_counters(cudaStream_t stream, SimParams& p, uint64_t retry_cap, bool* owned) {
-    if (owned) *owned = false;
+cudaError_t work_counters(cudaStream_t stream, SimParams& p, uint64_t retry_cap, WorkLease& lease) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaError_t e = cudaStreamIsCapturing(stream, &cs);
     if (e != cudaSuccess) return e;
@@ -194,21 +199,20 @@ cudaError_t work_counters(cudaStream_t stream, SimParams& p, uint64_t retry_cap,
         // inside a capture: counters and list are graph allocations (zeroed
         // by a memset node at every replay), so a replay never shares them
         // with the capturing stream's later work or with another replay
-        if (!owned) return cudaErrorInvalidValue;
         void* b = nullptr;
         e = cudaMallocAsync(&b, kWorkWords * sizeof(unsigned long long) + retry_cap * 4u, stream);
         if (e != cudaSuccess) return e;
+        lease.owned = b;
         e = cudaMemsetAsync(b, 0, kWorkWords * sizeof(unsigned long long), stream);
         if (e != cudaSuccess) return e;
         p.work = static_cast<unsigned long long*>(b);
         p.retry = retry_cap ? reinterpret_cast<uint32_t*>(p.work + kWorkWords) : nullptr;
-        *owned = true;
         return cudaSuccess;
     }
     int dev = 0;
     e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    std::lock_guard<std::mutex> lk(g_work_mu);
+    lease.lk = std::unique_lock<std::mutex>(g_work_mu);
     WorkPool& w = g_work[dev];
     if (!w.ctr) {
         e = cudaMalloc(&w.ctr, kWorkWords * kWorkSlots * sizeof(unsigned long long));
@@ -224,28 +228,97 @@ cudaError_t work_counters(cudaStream_t stream, SimParams& p, uint64_t retry_cap,
         w.next = (w.next + 1) % kWorkSlots;
         for (auto i = w.slot.begin(); i != w.slot.end();) i = i->second == s ? w.slot.erase(i) : std::next(i);
         w.slot[key] = s;
+        // the slot's previous owner may still have launches queued
+        if (w.last_use[s]) {
+            e = cudaStreamWaitEvent(stream, w.last_use[s], 0);
+            if (e != cudaSuccess) return e;
+        }
     } else {
         s = it->second;
     }
+    if (!w.last_use[s]) {
+        e = cudaEventCreateWithFlags(&w.last_use[s], cudaEventDisableTiming);
+        if (e != cudaSuccess) { w.last_use[s] = nullptr; return e; }
+    }
+    lease.last_use = w.last_use[s];
     p.work = w.ctr + kWorkWords * s;
     p.retry = nullptr;
     if (retry_cap == 0) return cudaSuccess;
     auto& rb = w.retry[s];
     if (rb.second < retry_cap) {
-        // grow: work already queued on the stream may still read the old list
+        // grow: the old list is freed in stream order, after every queued
+        // launch of this slot (this stream's, and the previous owner's,
+        // which this stream already waits on)
         if (rb.first) {
-            e = cudaStreamSynchronize(stream);
-            if (e == cudaSuccess) e = cudaFree(rb.first);
-            if (e != cudaSuccess) return e;
+            e = cudaFreeAsync(rb.first, stream);
             rb = {nullptr, 0};
+            if (e != cudaSuccess) return e;
         }
         const uint64_t c = std::max<uint64_t>(retry_cap, 1u << 16);
-        e = cudaMalloc(&rb.first, c * 4u);
+        e = cudaMallocAsync(reinterpret_cast<void**>(&rb.first), c * 4u, stream);
         if (e != cudaSuccess) { rb = {nullptr, 0}; return e; }
         rb.second = c;
     }
     p.retry = rb.first;
     return cudaSuccess;
+}
+
+cudaError_t work_release(cudaStream_t stream, WorkLease& lease, cudaError_t err) {
+    if (lease.owned) {
+        const cudaError_t e = cudaFreeAsync(lease.owned, stream);
+        lease.owned = nullptr;
+        if (err == cudaSuccess) err = e;
+    }
+    if (lease.last_use) {
+        const cudaError_t e = cudaEventRecord(lease.last_use, stream);
+        lease.last_use = nullptr;
+        if (err == cudaSuccess) err = e;
+    }
+    if (lease.lk.owns_lock()) lease.lk.unlock();
+    return err;
+}
+
+namespace {
+struct KernelCfg {
+    int per_sm, sms;
+};
+std::mutex g_cfg_mu;
+std::map<std::tuple<const void*, int, int, size_t>, KernelCfg> g_cfg;
+// the dynamic shared-memory limit set on each (kernel, device): only ever
+// raised, so a configuration cached at a larger size stays launchable
+std::map<std::pair<const void*, int>, size_t> g_smem_max;
+}  // namespace
+
+cudaError_t kernel_config(const void* kern, int threads, size_t smem, int* per_sm, int* sms) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const auto key = std::make_tuple(kern, dev, threads, smem);
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    auto it = g_cfg.find(key);
+    if (it == g_cfg.end()) {
+        if (smem > 227u * 1024u) return cudaErrorInvalidConfiguration;
+        size_t& lim = g_smem_max[std::make_pair(kern, dev)];
+        if (smem > lim) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            lim = smem;
+        }
+        // all of the unified L1/shared array as shared memory: the occupancy
+        // the grid is sized for must not depend on the driver's carveout choice
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
+        KernelCfg c{0, 0};
+        e = cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.per_sm, kern, threads, smem);
+        if (e != cudaSuccess) return e;
+        it = g_cfg.emplace(key, c).first;
+    }
+    *per_sm = it->second.per_sm;
+    *sms = it->second.sms;
+    return *per_sm < 1 ? cudaErrorInvalidConfiguration : cudaSuccess;
 }
 
 static inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
@@ -292,36 +365,22 @@ static cudaError_t launch_t(const SimParams& p, cudaStream_t stream, int* grid_o
     uint32_t wpb = kSimWarpsPerBlock;
     while (wpb > 1 && (size_t)p.warp_bytes * wpb > 227u * 1024u) wpb--;
     const size_t smem = (size_t)p.warp_bytes * wpb;
-    if (smem > 227u * 1024u) return cudaErrorInvalidConfiguration;
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int sms = 0, per_sm = 0;
+    cudaError_t err = kernel_config(reinterpret_cast<const void*>(kern), wpb * 32, smem, &per_sm, &sms);
     if (err != cudaSuccess) return err;
-    // all of the unified L1/shared array as shared memory: the occupancy the
-    // grid is sized for must not depend on the driver's carveout choice
-    err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared);
-    if (err != cudaSuccess) return err;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, smem);
-    if (err != cudaSuccess) return err;
-    if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const uint64_t need = (p.n_traces + wpb - 1) / wpb;
     uint64_t grid = (uint64_t)sms * per_sm;
     if (need < grid) grid = need;
     if (grid == 0) grid = 1;
     if (grid_out) *grid_out = (int)grid;
     SimParams q = p;
-    bool owned = false;
-    err = work_counters(stream, q, 0, &owned);
-    if (err != cudaSuccess) return err;
-    kern<<<(unsigned)grid, wpb * 32, smem, stream>>>(q);
-    err = cudaGetLastError();
-    if (owned) {
-        const cudaError_t e2 = cudaFreeAsync(q.work, stream);
-        if (err == cudaSuccess) err = e2;
+    WorkLease lease;
+    err = work_counters(stream, q, 0, lease);
+    if (err == cudaSuccess) {
+        kern<<<(unsigned)grid, wpb * 32, smem, stream>>>(q);
+        err = cudaGetLastError();
     }
-    return err;
+    return work_release(stream, lease, err);
 }
 
 template <class TM, bool PROG>

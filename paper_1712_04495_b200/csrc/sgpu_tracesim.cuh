@@ -111,11 +111,27 @@ __device__ __forceinline__ uint64_t q_pack(uint32_t app, uint32_t mib, uint32_t 
 // span), dev% = (100 * B * 2^-tick_log2) / span; an empty event list reports
 // 0 / 0 (harness.py:374-375).  Shared by both K1 kernels so their records are
 // identical by construction.
+//
+// Speed-up vs sequential execution (optional output), the reference's
+// sum(p.total_ms() for p in instances) * time_scale / report.makespan_ms
+// (harness.py:61-62, 378, 454; pkg/tests/test_harness.py:119-126) for a trace
+// whose cpu/busy durations are ticks run at time_scale = 1000 * 2^-tick_log2:
+// seq_ms = S * time_scale is exact (S = the sub-trace's cpu + busy ticks),
+// makespan_ms = max(T * 2^-tick_log2, 1e-9) * 1000.0, one correctly rounded
+// division.  An empty sub-trace (the reference divides 0.0 by 0.0) gives NaN.
+__device__ __forceinline__ double speedup_ticks(int32_t tick_log2, uint32_t n, uint64_t S, uint32_t T) {
+    if (n == 0) return __longlong_as_double(0x7FF8000000000000LL);
+    const double scale = ldexp(1.0, -tick_log2);
+    const double seq_ms = __dmul_rn(__ull2double_rn(S), __dmul_rn(1000.0, scale));
+    const double span = T > 0 ? __dmul_rn((double)T, scale) : 1e-9;
+    return __ddiv_rn(seq_ms, __dmul_rn(span, 1000.0));
+}
+
 __device__ __forceinline__ void store_tick_record(const SimParams& P, uint64_t rec, uint32_t n,
                                                   uint32_t cap, uint32_t last, uint32_t mem_t,
                                                   uint64_t I, uint32_t B, int64_t u, uint32_t grants,
                                                   uint32_t pops, uint32_t maxh, uint32_t unf,
-                                                  uint32_t st) {
+                                                  uint32_t st, uint64_t seq) {
     const double scale = ldexp(1.0, -P.tick_log2);
     const double cap_bytes = (double)cap * kMiB;
     uint64_t Iv = I;
@@ -145,15 +161,17 @@ __device__ __forceinline__ void store_tick_record(const SimParams& P, uint64_t r
     if (n == 0) { mem_pct = 0.0; dev_pct = 0.0; }
     if (P.mem_pct) P.mem_pct[rec] = mem_pct;
     if (P.dev_pct) P.dev_pct[rec] = dev_pct;
+    if (P.speedup) P.speedup[rec] = speedup_ticks(P.tick_log2, n, seq, last);
 }
 
 // Device d's sub-trace (apps whose device field is d; out-of-range devices
-// count as device 0), in index order, with its trace app indices.  Returns
-// its length.  Warp-collective.
+// count as device 0 and set `bad`), in index order, with its trace app
+// indices.  Returns its length.  Warp-collective.
 __device__ __forceinline__ uint32_t build_subtrace(const uint4* apps, uint32_t na, uint32_t d,
                                                    uint32_t ndev, uint4* s_sub, uint16_t* s_idx,
-                                                   uint32_t lane) {
+                                                   uint32_t lane, bool& bad) {
     uint32_t nd = 0;
+    bad = false;
     for (uint32_t base = 0; base < na; base += 32) {
         const uint32_t i = base + lane;
         uint4 f = make_uint4(0, 0, 0, 0);
@@ -161,8 +179,12 @@ __device__ __forceinline__ uint32_t build_subtrace(const uint4* apps, uint32_t n
         if (i < na) {
             f = apps[i];
             dv = (f.w >> 8) & 0xFFu;
-            if (dv >= ndev) dv = 0;
+            if (dv >= ndev) {
+                dv = 0;
+                bad = true;
+            }
         }
+        bad = __any_sync(FULL, bad);
         const uint32_t m = __ballot_sync(FULL, dv == d);
         if (dv == d) {
             const uint32_t pos = nd + __popc(m & lanemask_lt());
@@ -609,7 +631,11 @@ struct TraceSim {
                     held += (int32_t)mib;
                     maxh = max(maxh, (uint32_t)max(holders, 0));
                     grants += 1;
-                    if (TM::is_never(s_grant[app])) s_grant[app] = now;
+                    {   // first grant of the app: read by the warp, then one lane writes
+                        const bool first = TM::is_never(s_grant[app]);
+                        __syncwarp();
+                        if (first && lane == 0) s_grant[app] = now;
+                    }
                     emit(now, app, SG_EV_GRANT, mib);
                     emit(now, app, SG_EV_ALLOC, mib);
                     pc += 1;
@@ -801,16 +827,36 @@ struct TraceSim {
         }
     }
 
+    // cpu + busy ticks of app i (its AppProfile.total_ms() on the tick grid,
+    // harness.py:61-62): arrival + busy (T0), or its program's cpu and busy
+    // step durations
+    __device__ __forceinline__ uint64_t seq_ticks(uint32_t i) const {
+        const uint4 f = s_app[i];
+        if constexpr (PROG) {
+            uint64_t s = 0;
+            for (uint32_t k = 0; k < f.y; k++) {
+                const uint4 stp = s_steps ? s_steps[f.x + k]
+                                          : __ldg(reinterpret_cast<const uint4*>(P.steps) + f.x + k);
+                if (stp.x == SG_OP_CPU || stp.x == SG_OP_BUSY) s += ((uint64_t)stp.w << 32) | stp.z;
+            }
+            return s;
+        } else {
+            return (uint64_t)f.x + f.z;
+        }
+    }
+
     // --------------------------------------------------------------- output
     // rec: statistics record index; s_idx: sub-trace -> trace app index (or null)
     __device__ __forceinline__ void finish(uint64_t rec, uint64_t app_out_base, const uint16_t* s_idx,
                            uint32_t* ev_count_out) {
         __syncwarp();
         uint32_t unf = 0;
+        uint64_t seq = 0;  // cpu + busy ticks of the (sub-)trace, for P.speedup
         for (uint32_t base = 0; base < n; base += 32) {
             const uint32_t i = base + lane;
             const bool valid = i < n;
             T evv = TM::never();
+            if (!TM::F64 && valid && P.speedup) seq += seq_ticks(i);
             if (valid) {
                 const T gv = s_grant[i];
                 evv = s_end[i];
@@ -821,6 +867,10 @@ struct TraceSim {
             unf += __popc(__ballot_sync(FULL, valid && TM::is_never(evv)));
         }
         if (ev_count_out != nullptr && lane == 0) *ev_count_out = ev_n;
+        if (!TM::F64 && P.speedup) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) seq += __shfl_xor_sync(FULL, seq, o);
+        }
         if (lane == 0) {
             const int64_t u = (int64_t)used;
             uint32_t st = status;
@@ -844,9 +894,12 @@ struct TraceSim {
                 if (n == 0) { mem_pct = 0.0; dev_pct = 0.0; }  // empty event list (harness.py:374-375)
                 if (P.mem_pct) P.mem_pct[rec] = mem_pct;
                 if (P.dev_pct) P.dev_pct[rec] = dev_pct;
+                // seconds-valued steps carry no phase-level ms: the drop-in
+                // computes the speed-up from the spec (harness.speedup_vs_sequential)
+                if (P.speedup) P.speedup[rec] = __longlong_as_double(0x7FF8000000000000LL);
             } else {
                 store_tick_record(P, rec, n, cap, (uint32_t)last, (uint32_t)mem_t, (uint64_t)I,
-                                  (uint32_t)B, u, grants, pops + n, maxh, unf, st);
+                                  (uint32_t)B, u, grants, pops + n, maxh, unf, st, seq);
             }
         }
         __syncwarp();

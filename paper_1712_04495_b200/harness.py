@@ -363,5 +363,15 @@ def sequential_ms(spec: WorkloadSpec) -> float:
     return sum(p.total_ms() for p in spec.instances) * spec.time_scale
 
 
+def speedup_vs_sequential(spec: WorkloadSpec, report: MetricsReport) -> float:
+    """Concurrent speed-up over running the instances one after another:
+    sum(p.total_ms() for p in instances) * time_scale / makespan_ms, in the
+    reference's float order (harness.py:61-62; pkg/tests/test_harness.py:
+    119-126, where sequential = 12 x 10 s).  The batch API emits the same
+    value per (policy, trace, device) from the kernel (sg_out.speedup)."""
+    return sequential_ms(spec) / report.makespan_ms
+
+
 __all__ = ["Phase", "AppProfile", "builtin_profiles", "DEFAULT_DEVICE", "WorkloadSpec",
-           "MetricsReport", "simulate", "encode_spec", "sequential_ms", "TICK_MS"]
+           "MetricsReport", "simulate", "encode_spec", "sequential_ms", "speedup_vs_sequential",
+           "TICK_MS"]

@@ -10,13 +10,18 @@ tests/refsim.py).  Outputs (committed, small):
                      all four policies, dyadic time scale 1000/1024: per-app
                      first-grant / end ticks, makespan ticks, the report's
                      makespan_ms / avg_mem_util_pct / avg_device_util_pct
-                     (exact float64), max holders, grants, unfinished
+                     (exact float64), max holders, grants, unfinished, and
+                     the speed-up vs sequential execution
+                     sum(total_ms) * time_scale / makespan_ms
   ref_multidev.npz   C5-shaped traces (8 simulated devices per trace) pinned
                      by decomposition: simulate() on each device's sub-trace
   ref_reports.json   full MetricsReports (summary, float-exact events,
                      mem_trace, instances) for the reference's own test
                      scenarios and README examples, incl. non-dyadic scales
   ref_select.npz     random queues x 4 policies -> select_grants masks
+  ref_criterion5.npz the 100k queues of acceptance criterion 5
+                     (test_acceptance.py:174-226, seed 20260823) x 4
+                     policies -> the reference's select_grants flags
 """
 
 from __future__ import annotations
@@ -57,8 +62,10 @@ def burst_fixture(path: str):
             T = np.zeros(nt, dtype=np.uint32)
             f = np.zeros((nt, 3), dtype=np.float64)
             ints = np.zeros((nt, 3), dtype=np.int64)
+            spd = np.zeros(nt, dtype=np.float64)
             for t in range(nt):
                 r = refsim.run_burst(apps[t], cfg.cap_mib[0], pol)
+                spd[t] = r["speedup"]
                 g[t] = [NONE if x is None else x for x in r["grant"]]
                 e[t] = [NONE if x is None else x for x in r["end"]]
                 T[t] = r["T"]
@@ -69,6 +76,7 @@ def burst_fixture(path: str):
             out[f"{cname}_{pol}_T"] = T
             out[f"{cname}_{pol}_floats"] = f
             out[f"{cname}_{pol}_ints"] = ints
+            out[f"{cname}_{pol}_speedup"] = spd
     np.savez_compressed(path, **out)
 
 
@@ -84,6 +92,7 @@ def multidev_fixture(path: str, nt: int = 12, seed: int = 11):
         T = np.zeros((nt, ndev), dtype=np.uint32)
         f = np.zeros((nt, ndev, 3), dtype=np.float64)
         ints = np.zeros((nt, ndev, 3), dtype=np.int64)
+        spd = np.zeros((nt, ndev), dtype=np.float64)
         for t in range(nt):
             devs = (apps[t, :, 3] >> 8) & 0xFF
             for d in range(ndev):
@@ -95,7 +104,9 @@ def multidev_fixture(path: str, nt: int = 12, seed: int = 11):
                 T[t, d] = r["T"]
                 f[t, d] = (r["makespan_ms"], r["mem_pct"], r["dev_pct"])
                 ints[t, d] = (r["max_holders"], r["grants"], r["unfinished"])
+                spd[t, d] = r["speedup"]
         out[f"{pol}_grant"], out[f"{pol}_end"], out[f"{pol}_T"] = g, e, T
+        out[f"{pol}_speedup"] = spd
         out[f"{pol}_floats"], out[f"{pol}_ints"] = f, ints
     np.savez_compressed(path, **out)
 
@@ -209,6 +220,8 @@ def reports_fixture(path: str):
             "avg_mem_util_pct": float.hex(rep.avg_mem_util_pct),
             "avg_device_util_pct": float.hex(rep.avg_device_util_pct),
             "max_concurrent_holders": rep.max_concurrent_holders,
+            # sum(p.total_ms() for p in spec.instances) * time_scale / makespan_ms
+            "speedup": float.hex(refsim.speedup_of(spec, rep)),
             "oom_count": rep.oom_count,
             "summary": rep.summary(),
             "events": [[float.hex(e["t_ms"]), e["instance"], e["event"], e["device"], e["bytes"]]
@@ -256,6 +269,28 @@ def select_fixture(path: str, trials: int = 4000, seed: int = 20260823):
                         kind=np.array(kinds, np.uint32), granted=np.array(granted, np.uint8))
 
 
+def criterion5_fixture(path: str):
+    """The reference's own select_grants on the 100k criterion-5 queues x 4
+    policies (policy-major within a queue), granted flags packed as bits."""
+    _, pol, _ = refsim.ref_modules()
+
+    class E:
+        __slots__ = ("client", "nbytes", "priority")
+
+        def __init__(self, c, b, p):
+            self.client, self.nbytes, self.priority = c, b, p
+
+    flags = []
+    from util import criterion5_queues
+    for sizes, prios, free in criterion5_queues():
+        q = [E(i, sizes[i], prios[i]) for i in range(len(sizes))]
+        for kind in pol.PolicyKind:
+            got = set(pol.select_grants(q, free, kind))
+            flags += [1 if i in got else 0 for i in range(len(sizes))]
+    np.savez_compressed(path, granted_bits=np.packbits(np.array(flags, np.uint8)),
+                        n_flags=np.array([len(flags)], np.int64))
+
+
 def main():
     if not refsim.available():
         raise SystemExit("the reference tree is not available here")
@@ -263,6 +298,7 @@ def main():
     multidev_fixture(os.path.join(HERE, "ref_multidev.npz"))
     reports_fixture(os.path.join(HERE, "ref_reports.json"))
     select_fixture(os.path.join(HERE, "ref_select.npz"))
+    criterion5_fixture(os.path.join(HERE, "ref_criterion5.npz"))
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))
 

@@ -77,7 +77,20 @@ def run_burst(apps_row, cap_mib: int, policy: str, tick_log2: int = 10):
         devices=device.parse_device_config({"devices": [{"mib": int(cap_mib)}]}),
         time_scale=TIME_SCALE_DYADIC)
     report, events = run_spec(spec)
-    return summarize(report, events, len(apps_row))
+    out = summarize(report, events, len(apps_row))
+    out["speedup"] = speedup_of(spec, report)
+    return out
+
+
+def speedup_of(spec, report) -> float:
+    """The reference's speed-up vs sequential execution: sequential makespan
+    = sum(AppProfile.total_ms()) * time_scale (harness.py:61-62), as in
+    pkg/tests/test_harness.py:119-126 (120_000 / makespan_ms for 12 x 10 s).
+    NaN where the reference would divide 0.0 by 0.0 (no events)."""
+    seq = sum(p.total_ms() for p in spec.instances) * spec.time_scale
+    if report.makespan_ms == 0.0:
+        return float("nan")
+    return seq / report.makespan_ms
 
 
 def to_ticks(t: float, tick_log2: int = 10) -> int:

@@ -49,6 +49,53 @@ def test_report_matches_reference(rec, cuda):
     assert inst == rec["instances"]
     csv = rep.to_csv().splitlines()
     assert csv[:3] == rec["csv_head"] and csv[-1] == rec["csv_tail"]
+    # speed-up vs sequential execution (pkg/tests/test_harness.py:119-126),
+    # the reference's own value, bit for bit (well inside 1e-12 relative)
+    assert S.speedup_vs_sequential(build_spec(rec), rep) == float.fromhex(rec["speedup"])
+
+
+def _exact_on_grid(rec):
+    """Every step duration ms * time_scale / 1000 and the sequential total
+    sum(ms) * time_scale are exact in float64 (Fractions), so the kernel's
+    tick-sum S and the reference's float sum describe the same number."""
+    from fractions import Fraction as F
+    sp = rec["spec"]
+    if sp["from_json"] is not None:
+        return False
+    ts = float.fromhex(sp["time_scale"])
+    tot = F(0)
+    for i in sp["instances"]:
+        for ph in i["phases"]:
+            for ms in (ph[0], ph[2]):
+                if F(ms) * F(ts) / 1000 != F(ms * ts / 1000.0):
+                    return False
+                tot += F(ms)
+    return F(float(tot)) == tot and F(float(tot) * ts) == tot * F(ts)
+
+
+@pytest.mark.parametrize("rec", [r for r in RECORDS if _exact_on_grid(r)], ids=lambda r: r["name"])
+def test_kernel_speedup_program_mode(rec, cuda):
+    """The kernel's own speed-up output (sg_out.speedup) in step-program
+    mode: when every duration is exact on the tick grid, the kernel's
+    (S * 1000 * 2^-e) / (T * 2^-e * 1000) is the reference's value exactly."""
+    import numpy as np
+    import torch
+    from paper_1712_04495_b200 import batch as B
+    from paper_1712_04495_b200 import harness as H
+    spec = build_spec(rec)
+    enc = H.encode_spec(spec)
+    if enc.time_mode != 0:
+        pytest.skip("float64 mode: the drop-in computes the speed-up from the spec")
+    dev = torch.device("cuda", 0)
+    n = len(enc.attr)
+    apps = np.zeros((1, n, 4), dtype=np.uint32)
+    apps[0, :, 3] = enc.attr
+    res = B.simulate_batch(torch.from_numpy(apps.view(np.int32)).to(dev), (spec.policy,), enc.cap_mib,
+                           steps=torch.from_numpy(enc.steps.view(np.int32).reshape(-1, 4).copy()).to(dev),
+                           step_offsets=torch.from_numpy(enc.step_offsets.view(np.int32).copy()).to(dev),
+                           tick_log2=enc.tick_log2)
+    got = float(res.speedup[0, 0, 0].cpu())
+    assert got == float.fromhex(rec["speedup"])
 
 
 def test_reference_simulator_goldens(cuda):

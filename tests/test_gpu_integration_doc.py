@@ -38,8 +38,10 @@ def test_stub_runs_bit_exact(cuda):
     cfg = CONFIGS["C2"]
     apps = np.ascontiguousarray(as_u32x4(generate(cfg.gen, 77, 400)))
     for code, pol in enumerate(("fifo", "mmu", "pfifo", "pmmu")):
-        g, e, st = ns["simulate_many"](apps, cfg.cap_mib[0], code)
+        g, e, st, sp = ns["simulate_many"](apps, cfg.cap_mib[0], code)
         og, oe, os_ = O.simulate_burst(apps, cfg.cap_mib, pol)
+        want = O.speedup_from(O.seq_ticks(apps)[:, 0], os_[:, 0]["makespan"], np.full(len(apps), apps.shape[1]))
+        np.testing.assert_array_equal(sp.view(np.uint64), want.view(np.uint64))
         np.testing.assert_array_equal(g, og)
         np.testing.assert_array_equal(e, oe)
         np.testing.assert_array_equal(st.view(np.uint8).reshape(len(apps), -1), os_.view(np.uint8).reshape(len(apps), -1))

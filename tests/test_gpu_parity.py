@@ -12,7 +12,7 @@ import torch
 from oracle import oracle as O
 from paper_1712_04495_b200 import batch as B
 from paper_1712_04495_b200.tracegen import CONFIGS, GenParams, as_u32x4, generate
-from util import NEVER, POLICIES, floats_equal, golden
+from util import NEVER, POLICIES, criterion5_flags, criterion5_queues, floats_equal, golden
 
 pytestmark = pytest.mark.gpu
 
@@ -47,8 +47,17 @@ def check_against_oracle(apps, caps, dev, policies=POLICIES):
     end = res.ticks("end").reshape(len(res.policies), *apps.shape[:2])
     mem = res.mem_pct.cpu().numpy()
     devp = res.dev_pct.cpu().numpy()
+    spd = res.speedup.cpu().numpy()
+    ndev = len(caps)
+    seq = O.seq_ticks(apps, ndev)
+    dv = (apps[..., 3] >> 8) & 0xFF if ndev > 1 else np.zeros(apps.shape[:2], np.uint32)
+    dv = np.where(dv < ndev, dv, 0)
+    cnt = np.stack([(dv == d).sum(axis=1) for d in range(ndev)], axis=1)
     for pi, pol in enumerate(res.policies):
         g, e, s = O.simulate_burst(apps, caps, pol.value)
+        want = O.speedup_from(seq, s["makespan"], cnt)
+        assert np.array_equal(np.isnan(spd[pi]), np.isnan(want)), pol
+        assert floats_equal(np.nan_to_num(spd[pi]), np.nan_to_num(want)), f"speedup {pol}"
         np.testing.assert_array_equal(grant[pi], g, err_msg=f"grant {pol}")
         np.testing.assert_array_equal(end[pi], e, err_msg=f"end {pol}")
         for f in ("makespan", "busy", "mem_integral", "grants", "pops", "max_holders",
@@ -75,8 +84,11 @@ def test_golden_burst(cname, cuda):
     end = res.ticks("end").reshape(4, n_tr, n)
     mem = res.mem_pct.cpu().numpy()[..., 0]
     devp = res.dev_pct.cpu().numpy()[..., 0]
+    spd = res.speedup.cpu().numpy()[..., 0]
     for pi, pol in enumerate(POLICIES):
         assert res.policies[pi].value == pol
+        # speed-up vs sequential, as the reference computes it (bit-exact)
+        assert floats_equal(spd[pi], z[f"{cname}_{pol}_speedup"]), pol
         np.testing.assert_array_equal(grant[pi], z[f"{cname}_{pol}_grant"])
         np.testing.assert_array_equal(end[pi], z[f"{cname}_{pol}_end"])
         np.testing.assert_array_equal(st[pi][:, 0]["makespan"], z[f"{cname}_{pol}_T"])
@@ -114,7 +126,9 @@ def test_golden_multidev(cuda):
     n_tr, n = apps.shape[:2]
     mem = res.mem_pct.cpu().numpy()
     devp = res.dev_pct.cpu().numpy()
+    spd = res.speedup.cpu().numpy()
     for pi, pol in enumerate(POLICIES):
+        assert floats_equal(spd[pi], z[f"{pol}_speedup"]), pol
         np.testing.assert_array_equal(res.ticks("grant")[pi].reshape(n_tr, n), z[f"{pol}_grant"])
         np.testing.assert_array_equal(res.ticks("end")[pi].reshape(n_tr, n), z[f"{pol}_end"])
         np.testing.assert_array_equal(st[pi]["makespan"], z[f"{pol}_T"])
@@ -266,7 +280,8 @@ def test_ragged_offsets(cuda):
     offs = np.zeros(len(lens) + 1, dtype=np.int64)
     np.cumsum(lens, out=offs[1:])
     res = B.simulate_batch(to_dev(flat, cuda), POLICIES, 184_320,
-                           trace_offsets=torch.from_numpy(offs).to(cuda))
+                           trace_offsets=torch.from_numpy(offs).to(cuda),
+                           apps_total=total, max_apps=int(lens.max()))
     torch.cuda.synchronize()
     st = res.stats()
     for pi, pol in enumerate(res.policies):
@@ -524,3 +539,77 @@ def test_cuda_graph_replay_beside_its_capture_stream(cuda):
             _, e, sref = O.simulate_burst(apps, cfg.cap_mib, pol.value)
             np.testing.assert_array_equal(res.ticks("end")[pi].reshape(e.shape), e)
             np.testing.assert_array_equal(res.stats()[pi].view(np.uint8), sref.view(np.uint8))
+
+
+def test_bad_device_index_flagged(cuda):
+    """ndev > 1: an app whose device index is >= ndev runs on device 0 and
+    sets SG_ST_BAD_DEVICE on every record of its trace (both engines, the
+    oracle restates the same; check_against_oracle compares status)."""
+    cfg = CONFIGS["C5"]
+    apps = as_u32x4(generate(cfg.gen, 0, 64)).copy()
+    apps[5, 7, 3] = (apps[5, 7, 3] & 0xFF) | (200 << 8)
+    apps[9, 0, 3] = (apps[9, 0, 3] & 0xFF) | (8 << 8)
+    res = check_against_oracle(apps, cfg.cap_mib, cuda)
+    st = res.stats()
+    bad = (st["status"] & 0x4) != 0
+    assert bad[:, [5, 9], :].all()
+    assert bad.sum() == 2 * len(POLICIES) * cfg.ndev
+
+
+def test_ragged_graph_capture(cuda):
+    """A CSR (ragged) batch with apps_total / max_apps given makes no host
+    read of device memory, so it captures into a CUDA graph and replays."""
+    rng = np.random.default_rng(21)
+    lens = rng.integers(0, 70, 500)
+    total = int(lens.sum())
+    flat = as_u32x4(generate(GenParams(seed=8, apps_per_trace=total), 0, 1))[0]
+    offs = np.zeros(len(lens) + 1, dtype=np.int64)
+    np.cumsum(lens, out=offs[1:])
+    a_t = to_dev(flat, cuda)
+    o_t = torch.from_numpy(offs).to(cuda)
+    kw = dict(trace_offsets=o_t, apps_total=total, max_apps=int(lens.max()))
+    B.simulate_batch(a_t, POLICIES, 184_320, **kw)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        res = B.simulate_batch(a_t, POLICIES, 184_320, stream=s, **kw)
+    res.end.fill_(0)
+    g.replay()
+    torch.cuda.synchronize()
+    for pi, pol in enumerate(res.policies):
+        for t in range(0, len(lens), 7):
+            a = flat[offs[t]:offs[t + 1]][None]
+            _, ee, ss = O.simulate_burst(a, (184_320,), pol.value)
+            np.testing.assert_array_equal(res.ticks("end")[pi][offs[t]:offs[t + 1]], ee[0])
+            assert res.stats()[pi][t, 0]["makespan"] == ss[0, 0]["makespan"]
+
+
+def test_device_info_reports_residency(cuda):
+    """sg_device_info: SMs and the lane kernel's resident warps per SM (C2
+    shape), the residency the persistent grid is sized for."""
+    import ctypes
+    from paper_1712_04495_b200 import _lib
+    sms, wps = ctypes.c_int(0), ctypes.c_int(0)
+    _lib.check(_lib.lib().sg_device_info(0, ctypes.byref(sms), ctypes.byref(wps)), "sg_device_info")
+    assert sms.value == torch.cuda.get_device_properties(0).multi_processor_count
+    assert 8 <= wps.value <= 64 and wps.value % 2 == 0
+
+
+def test_criterion5_select_grants_full(cuda):
+    """Acceptance criterion 5 at full size (test_acceptance.py:174-226): K4
+    on all 100,000 queues x 4 policies (seed 20260823) in one launch equals
+    the reference's select_grants everywhere (0 mismatches)."""
+    from paper_1712_04495_b200.policy import select_grants_batch
+    queues = criterion5_queues()
+    qs, fr, kinds = [], [], []
+    for sizes, prios, free in queues:
+        for code in range(4):
+            qs.append((sizes, prios))
+            fr.append(free)
+            kinds.append(code)
+    got = select_grants_batch(qs, fr, kinds)
+    flat = np.concatenate([g for g in got if len(g)])
+    want = criterion5_flags()
+    assert flat.shape == want.shape
+    assert np.array_equal(flat, want), f"{int((flat != want).sum())} entries differ"

@@ -8,7 +8,8 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from util import GOLDEN, POLICIES, floats_equal, golden
+from paper_1712_04495_b200.tracegen import CONFIGS, as_u32x4, generate
+from util import GOLDEN, POLICIES, brute_select, criterion5_flags, criterion5_queues, floats_equal, golden
 
 
 @pytest.mark.parametrize("cname", ["C1", "C2", "C3", "C4"])
@@ -124,3 +125,65 @@ def test_oracle_program_mode_reports(rec):
             names[ev["kind"][i]], 0,
             int(ev["mib"][i]) << 20 if ev["kind"][i] in (1, 2, 3, 6) else 0] for i in order]
     assert got == rec["events"]
+
+
+def test_speedup_restatement_matches_reference():
+    """Speed-up vs sequential (pkg/tests/test_harness.py:119-126): the
+    oracle's restatement from sequential ticks and makespan equals the value
+    the reference computes from its own report, bit for bit (the GPU kernels
+    implement the same expression, sgpu_tracesim.cuh speedup_ticks)."""
+    z = golden("ref_burst.npz")
+    for cname in ("C1", "C2", "C3", "C4"):
+        apps = z[f"{cname}_apps"]
+        S = O.seq_ticks(apps)[:, 0]
+        for pol in POLICIES:
+            sp = O.speedup_from(S, z[f"{cname}_{pol}_T"], np.full(len(apps), apps.shape[1]))
+            assert floats_equal(sp, z[f"{cname}_{pol}_speedup"]), (cname, pol)
+    z = golden("ref_multidev.npz")
+    apps = z["apps"]
+    nd = len(z["cap"])
+    dev = (apps[..., 3] >> 8) & 0xFF
+    cnt = np.stack([(dev == d).sum(axis=1) for d in range(nd)], axis=1)
+    for pol in POLICIES:
+        sp = O.speedup_from(O.seq_ticks(apps, nd), z[f"{pol}_T"], cnt)
+        assert floats_equal(sp, z[f"{pol}_speedup"]), pol
+
+
+def test_oracle_flags_bad_device():
+    """ndev > 1: an app whose device index is out of range is simulated on
+    device 0 and flags every record of its trace (SG_ST_BAD_DEVICE)."""
+    apps = as_u32x4(generate(CONFIGS["C5"].gen, 0, 4)).copy()
+    apps[1, 3, 3] = (apps[1, 3, 3] & 0xFF) | (9 << 8)
+    caps = CONFIGS["C5"].cap_mib
+    _, _, st = O.simulate_burst(apps, caps, "fifo")
+    assert np.all(st[1]["status"] & 0x4)
+    assert not np.any(st[[0, 2, 3]]["status"] & 0x4)
+    moved = apps.copy()
+    moved[1, 3, 3] &= 0xFF   # the same app on device 0: same schedule, no flag
+    g0, e0, s0 = O.simulate_burst(moved, caps, "fifo")
+    g1, e1, s1 = O.simulate_burst(apps, caps, "fifo")
+    np.testing.assert_array_equal(g0, g1)
+    np.testing.assert_array_equal(e0, e1)
+    np.testing.assert_array_equal(s0["makespan"], s1["makespan"])
+
+
+def test_criterion5_oracle_and_brute_force():
+    """Acceptance criterion 5 (test_acceptance.py:174-226): the reference's
+    select_grants on its 100k random queues x 4 policies (fixture) equals the
+    oracle's restatement everywhere and the test's brute-force oracle on a
+    sample."""
+    queues = criterion5_queues()
+    flags = criterion5_flags()
+    k = 0
+    for qi, (sizes, prios, free) in enumerate(queues):
+        n = len(sizes)
+        for code in range(4):
+            want = flags[k:k + n]
+            k += n
+            got = O.select_grants(sizes, prios, free, code)
+            assert np.array_equal(got, want), (qi, code)
+            if qi % 50 == 0:
+                b = np.zeros(n, bool)
+                b[brute_select(sizes, prios, free, code)] = True
+                assert np.array_equal(b, want), (qi, code)
+    assert k == len(flags)
