@@ -29,6 +29,12 @@ inline int __ffs(int x) { return __builtin_ffs(x); }
 }  // namespace sg
 #endif
 
+// Host-side instrumentation point (loop iterations per simulation, used by
+// profiling tools that compile LaneSim on the host); empty otherwise.
+#ifndef SG_LANE_ITER_HOOK
+#define SG_LANE_ITER_HOOK(granting)
+#endif
+
 namespace sg {
 
 constexpr uint32_t kLaneHeapN = 20;         // busy-end heap slots per lane: 4-ary, depth 2
@@ -516,6 +522,7 @@ struct LaneSim {
             ka = KY::make(s_a[ap], KY::c_init(bw_app(bwa)), ap);
         }
         while (true) {
+            SG_LANE_ITER_HOOK(gs);
             if (!gs) {
                 // next event: a granted waiter resumes after every other entry of
                 // its tick; otherwise the smaller of the arrival / busy-end keys

@@ -45,6 +45,7 @@ __attribute__((target("avx2"))) static void expand(const uint16_t* src, uint32_t
 }
 
 int main(int argc, char** argv) {
+    setvbuf(stdout, nullptr, _IONBF, 0);
     const uint64_t PAIRS = 64ull << 20 << 2;   // 64M apps x 4 policies
     const uint64_t in_b = 1ull << 30;
     uint8_t *h_in, *d_in;
@@ -91,7 +92,7 @@ int main(int argc, char** argv) {
             std::vector<std::thread> th;
             for (int w = 0; w < nthr; w++)
                 th.emplace_back([&, w]() {
-                    const uint64_t lo = PAIRS * w / nthr, hi = PAIRS * (w + 1) / nthr;
+                    const uint64_t lo = PAIRS * w / nthr & ~15ull, hi = w + 1 == nthr ? PAIRS : PAIRS * (w + 1) / nthr & ~15ull;
                     expand(big + 2 * lo, g + lo, e + lo, hi - lo);
                     _mm_sfence();
                 });
@@ -139,7 +140,8 @@ int main(int argc, char** argv) {
                             const int s = (int)(k % R);
                             while (issued[s].load(std::memory_order_acquire) != (int64_t)k) _mm_pause();
                             while (cudaEventQuery(ev[s]) == cudaErrorNotReady) _mm_pause();
-                            const uint64_t lo = pairs_per * w / nthr, hi = pairs_per * (w + 1) / nthr;
+                            const uint64_t lo = pairs_per * w / nthr & ~15ull,
+                                           hi = w + 1 == nthr ? pairs_per : pairs_per * (w + 1) / nthr & ~15ull;
                             const uint64_t base = k * pairs_per;
                             expand(reinterpret_cast<const uint16_t*>(ring + s * S) + 2 * lo, g + base + lo,
                                    e + base + lo, hi - lo);
