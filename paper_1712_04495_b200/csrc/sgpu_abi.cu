@@ -8,6 +8,8 @@
 #include <mutex>
 #include <thread>
 #include <immintrin.h>
+#include <map>
+#include <memory>
 #include <vector>
 
 #include "sgpu_common.cuh"
@@ -177,6 +179,20 @@ struct HostChunk {
     cudaEvent_t done;
 };
 
+constexpr int kPipeBufs = 3;
+struct PipeStreams {
+    std::mutex mu;
+    cudaStream_t st[kPipeBufs] = {nullptr, nullptr, nullptr};
+};
+PipeStreams& pipe_streams(int dev) {
+    static std::mutex m;
+    static std::map<int, std::unique_ptr<PipeStreams>> all;
+    std::lock_guard<std::mutex> lk(m);
+    auto& p = all[dev];
+    if (!p) p.reset(new PipeStreams());
+    return *p;
+}
+
 // One (trace, policy) row: g = (mem != 0 && end != NEVER) ? end - busy : NEVER.
 // AVX2 with streaming stores when the row is 32-byte aligned (the grant
 // array is write-only here: no read-for-ownership traffic).
@@ -270,7 +286,7 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
         if (host_grant && v >= 0) n_dma = (uint32_t)v < s.npol ? (uint32_t)v : s.npol;
     }
     const bool derive = host_grant && n_dma < s.npol;
-    constexpr int NBUF = 3;
+    constexpr int NBUF = kPipeBufs;
     const size_t app_b = chunk_traces * napps * sizeof(sg_app);
     const size_t tick_b = (size_t)s.npol * chunk_traces * napps * sizeof(uint32_t);
     const size_t st_b = (size_t)s.npol * chunk_traces * ndev * sizeof(sg_trace_stats);
@@ -301,6 +317,12 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
             pool_tuned[cuda_device] = true;
         }
     }
+    // The pipeline's streams persist per device (created once, reused by
+    // every call: their work-counter slots stay theirs); one host-pipeline
+    // call per device at a time (they would share PCIe and host memory
+    // bandwidth anyway).
+    PipeStreams& ps = pipe_streams(cuda_device);
+    std::unique_lock<std::mutex> pipe_lk(ps.mu);
     auto cleanup = [&]() {
         for (auto& b : B) {
             if (!b.st) continue;
@@ -308,12 +330,16 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
             cudaFreeAsync(b.stats, b.st); cudaFreeAsync(b.mem, b.st); cudaFreeAsync(b.dev, b.st);
             cudaFreeAsync(b.spd, b.st);
             cudaStreamSynchronize(b.st);
-            cudaStreamDestroy(b.st);
         }
         for (auto& c : chunks) cudaEventDestroy(c.done);
+        if (pipe_lk.owns_lock()) pipe_lk.unlock();
     };
-    for (auto& b : B) {
-        e = cudaStreamCreateWithFlags(&b.st, cudaStreamNonBlocking);
+    for (int i = 0; i < NBUF; i++) {
+        Buf& b = B[i];
+        e = cudaSuccess;
+        if (!ps.st[i]) e = cudaStreamCreateWithFlags(&ps.st[i], cudaStreamNonBlocking);
+        if (e != cudaSuccess) { ps.st[i] = nullptr; cleanup(); return cuda_fail(e, "pipeline streams"); }
+        b.st = ps.st[i];
         if (e == cudaSuccess) e = cudaMallocAsync(&b.apps, app_b, b.st);
         if (e == cudaSuccess && out->grant && n_dma > 0) e = cudaMallocAsync(&b.grant, tick_b, b.st);
         if (e == cudaSuccess && out->end) e = cudaMallocAsync(&b.end, tick_b, b.st);
@@ -328,10 +354,37 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
     static const bool trace = getenv("SGPU_PIPE_TRACE") != nullptr;
     const auto tp0 = std::chrono::steady_clock::now();
     auto ms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count(); };
+    // Chunk schedule: fixed-size chunks.  SGPU_PIPE_TAPER=1 fills (first
+    // H2D + simulation before any D2H) and drains (last D2H + grant
+    // derivation) on small chunks ramping from chunk/8: measured neutral
+    // within box noise on C2 (42.4 vs 44.2 ms, then 47.3 vs 45.4 ms), so off.
+    std::vector<std::pair<uint64_t, uint64_t>> sched;
+    {
+        static const bool taper = getenv("SGPU_PIPE_TAPER") && atoi(getenv("SGPU_PIPE_TAPER")) == 1;
+        std::vector<uint64_t> head, tail;
+        uint64_t left = N;
+        if (taper && N >= 4 * chunk_traces) {
+            for (uint64_t c = chunk_traces / 8; c < chunk_traces && c > 0; c *= 2) {
+                head.push_back(c);
+                tail.push_back(c);
+                left -= 2 * c;
+            }
+        }
+        uint64_t t0 = 0;
+        for (uint64_t c : head) { sched.push_back({t0, c}); t0 += c; }
+        while (left > 0) {
+            const uint64_t c = left < chunk_traces ? left : chunk_traces;
+            sched.push_back({t0, c});
+            t0 += c;
+            left -= c;
+        }
+        for (auto it = tail.rbegin(); it != tail.rend(); ++it) { sched.push_back({t0, *it}); t0 += *it; }
+    }
     uint64_t chunk = 0;
-    for (uint64_t t0 = 0; t0 < N; t0 += chunk_traces, chunk++) {
+    for (const auto& sc : sched) {
+        const uint64_t t0 = sc.first, nt = sc.second;
         Buf& b = B[chunk % NBUF];
-        const uint64_t nt = (N - t0 < chunk_traces) ? N - t0 : chunk_traces;
+        chunk++;
         const uint64_t a0 = t0 * napps, na = nt * napps;
         e = cudaMemcpyAsync(b.apps, in->apps + a0, na * sizeof(sg_app), cudaMemcpyHostToDevice, b.st);
         if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "H2D apps"); }
@@ -409,7 +462,7 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
                     const double tr = ms();
                     const uint64_t lo = c.t0 + c.nt * w / nthr, hi = c.t0 + c.nt * (w + 1) / nthr;
                     derive_grants(in, out, n_dma, s.npol, lo, hi, ov[w], avx2);
-                    if (trace && w == 0) fprintf(stderr, "[pipe] chunk %llu ready %.2f derived %.2f ms\n", (unsigned long long)(c.t0 / chunk_traces), tr, ms());
+                    if (trace && w == 0) fprintf(stderr, "[pipe] chunk at trace %llu ready %.2f derived %.2f ms\n", (unsigned long long)c.t0, tr, ms());
                 }
             });
         }

@@ -103,30 +103,43 @@ int main(int argc, char** argv) {
         }
         cudaFreeHost(big);
     }
-    // ring
-    const uint64_t slot_sizes[] = {1u << 20, 2u << 20, 4u << 20, 8u << 20, 32u << 20};
-    const int ring_ns[] = {4, 8, 16};
+    // ring v2: slot k is expanded by thread k % nthr alone (no per-slot
+    // split, no cross-thread counters on the slot), R = slots_per_thread *
+    // nthr; optionally a fraction of the policies copied directly as u32
+    // grant + end into the final arrays (PCIe 8 B, host DRAM 8 B per app-
+    // policy) instead of packed 16-bit pairs through the ring
+    const uint64_t slot_sizes[] = {512u << 10, 1u << 20, 2u << 20};
+    const int per_thr[] = {2, 4};
+    const double directs[] = {0.0, 0.25};
+    for (double fdir : directs)
     for (uint64_t S : slot_sizes) {
-        for (int R : ring_ns) {
-            if ((uint64_t)R * S > (256u << 20)) continue;
+        for (int spt : per_thr) {
+            const int R = spt * nthr;
             uint8_t* ring;
             CK(cudaMallocHost(&ring, R * S));
             memset(ring, 0, R * S);
             std::vector<cudaEvent_t> ev(R);
             for (auto& x : ev) CK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
-            const uint64_t nchunks = PAIRS * 4 / S;
+            const uint64_t dir_pairs = (uint64_t)(PAIRS * fdir) & ~((S / 4) - 1);
+            const uint64_t ring_pairs = PAIRS - dir_pairs;
+            const uint64_t nchunks = ring_pairs * 4 / S;
             const uint64_t pairs_per = S / 4;
+            cudaStream_t s_dir;
+            CK(cudaStreamCreateWithFlags(&s_dir, cudaStreamNonBlocking));
             for (int rep = 0; rep < 2; rep++) {
-                std::vector<std::atomic<int>> done(R);
-                std::vector<std::atomic<int64_t>> issued(R);
-                for (int i = 0; i < R; i++) { done[i] = nthr; issued[i] = -1; }
+                std::vector<std::atomic<int64_t>> freed(R), issued(R);
+                for (int i = 0; i < R; i++) { freed[i] = -1; issued[i] = -1; }
                 double t0 = now();
                 CK(cudaMemcpyAsync(d_in, h_in, in_b, cudaMemcpyHostToDevice, s_in));
+                if (dir_pairs) {  // u32 grant + end of the direct policies (sources: any device bytes)
+                    CK(cudaMemcpyAsync(g + ring_pairs, d_src, dir_pairs * 4, cudaMemcpyDeviceToHost, s_dir));
+                    CK(cudaMemcpyAsync(e + ring_pairs, d_src, dir_pairs * 4, cudaMemcpyDeviceToHost, s_dir));
+                }
                 std::thread coord([&]() {
                     for (uint64_t k = 0; k < nchunks; k++) {
                         const int s = (int)(k % R);
-                        while (done[s].load(std::memory_order_acquire) < nthr) _mm_pause();
-                        done[s].store(0, std::memory_order_relaxed);
+                        // the slot's previous chunk (k - R) must be expanded
+                        while (k >= (uint64_t)R && freed[s].load(std::memory_order_acquire) != (int64_t)(k - R)) _mm_pause();
                         CK(cudaMemcpyAsync(ring + s * S, reinterpret_cast<uint8_t*>(d_src) + k * S, S,
                                            cudaMemcpyDeviceToHost, s_out));
                         CK(cudaEventRecord(ev[s], s_out));
@@ -136,27 +149,26 @@ int main(int argc, char** argv) {
                 std::vector<std::thread> th;
                 for (int w = 0; w < nthr; w++)
                     th.emplace_back([&, w]() {
-                        for (uint64_t k = 0; k < nchunks; k++) {
+                        for (uint64_t k = w; k < nchunks; k += nthr) {
                             const int s = (int)(k % R);
                             while (issued[s].load(std::memory_order_acquire) != (int64_t)k) _mm_pause();
-                            while (cudaEventQuery(ev[s]) == cudaErrorNotReady) _mm_pause();
-                            const uint64_t lo = pairs_per * w / nthr & ~15ull,
-                                           hi = w + 1 == nthr ? pairs_per : pairs_per * (w + 1) / nthr & ~15ull;
+                            CK(cudaEventSynchronize(ev[s]));
                             const uint64_t base = k * pairs_per;
-                            expand(reinterpret_cast<const uint16_t*>(ring + s * S) + 2 * lo, g + base + lo,
-                                   e + base + lo, hi - lo);
-                            done[s].fetch_add(1, std::memory_order_acq_rel);
+                            expand(reinterpret_cast<const uint16_t*>(ring + s * S), g + base, e + base, pairs_per);
+                            freed[s].store((int64_t)k, std::memory_order_release);
                         }
                         _mm_sfence();
                     });
                 coord.join();
                 for (auto& t : th) t.join();
                 CK(cudaStreamSynchronize(s_in));
+                CK(cudaStreamSynchronize(s_dir));
                 double t1 = now();
                 if (rep == 1)
-                    printf("ring S=%5.1f MB R=%2d (%.0f MB), %d threads + 1 GiB h2d: %.1f ms\n", S / 1048576.0, R,
-                           R * S / 1048576.0, nthr, (t1 - t0) * 1e3);
+                    printf("ring2 S=%5.2f MB R=%2d (%.0f MB) direct %.2f, %d threads + 1 GiB h2d: %.1f ms\n",
+                           S / 1048576.0, R, R * S / 1048576.0, fdir, nthr, (t1 - t0) * 1e3);
             }
+            cudaStreamDestroy(s_dir);
             for (auto& x : ev) cudaEventDestroy(x);
             cudaFreeHost(ring);
         }
