@@ -111,6 +111,7 @@ static int simulate_device(const sg_batch* in, const sg_out* out, cudaStream_t s
     p.n_traces = in->n_traces;
     p.trace_offsets = in->trace_offsets;
     p.apps_per_trace = in->apps_per_trace;
+    p.max_apps = in->trace_offsets ? in->max_apps : in->apps_per_trace;
     p.n_pad = s.n_pad;
     p.apps = in->apps;
     p.steps = in->steps;
@@ -139,9 +140,13 @@ static int simulate_device(const sg_batch* in, const sg_out* out, cudaStream_t s
     const bool want_warp = eng && strcmp(eng, "warp") == 0;
     const bool want_lane = eng && strcmp(eng, "lane") == 0;
     const bool lane_ok = sg::lane_eligible(p, s.program, s.f64, want_lane);
-    if (want_lane && !lane_ok) return fail(E_ARG, "SGPU_K1=lane: batch not eligible for the lane kernel");
+    const bool prog_ok = sg::prog_lane_eligible(p, s.program, s.f64, want_lane);
+    if (want_lane && !lane_ok && !prog_ok) return fail(E_ARG, "SGPU_K1=lane: batch not eligible for a lane kernel");
     cudaError_t e;
-    if (lane_ok && !want_warp) {
+    if (prog_ok && !want_warp) {
+        e = sg::launch_sim_prog_lane(p, stream, nullptr);
+        if (e != cudaSuccess) return cuda_fail(e, "trace_prog_lane launch");
+    } else if (lane_ok && !want_warp) {
         e = sg::launch_sim_lane(p, stream, nullptr);
         if (e != cudaSuccess) return cuda_fail(e, "trace_sim_lane launch");
     } else {

@@ -15,6 +15,7 @@ struct SimParams {
     uint64_t n_traces;
     const uint64_t* trace_offsets;  // optional CSR
     uint32_t apps_per_trace;
+    uint32_t max_apps;              // upper bound of apps per trace
     uint32_t n_pad;                 // per-warp app capacity (multiple of 32)
     const sg_app* apps;
     const sg_step* steps;           // program mode
@@ -83,6 +84,10 @@ cudaError_t launch_sim(const SimParams& p, bool program_mode, bool f64, cudaStre
 // (sgpu_lane.cu), with an in-kernel exact fallback to TraceSim.
 bool lane_eligible(const SimParams& p, bool program_mode, bool f64, bool forced);
 cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_out);
+// K1 v6: lane-per-(trace, policy) kernel for step-program tick-mode batches
+// (sgpu_proglane.cu), with an in-kernel exact fallback to TraceSim.
+bool prog_lane_eligible(const SimParams& p, bool program_mode, bool f64, bool forced);
+cudaError_t launch_sim_prog_lane(const SimParams& p, cudaStream_t stream, int* grid_out);
 // Resident warps per SM of the lane kernel for a C2-shaped batch (64 apps, 4
 // policies, 1 device) on the current device (sg_device_info).
 cudaError_t lane_warps_per_sm(int* warps);

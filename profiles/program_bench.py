@@ -1,8 +1,9 @@
 """Step-program mode throughput: the reference's
 multi-phase builtin profiles (memshare/harness.py:65-83: ara-like,
 mummer-like, blast-like) as step programs, one batch of many traces on one
-B200 through simulate_batch (K1 warp kernel, program mode), checked
-bit-exactly against the oracle on a sample.
+B200 through simulate_batch (default engine: K1 v6 lane-per-simulation
+kernel; SGPU_K1=warp: the warp-per-trace kernel), checked bit-exactly
+against the oracle on a sample.
 
 Each trace is the acceptance workload shape (test_acceptance.py:229-246:
 4 ara + 4 mummer (priority 2) + 4 blast on a 2400 MiB device) with a seeded
@@ -97,7 +98,9 @@ def main():
             g, e, s = O.simulate_program(steps[s0:s1], so[t * n:(t + 1) * n + 1] - s0, attr[t], cap, pol)
             assert np.array_equal(grant[pi, t], g) and np.array_equal(end[pi, t], e), (pol, t)
             assert np.array_equal(st[pi, t].view(np.uint8), s.view(np.uint8)), (pol, t)
-    print(f"program mode: {n_traces} traces x {n} apps ({len(steps) // n_traces} steps/trace) x "
+    import os as _os
+    eng = _os.environ.get("SGPU_K1", "auto")
+    print(f"program mode [{eng}]: {n_traces} traces x {n} apps ({len(steps) // n_traces} steps/trace) x "
           f"{len(POLICIES)} policies: {ms:.1f} ms per launch = "
           f"{n_traces * len(POLICIES) / ms * 1e3:.3g} trace-sims/s; 64-trace oracle sample bit-exact")
 

@@ -613,3 +613,64 @@ def test_criterion5_select_grants_full(cuda):
     want = criterion5_flags()
     assert flat.shape == want.shape
     assert np.array_equal(flat, want), f"{int((flat != want).sum())} entries differ"
+
+
+# ------------------------------------------------------------ step programs
+
+def _program_batch(rng, n_traces, n, long_every=0, huge_every=0):
+    """Random multi-phase programs (tests/test_proglanesim_host.py
+    random_trace), n apps per trace, as one simulate_batch in step-program
+    mode.  long_every: every k-th trace gets more steps than a lane slot
+    holds; huge_every: every k-th trace has a cpu step near 2^32 ticks (time
+    overflow: the warp engine's status flag)."""
+    from test_proglanesim_host import random_trace
+    steps, so, attr = [], [0], []
+    per = []
+    for t in range(n_traces):
+        st, first, prio = random_trace(rng, n, max_phases=4 if not (long_every and t % long_every == 0) else 40)
+        if huge_every and t % huge_every == 0:
+            st = [(0, 0, 0xFFFFFFF0), (2, 0, 100)] + st   # app 0 runs past 2^32 - 2 ticks
+            first = [0] + [f + 2 for f in first[1:]]
+        base = len(steps)
+        steps.extend(st)
+        so.extend(base + f for f in first[1:])
+        attr.append(prio)
+        per.append((st, first, prio))
+    steps_a = np.array(steps, dtype=B.STEP_DTYPE)
+    return steps_a, np.array(so, np.uint32), np.array(attr, np.uint32), per
+
+
+@pytest.mark.parametrize("n,long_every,huge_every", [(5, 0, 0), (12, 7, 0), (16, 0, 11), (17, 0, 0), (32, 5, 9)])
+def test_program_batches_against_oracle(n, long_every, huge_every, cuda, engine):
+    """Step-program batches on both engines (auto: the K1 v6 lane-per-
+    simulation kernel, with its in-kernel warp fallback for traces longer
+    than a slot and for time overflows; warp: K1 v3) against the oracle's
+    program mode, every output bit-exact."""
+    rng = np.random.default_rng(n * 7 + long_every)
+    nt = 300
+    steps, so, attr, per = _program_batch(rng, nt, n, long_every, huge_every)
+    apps = np.zeros((nt, n, 4), np.uint32)
+    apps[..., 3] = attr
+    cap = 700
+    res = B.simulate_batch(to_dev(apps, cuda), POLICIES, cap,
+                           steps=torch.from_numpy(steps.view(np.int32).reshape(-1, 4).copy()).to(cuda),
+                           step_offsets=torch.from_numpy(so.view(np.int32).copy()).to(cuda))
+    torch.cuda.synchronize()
+    st = res.stats()
+    grant = res.ticks("grant").reshape(4, nt, n)
+    end = res.ticks("end").reshape(4, nt, n)
+    spd = res.speedup.cpu().numpy()
+    for pi, pol in enumerate(POLICIES):
+        for t, (s_, first, prio) in enumerate(per):
+            if huge_every and t % huge_every == 0:
+                # times past 2^32 - 2 ticks: flagged (the drop-in then raises)
+                assert st[pi, t, 0]["status"] & 1, (pol, t)
+                continue
+            sa = np.array(s_, dtype=O.STEP_DTYPE) if s_ else np.zeros(0, O.STEP_DTYPE)
+            g, e, s = O.simulate_program(sa, np.array(first, np.uint32), np.array(prio, np.uint32), cap, pol)
+            np.testing.assert_array_equal(grant[pi, t], g, err_msg=f"grant {pol} {t}")
+            np.testing.assert_array_equal(end[pi, t], e, err_msg=f"end {pol} {t}")
+            assert st[pi, t, 0].tobytes() == s[0].tobytes(), (pol, t, st[pi, t, 0], s[0])
+            seq = sum(d for op, _, d in s_ if op in (0, 2))
+            want = O.speedup_from(np.array([seq]), s["makespan"][:1], np.array([n]))
+            assert floats_equal(spd[pi, t, :1], want), (pol, t)
