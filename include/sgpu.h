@@ -12,6 +12,9 @@
  *                               fused as per-trace integer statistics)
  *                            batched: one warp per (trace, policy)
  *   sg_simulate_batch_host   same, host buffers, chunked H2D/compute/D2H pipeline
+ *   sg_simulate_small_host   same, host buffers, a few traces at the lowest
+ *                            latency (one H2D, one launch, one D2H): the
+ *                            drop-in simulate(spec) of one workload
  *   sg_select_grants_batch   replaces memshare/policy.py:52-74 select_grants
  *   sg_reduce_stats          new: aggregate statistics over traces (no reference
  *                            counterpart; feeds the single cross-GPU collective)
@@ -248,6 +251,16 @@ int sg_simulate_batch(const sg_batch* in, const sg_out* out, void* stream);
  * overlapping the three with streams.  Synchronous.  Event logs unsupported. */
 int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_device,
                            uint64_t chunk_traces);
+
+/* Host-buffer simulation of a few traces with the lowest latency (the
+ * drop-in simulate(spec) path, memshare/harness.py:475-572): any mode the
+ * device call supports (step programs, float64 time, event logs), fixed
+ * apps_per_trace (no trace_offsets).  Inputs are packed into one pinned
+ * staging buffer and copied in one H2D, simulated, and every requested
+ * output comes back in one D2H; staging, device buffers and the stream are
+ * kept per calling thread and device.  Synchronous.  Event slots past a
+ * trace's count are zero. */
+int sg_simulate_small_host(const sg_batch* in, const sg_out* out, int cuda_device);
 
 /* Reduce `count` sg_trace_stats records into *out (device pointer, overwritten). */
 int sg_reduce_stats(const sg_trace_stats* stats, uint64_t count, sg_aggr* out,

@@ -35,8 +35,8 @@ ST_ZERO_SPAN_LEVEL = 0x10
 NEVER = 0xFFFFFFFF
 
 EXPORTS = ("sg_abi_version", "sg_last_error", "sg_device_info", "sg_simulate_batch",
-           "sg_simulate_batch_host", "sg_reduce_stats", "sg_generate_traces",
-           "sg_select_grants_batch")
+           "sg_simulate_batch_host", "sg_simulate_small_host", "sg_reduce_stats",
+           "sg_generate_traces", "sg_select_grants_batch")
 
 P = ctypes.c_void_p
 U32 = ctypes.c_uint32
@@ -91,6 +91,7 @@ def _load():
     L.sg_simulate_batch.argtypes = [ctypes.POINTER(SgBatch), ctypes.POINTER(SgOut), P]
     L.sg_simulate_batch_host.argtypes = [ctypes.POINTER(SgBatch), ctypes.POINTER(SgOut),
                                          ctypes.c_int, U64]
+    L.sg_simulate_small_host.argtypes = [ctypes.POINTER(SgBatch), ctypes.POINTER(SgOut), ctypes.c_int]
     L.sg_reduce_stats.argtypes = [P, U64, P, P]
     L.sg_generate_traces.argtypes = [ctypes.POINTER(SgGenParams), U64, U64, P, P]
     L.sg_select_grants_batch.argtypes = [U64, P, P, P, P, P, P, P]

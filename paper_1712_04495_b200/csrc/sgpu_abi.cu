@@ -1,5 +1,6 @@
 // sgpu_abi.cu — extern "C" entry points of libsgpu.so (include/sgpu.h):
 // argument validation, kernel dispatch, and the host-buffer pipeline.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -506,6 +507,129 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
                 memcpy(static_cast<uint32_t*>(out->grant) + (uint64_t)p * n_apps_total + overflow[k] * napps,
                        &g[((uint64_t)p * no + k) * napps], napps * sizeof(uint32_t));
     }
+    return 0;
+}
+
+// ---------------------------------------------------------------- small batches
+
+namespace {
+// Per (thread, device): a stream, pinned staging for inputs and outputs, and
+// a device buffer, grown on demand and kept for the thread's lifetime.
+struct SmallCtx {
+    cudaStream_t st = nullptr;
+    uint8_t* h_in = nullptr;
+    uint8_t* h_out = nullptr;
+    uint8_t* d_buf = nullptr;
+    size_t cap_in = 0, cap_out = 0, cap_d = 0;
+};
+thread_local std::map<int, SmallCtx> t_small;
+
+inline size_t al16(size_t x) { return (x + 15u) & ~(size_t)15u; }
+
+cudaError_t small_grow(SmallCtx& c, size_t in_b, size_t out_b) {
+    cudaError_t e = cudaSuccess;
+    if (!c.st) e = cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking);
+    if (e == cudaSuccess && in_b > c.cap_in) {
+        if (c.h_in) cudaFreeHost(c.h_in);
+        c.cap_in = std::max<size_t>(in_b, 1u << 16);
+        e = cudaMallocHost(reinterpret_cast<void**>(&c.h_in), c.cap_in);
+        if (e != cudaSuccess) { c.h_in = nullptr; c.cap_in = 0; }
+    }
+    if (e == cudaSuccess && out_b > c.cap_out) {
+        if (c.h_out) cudaFreeHost(c.h_out);
+        c.cap_out = std::max<size_t>(out_b, 1u << 16);
+        e = cudaMallocHost(reinterpret_cast<void**>(&c.h_out), c.cap_out);
+        if (e != cudaSuccess) { c.h_out = nullptr; c.cap_out = 0; }
+    }
+    if (e == cudaSuccess && in_b + out_b > c.cap_d) {
+        if (c.d_buf) {
+            cudaStreamSynchronize(c.st);
+            cudaFree(c.d_buf);
+        }
+        c.cap_d = std::max<size_t>(in_b + out_b, 1u << 17);
+        e = cudaMalloc(reinterpret_cast<void**>(&c.d_buf), c.cap_d);
+        if (e != cudaSuccess) { c.d_buf = nullptr; c.cap_d = 0; }
+    }
+    return e;
+}
+}  // namespace
+
+int sg_simulate_small_host(const sg_batch* in, const sg_out* out, int cuda_device) {
+    Shape s;
+    int rc = validate(in, s);
+    if (rc) return rc;
+    if (!out || !out->stats) return fail(E_ARG, "sg_out.stats is required");
+    if (in->trace_offsets) return fail(E_ARG, "sg_simulate_small_host takes fixed-length traces");
+    if (in->n_traces == 0) return 0;
+    if (s.program && !in->step_offsets) return fail(E_ARG, "steps given without step_offsets");
+    cudaError_t e = cudaSetDevice(cuda_device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    const uint64_t nt = in->n_traces, A = nt * in->apps_per_trace;
+    const uint32_t npol = s.npol, ndev = in->ndev;
+    const size_t tsz = s.f64 ? 8 : 4, rec = s.f64 ? sizeof(sg_trace_stats_f64) : sizeof(sg_trace_stats);
+    // input region: apps | step_offsets | steps
+    uint64_t n_steps = 0;
+    uint32_t so0 = 0;
+    if (s.program) {
+        so0 = in->step_offsets[0];
+        n_steps = in->step_offsets[A] - so0;
+    }
+    const size_t o_apps = 0, o_so = al16(A * sizeof(sg_app)),
+                 o_steps = al16(o_so + (s.program ? (A + 1) * 4 : 0)),
+                 in_b = al16(o_steps + n_steps * sizeof(sg_step));
+    // output region
+    const uint64_t nrec = (uint64_t)npol * nt * ndev;
+    const size_t o_grant = 0, o_end = al16(out->grant ? npol * A * tsz : 0);
+    const size_t o_stats = al16(o_end + (out->end ? npol * A * tsz : 0));
+    const size_t o_mem = al16(o_stats + nrec * rec);
+    const size_t o_dev = al16(o_mem + (out->mem_pct ? nrec * 8 : 0));
+    const size_t o_spd = al16(o_dev + (out->dev_pct ? nrec * 8 : 0));
+    const size_t o_ev = al16(o_spd + (out->speedup ? nrec * 8 : 0));
+    const size_t ev_b = out->events ? (size_t)npol * nt * out->events_per_trace * sizeof(sg_event) : 0;
+    const size_t o_cnt = al16(o_ev + ev_b);
+    const size_t out_b = al16(o_cnt + (out->event_counts ? npol * nt * 4 : 0));
+    SmallCtx& c = t_small[cuda_device];
+    e = small_grow(c, in_b, out_b);
+    if (e != cudaSuccess) return cuda_fail(e, "small-batch buffers");
+    memcpy(c.h_in + o_apps, in->apps, A * sizeof(sg_app));
+    if (s.program) {
+        uint32_t* so = reinterpret_cast<uint32_t*>(c.h_in + o_so);
+        for (uint64_t i = 0; i <= A; i++) so[i] = in->step_offsets[i] - so0;
+        memcpy(c.h_in + o_steps, in->steps, n_steps * sizeof(sg_step));
+    }
+    uint8_t* d_in = c.d_buf;
+    uint8_t* d_out = c.d_buf + in_b;
+    e = cudaMemcpyAsync(d_in, c.h_in, in_b, cudaMemcpyHostToDevice, c.st);
+    if (e == cudaSuccess && ev_b) e = cudaMemsetAsync(d_out + o_ev, 0, ev_b, c.st);
+    if (e != cudaSuccess) return cuda_fail(e, "small-batch H2D");
+    sg_batch b = *in;
+    b.apps = reinterpret_cast<const sg_app*>(d_in + o_apps);
+    b.steps = s.program ? reinterpret_cast<const sg_step*>(d_in + o_steps) : nullptr;
+    b.step_offsets = s.program ? reinterpret_cast<const uint32_t*>(d_in + o_so) : nullptr;
+    sg_out o;
+    memset(&o, 0, sizeof(o));
+    o.grant = out->grant ? d_out + o_grant : nullptr;
+    o.end = out->end ? d_out + o_end : nullptr;
+    o.stats = d_out + o_stats;
+    o.mem_pct = out->mem_pct ? reinterpret_cast<double*>(d_out + o_mem) : nullptr;
+    o.dev_pct = out->dev_pct ? reinterpret_cast<double*>(d_out + o_dev) : nullptr;
+    o.speedup = out->speedup ? reinterpret_cast<double*>(d_out + o_spd) : nullptr;
+    o.events = out->events ? reinterpret_cast<sg_event*>(d_out + o_ev) : nullptr;
+    o.event_counts = out->event_counts ? reinterpret_cast<uint32_t*>(d_out + o_cnt) : nullptr;
+    o.events_per_trace = out->events_per_trace;
+    rc = simulate_device(&b, &o, c.st, A);
+    if (rc) return rc;
+    e = cudaMemcpyAsync(c.h_out, d_out, out_b, cudaMemcpyDeviceToHost, c.st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c.st);
+    if (e != cudaSuccess) return cuda_fail(e, "small-batch D2H");
+    if (out->grant) memcpy(out->grant, c.h_out + o_grant, npol * A * tsz);
+    if (out->end) memcpy(out->end, c.h_out + o_end, npol * A * tsz);
+    memcpy(out->stats, c.h_out + o_stats, nrec * rec);
+    if (out->mem_pct) memcpy(out->mem_pct, c.h_out + o_mem, nrec * 8);
+    if (out->dev_pct) memcpy(out->dev_pct, c.h_out + o_dev, nrec * 8);
+    if (out->speedup) memcpy(out->speedup, c.h_out + o_spd, nrec * 8);
+    if (out->events) memcpy(out->events, c.h_out + o_ev, ev_b);
+    if (out->event_counts) memcpy(out->event_counts, c.h_out + o_cnt, npol * nt * 4);
     return 0;
 }
 

@@ -25,6 +25,7 @@ reference's report from the GPU's outputs:
 
 from __future__ import annotations
 
+import ctypes
 import json
 import math
 import struct
@@ -252,41 +253,65 @@ def encode_spec(spec: WorkloadSpec) -> EncodedTrace:
 
 # ------------------------------------------------------------------ simulate
 
-def _gpu_device():
+_CUDA_OK = None
+
+
+def _gpu_device() -> int:
+    """The current CUDA device index (torch's), checked once per process."""
+    global _CUDA_OK
     import torch
-    if not torch.cuda.is_available():
+    if _CUDA_OK is None:
+        _CUDA_OK = torch.cuda.is_available()
+    if not _CUDA_OK:
         raise SgpuUnavailable("simulate() runs on the GPU; no CUDA device is available")
-    return torch.device("cuda", torch.cuda.current_device())
+    return torch.cuda.current_device()
+
+
+_EVENT_DTYPE = np.dtype([("t", "<u8"), ("app", "<u2"), ("kind", "u1"), ("dev", "u1"), ("mib", "<u4")])
 
 
 def run_encoded(enc: EncodedTrace, policy) -> dict:
-    """Run one encoded trace on the GPU with the event log; returns host
-    copies of the outputs."""
-    import torch
+    """Run one encoded trace on the GPU with the event log through the C
+    ABI's small-batch call (sg_simulate_small_host: one H2D copy, one
+    launch, one D2H copy from persistent pinned staging); returns host
+    outputs."""
+    from .policy import as_policy
+    L = _lib.lib()
     dev = _gpu_device()
     n = len(enc.attr)
     apps = np.zeros((n, 4), dtype=np.uint32)
     apps[:, 3] = enc.attr
-    steps_t = torch.from_numpy(enc.steps.view(np.int32).reshape(-1, 4).copy()).to(dev)
-    offs_t = torch.from_numpy(enc.step_offsets.view(np.int32).copy()).to(dev)
-    apps_t = torch.from_numpy(apps.view(np.int32).reshape(1, n, 4).copy()).to(dev)
-    ev_cap = 2 * n + 3 * int(enc.step_offsets[-1]) + 8
-    res = simulate_batch(apps_t, (policy,), enc.cap_mib, steps=steps_t, step_offsets=offs_t,
-                         time_mode=enc.time_mode, tick_log2=enc.tick_log2,
-                         events_per_trace=ev_cap)
-    # one device->host round trip for every output of the trace
-    pct = torch.stack([res.mem_pct[0, 0, 0], res.dev_pct[0, 0, 0]])
-    host = [t.to("cpu", non_blocking=True) for t in (res.stats_raw, res.event_counts[0, 0], res.events[0, 0], pct)]
-    torch.cuda.current_stream(dev).synchronize()
-    raw = host[0].numpy()
-    dt = STATS_F64_DTYPE if res.time_mode == _lib.TIME_F64 else STATS_DTYPE
-    stats = np.ascontiguousarray(raw).view(dt).reshape(raw.shape[:3])[0, 0, 0]
-    count = int(host[1])
-    ev = host[2][:min(count, ev_cap)].numpy().copy().view(
-        np.dtype([("t", "<u8"), ("app", "<u2"), ("kind", "u1"), ("dev", "u1"),
-                  ("mib", "<u4")])).reshape(-1)
-    return {"stats": stats, "events": ev, "count": count, "ev_cap": ev_cap,
-            "mem_pct": float(host[3][0]), "dev_pct": float(host[3][1])}
+    steps = np.ascontiguousarray(enc.steps)
+    offs = np.ascontiguousarray(enc.step_offsets, dtype=np.uint32)
+    ev_cap = 2 * n + 3 * int(offs[-1]) + 8
+    f64 = enc.time_mode == _lib.TIME_F64
+    stats = np.empty(1, dtype=STATS_F64_DTYPE if f64 else STATS_DTYPE)
+    pct = np.empty(2, dtype=np.float64)
+    events = np.empty(ev_cap, dtype=_EVENT_DTYPE)
+    count = np.zeros(1, dtype=np.uint32)
+    b = _lib.SgBatch()
+    b.n_traces = 1
+    b.apps_per_trace = n
+    b.max_apps = n
+    b.apps = apps.ctypes.data
+    b.steps = steps.ctypes.data
+    b.step_offsets = offs.ctypes.data
+    b.policy_mask = 1 << as_policy(policy).code
+    b.ndev = 1
+    b.cap_mib[0] = enc.cap_mib
+    b.time_mode = enc.time_mode
+    b.tick_log2 = enc.tick_log2
+    o = _lib.SgOut()
+    o.stats = stats.ctypes.data
+    o.mem_pct = pct.ctypes.data
+    o.dev_pct = pct.ctypes.data + 8
+    o.events = events.ctypes.data
+    o.event_counts = count.ctypes.data
+    o.events_per_trace = ev_cap
+    _lib.check(L.sg_simulate_small_host(ctypes.byref(b), ctypes.byref(o), dev), "sg_simulate_small_host")
+    c = int(count[0])
+    return {"stats": stats[0], "events": events[:min(c, ev_cap)], "count": c, "ev_cap": ev_cap,
+            "mem_pct": float(pct[0]), "dev_pct": float(pct[1])}
 
 
 def _time_of(enc: EncodedTrace, raw: int) -> float:
@@ -295,9 +320,15 @@ def _time_of(enc: EncodedTrace, raw: int) -> float:
     return struct.unpack("<d", struct.pack("<Q", int(raw)))[0]
 
 
+_BYTES_KINDS = np.zeros(8, dtype=bool)
+_BYTES_KINDS[[_lib.EV_REQUEST, _lib.EV_GRANT, _lib.EV_ALLOC, _lib.EV_FREE]] = True
+
+
 def simulate(spec: WorkloadSpec) -> MetricsReport:
     """Discrete-event prediction of `spec` (memshare/harness.py:475-572) on
-    the GPU.  Deterministic; bit-identical to the reference's report."""
+    the GPU.  Deterministic; bit-identical to the reference's report.  The
+    report is assembled from the GPU's event log with numpy (every float is
+    produced by the same IEEE operation the reference performs)."""
     if not spec.instances:
         return MetricsReport(0.0, {}, [], [], 0.0, 0.0, 0, 0)
     enc = encode_spec(spec)
@@ -309,44 +340,61 @@ def simulate(spec: WorkloadSpec) -> MetricsReport:
     if status & (_lib.ST_TICK_OVERFLOW | _lib.ST_COUNTER_OVERFLOW | _lib.ST_BAD_DEVICE):
         raise _lib.SgpuError(f"simulation status 0x{status:x}")
     capacity = spec.devices[0].total_bytes
-    raw = [(_time_of(enc, int(e["t"])), int(e["app"]), int(e["kind"]), int(e["mib"]))
-           for e in out["events"]]
-    raw.sort(key=lambda x: x[0])  # stable, harness.py:567
+    ev = out["events"]
     if enc.time_mode == _lib.TIME_TICKS:
+        # t = ticks * 2^-e exactly (math.ldexp(float(ticks), -e))
+        t_all = ev["t"].astype(np.float64) * (2.0 ** -enc.tick_log2)
         t_end = math.ldexp(float(st["makespan"]), -enc.tick_log2)
     else:
+        t_all = ev["t"].view(np.float64)
         t_end = float(st["makespan_s"])
+    order = np.argsort(t_all, kind="stable")  # harness.py:567 (stable sort by t)
+    t_s = t_all[order]
+    kind = ev["kind"][order]
+    app = ev["app"][order]
+    nbytes = np.where(_BYTES_KINDS[kind], ev["mib"][order].astype(np.int64) * MIB, 0)
     makespan_s = max(t_end - 0.0, 1e-9)
+    t_ms = (t_s - 0.0) * 1000.0
+    t_ms_l, app_l, kind_l, nb_l = t_ms.tolist(), app.tolist(), kind.tolist(), nbytes.tolist()
+    names = _lib.EVENT_NAMES
+    out_events = [{"t_ms": a, "instance": b, "event": names[k], "device": 0, "bytes": c}
+                  for a, b, k, c in zip(t_ms_l, app_l, kind_l, nb_l)]
+    # every app emits start at t = 0 (index order, first in the sorted log)
+    # and at most one end: the reference's setdefault walk gives
+    # {i: {"start_ms": .., "end_ms": ..}} in index order
+    n = len(enc.attr)
+    ends = [None] * n
+    for i, a in zip(app[kind == _lib.EV_END].tolist(), t_ms[kind == _lib.EV_END].tolist()):
+        ends[i] = a
+    starts = [None] * n
+    for i, a in zip(app[kind == _lib.EV_START].tolist(), t_ms[kind == _lib.EV_START].tolist()):
+        starts[i] = a
     instances: dict[int, dict] = {}
-    out_events = []
-    mem_points = []
-    for t, idx, kind, mib in raw:
-        name = _lib.EVENT_NAMES[kind]
-        nbytes = mib * MIB if kind in (_lib.EV_REQUEST, _lib.EV_GRANT, _lib.EV_ALLOC,
-                                       _lib.EV_FREE) else 0
-        out_events.append({"t_ms": (t - 0.0) * 1000.0, "instance": idx, "event": name,
-                           "device": 0, "bytes": nbytes})
-        inst = instances.setdefault(idx, {})
-        if kind == _lib.EV_START:
-            inst["start_ms"] = t * 1000.0
-        elif kind == _lib.EV_END:
-            inst["end_ms"] = t * 1000.0
-        elif kind == _lib.EV_ALLOC:
-            mem_points.append((t, nbytes))
-        elif kind == _lib.EV_FREE:
-            mem_points.append((t, -nbytes))
-    # 100 ms memory-utilisation samples (harness.py:439-450)
-    trace = []
-    level = 0
-    pts = iter(sorted(mem_points))
-    nxt = next(pts, None)
+    for i in range(n):
+        d = {}
+        if starts[i] is not None:
+            d["start_ms"] = starts[i]
+        if ends[i] is not None:
+            d["end_ms"] = ends[i]
+        instances[i] = d
+    # 100 ms memory-utilisation samples (harness.py:439-450): the level at a
+    # sample is the sum of every alloc/free delta at or before it
+    memsel = (kind == _lib.EV_ALLOC) | (kind == _lib.EV_FREE)
+    pt_t = t_s[memsel]
+    pt_d = np.where(kind[memsel] == _lib.EV_ALLOC, nbytes[memsel], -nbytes[memsel])
+    po = np.argsort(pt_t, kind="stable")
+    pt_t = pt_t[po]
+    cum = np.concatenate(([0], np.cumsum(pt_d[po])))
+    ts = []
     t = 0.0
-    while t <= makespan_s + 1e-9:
-        while nxt is not None and nxt[0] <= t:
-            level += nxt[1]
-            nxt = next(pts, None)
-        trace.append((t * 1000.0, level / capacity))
-        t += TICK_MS / 1000.0
+    lim = makespan_s + 1e-9
+    step = TICK_MS / 1000.0
+    while t <= lim:
+        ts.append(t)
+        t += step
+    ts_a = np.array(ts)
+    level = cum[np.searchsorted(pt_t, ts_a, side="right")]
+    trace = list(zip((ts_a * 1000.0).tolist(), (level / capacity).tolist()))
     report = MetricsReport(makespan_ms=makespan_s * 1000.0, instances=instances,
                            events=out_events, mem_trace=trace,
                            avg_mem_util_pct=out["mem_pct"], avg_device_util_pct=out["dev_pct"],
