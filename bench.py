@@ -483,17 +483,18 @@ def main():
         gc.disable()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            B.simulate_batch_host(host_apps, pols, cfg.cap_mib, device=local, out=outb,
-                                  chunk_traces=args.chunk)
+            hr = B.simulate_batch_host(host_apps, pols, cfg.cap_mib, device=local, out=outb,
+                                       chunk_traces=args.chunk)
             _ = float(outb.stats["makespan"][0, 0, 0])
         dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         gc.enable()
         if ws > 1:
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e = {"value": units_per_step * e2e_steps / float(dt[0]), "unit": "traces/s",
-               "h2d_bytes_per_step": int(host_apps.nbytes), "d2h_bytes_per_step": int(outb.d2h_bytes()),
+               "h2d_bytes_per_step": hr.h2d_bytes, "d2h_bytes_per_step": hr.d2h_bytes,
                "api": "sg_simulate_batch_host (C ABI, pinned host buffers, 3-stream pipeline; "
-                      "grant ticks derived on host threads from end ticks and inputs)",
+                      "grant ticks derived on host threads from the end ticks and a 2 B/app busy16 "
+                      "side channel)",
                "steps": e2e_steps}
 
     cpu = None

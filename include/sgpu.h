@@ -248,9 +248,16 @@ int sg_simulate_batch(const sg_batch* in, const sg_out* out, void* stream);
 
 /* Host-pointer batch simulation: copies inputs to `cuda_device` in chunks of
  * chunk_traces traces (0 = automatic), simulates, copies outputs back,
- * overlapping the three with streams.  Synchronous.  Event logs unsupported. */
+ * overlapping the three with streams.  Synchronous.  Event logs unsupported.
+ * With both tick arrays requested, a chunk whose ticks all fit 16 bits
+ * crosses PCIe as packed (grant, end) u16 pairs (4 B per app and policy)
+ * and is expanded by host threads; other chunks as u32 arrays. */
 int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_device,
                            uint64_t chunk_traces);
+
+/* Bytes the calling thread's last sg_simulate_batch_host call copied host ->
+ * device and device -> host (either pointer may be NULL). */
+void sg_last_host_transfer(uint64_t* h2d_bytes, uint64_t* d2h_bytes);
 
 /* Host-buffer simulation of a few traces with the lowest latency (the
  * drop-in simulate(spec) path, memshare/harness.py:475-572): any mode the

@@ -36,7 +36,7 @@ NEVER = 0xFFFFFFFF
 
 EXPORTS = ("sg_abi_version", "sg_last_error", "sg_device_info", "sg_simulate_batch",
            "sg_simulate_batch_host", "sg_simulate_small_host", "sg_reduce_stats",
-           "sg_generate_traces", "sg_select_grants_batch")
+           "sg_generate_traces", "sg_select_grants_batch", "sg_last_host_transfer")
 
 P = ctypes.c_void_p
 U32 = ctypes.c_uint32
@@ -95,8 +95,10 @@ def _load():
     L.sg_reduce_stats.argtypes = [P, U64, P, P]
     L.sg_generate_traces.argtypes = [ctypes.POINTER(SgGenParams), U64, U64, P, P]
     L.sg_select_grants_batch.argtypes = [U64, P, P, P, P, P, P, P]
-    for name in EXPORTS[2:]:
+    L.sg_last_host_transfer.argtypes = [P, P]
+    for name in EXPORTS[2:-1]:
         getattr(L, name).restype = ctypes.c_int
+    L.sg_last_host_transfer.restype = None
     v = L.sg_abi_version()
     if v != ABI_VERSION:
         raise SgpuUnavailable(f"libsgpu ABI version {v} != expected {ABI_VERSION}")

@@ -204,7 +204,8 @@ class HostResult:
     mem_pct: Optional[np.ndarray]
     dev_pct: Optional[np.ndarray]
     speedup: Optional[np.ndarray] = None
-    h2d_bytes: int = 0            # input bytes the call copied host -> device
+    h2d_bytes: int = 0            # bytes the call copied host -> device
+    d2h_bytes: int = 0            # bytes the call copied device -> host (sg_last_host_transfer)
 
 
 class HostBuffers:
@@ -225,26 +226,6 @@ class HostBuffers:
         self.mem_pct = alloc((npol, n_traces, ndev), torch.float64) if want_pct else None
         self.dev_pct = alloc((npol, n_traces, ndev), torch.float64) if want_pct else None
         self.speedup = alloc((npol, n_traces, ndev), torch.float64) if want_speedup else None
-
-    def d2h_bytes(self) -> int:
-        """Bytes the host pipeline copies device -> host per call.  With both
-        tick arrays requested, the grants are derived on the host from the end
-        ticks and the inputs (grant = end - busy) and cross no bus
-        (sg_simulate_batch_host, csrc/sgpu_abi.cu; SGPU_GRANT_DMA=k copies the
-        first k policies' grants instead, there and here)."""
-        n = sum(a.nbytes for a in (self.end, self.stats, self.mem_pct, self.dev_pct, self.speedup)
-                if a is not None)
-        if self.grant is not None:
-            npol = self.grant.shape[0]
-            n_dma = npol
-            if self.end is not None:
-                n_dma = 0
-                env = os.environ.get("SGPU_GRANT_DMA")
-                if env is not None and int(env) >= 0:
-                    n_dma = min(int(env), npol)
-            n += self.grant[:n_dma].nbytes
-        return n
-
 
 def pinned_apps(n_traces: int, n_apps: int) -> np.ndarray:
     """A pinned (page-locked) host array for T0 records, (n_traces, n_apps, 4) uint32."""
@@ -295,9 +276,11 @@ def simulate_batch_host(apps: np.ndarray, policies: Iterable = ("fifo",), cap_mi
     o.speedup = p(out.speedup if want_speedup else None)
     rc = L.sg_simulate_batch_host(ctypes.byref(b), ctypes.byref(o), int(device), int(chunk_traces))
     _lib.check(rc, "sg_simulate_batch_host")
+    h2d, d2h = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    L.sg_last_host_transfer(ctypes.byref(h2d), ctypes.byref(d2h))
     return HostResult(ordered, out.grant if want_ticks else None, out.end if want_ticks else None,
                       out.stats, out.mem_pct if want_pct else None, out.dev_pct if want_pct else None,
-                      out.speedup if want_speedup else None, int(a.nbytes))
+                      out.speedup if want_speedup else None, int(h2d.value), int(d2h.value))
 
 
 def k1_engine(apps_per_trace: int, n_policies: int, ndev: int = 1) -> str:

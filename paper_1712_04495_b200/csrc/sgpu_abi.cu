@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <chrono>
 #include <mutex>
 #include <thread>
@@ -173,23 +174,50 @@ int sg_simulate_batch(const sg_batch* in, const sg_out* out, void* stream) {
 // The per-app grant ticks are not copied back: for T0 traces the grant is
 // the start of the busy step, so grant = end - busy for apps that request
 // memory and end, NEVER otherwise (memshare/harness.py:514-531) — host
-// threads derive it from the end ticks and the caller's own input records
-// while later chunks are still on the GPU.  That removes a third of the
-// device->host bytes (the pipeline is PCIe-bound).  Traces whose record
-// reports a tick overflow (where that identity does not hold) are
-// re-simulated with device grants afterwards.
+// threads derive it from the end ticks while later chunks are still on the
+// GPU.  The busy ticks come from a 2-byte-per-app side channel (K5 busy16:
+// 0xFFFF = no request) rather than from the caller's 16-byte records, so a
+// derivation reads 2 B of busy + 4 B of end per app and policy instead of
+// 16 B of records per app (the pipeline is bound by host memory bandwidth:
+// DESIGN.md, "End to end").  A chunk with a busy step >= 0xFFFF ticks is
+// derived from the records; traces whose record reports a tick overflow
+// (where grant = end - busy does not hold) are re-simulated with device
+// grants afterwards.
 namespace {
+
+thread_local uint64_t t_h2d = 0, t_d2h = 0;  // sg_last_host_transfer
 
 struct HostChunk {
     uint64_t t0, nt;
     cudaEvent_t done;
+    uint32_t idx;  // chunk index (pack16 overflow flag)
 };
 
-constexpr int kPipeBufs = 3;
+constexpr int kPipeBufs = 8;  // at most; SGPU_PIPE_BUFS picks (default 4)
 struct PipeStreams {
     std::mutex mu;
-    cudaStream_t st[kPipeBufs] = {nullptr, nullptr, nullptr};
+    cudaStream_t st[kPipeBufs] = {};
+    // pinned: the batch's pack16 staging (end ticks, then busy ticks, u16)
+    // and per-chunk overflow flags, grown on demand and kept
+    uint16_t* stage = nullptr;
+    size_t stage_cap = 0;
+    uint32_t* flags = nullptr;
+    size_t flags_cap = 0;
 };
+uint64_t env_u64(const char* name, uint64_t dflt) {
+    const char* v = getenv(name);
+    return v && atoll(v) > 0 ? (uint64_t)atoll(v) : dflt;
+}
+
+cudaError_t grow_pinned(void** p, size_t& cap, size_t need) {
+    if (need <= cap) return cudaSuccess;
+    if (*p) cudaFreeHost(*p);
+    *p = nullptr;
+    cap = 0;
+    const cudaError_t e = cudaMallocHost(p, need);
+    if (e == cudaSuccess) cap = need;
+    return e;
+}
 PipeStreams& pipe_streams(int dev) {
     static std::mutex m;
     static std::map<int, std::unique_ptr<PipeStreams>> all;
@@ -223,8 +251,68 @@ void grant_row_scalar(const uint32_t* mem, const uint32_t* busy, const uint32_t*
     for (uint32_t i = 0; i < n; i++) g[i] = (mem[i] != 0 && e[i] != SG_NEVER) ? e[i] - busy[i] : SG_NEVER;
 }
 
-// grant[p][a] for traces [t_lo, t_hi) of the batch; overflowing (trace,
-// policy) pairs are skipped and reported.
+// One (trace, policy) row from the pack16 staging: end = e16 (0xFFFF ->
+// NEVER), grant = (b16 != 0xFFFF && e16 != 0xFFFF) ? end - busy : NEVER;
+// both written with streaming stores when `vec` (32-byte aligned rows).
+__attribute__((target("avx2"))) void tick_row16_avx2(const uint16_t* b16, const uint16_t* e16, uint32_t* g,
+                                                     uint32_t* e, uint32_t n) {
+    const __m256i never = _mm256_set1_epi32((int)SG_NEVER);
+    const __m256i none = _mm256_set1_epi32(0xFFFF);
+    uint32_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+        const __m256i bv = _mm256_cvtepu16_epi32(_mm_loadu_si128(reinterpret_cast<const __m128i*>(b16 + i)));
+        const __m256i ev = _mm256_cvtepu16_epi32(_mm_loadu_si128(reinterpret_cast<const __m128i*>(e16 + i)));
+        const __m256i en = _mm256_cmpeq_epi32(ev, none);
+        const __m256i no = _mm256_or_si256(_mm256_cmpeq_epi32(bv, none), en);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(e + i), _mm256_or_si256(ev, en));
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(g + i),
+                            _mm256_blendv_epi8(_mm256_sub_epi32(ev, bv), never, no));
+    }
+    for (; i < n; i++) {
+        e[i] = e16[i] == 0xFFFFu ? SG_NEVER : e16[i];
+        g[i] = (b16[i] != 0xFFFFu && e16[i] != 0xFFFFu) ? (uint32_t)e16[i] - b16[i] : SG_NEVER;
+    }
+}
+
+void tick_row16_scalar(const uint16_t* b16, const uint16_t* e16, uint32_t* g, uint32_t* e, uint32_t n) {
+    for (uint32_t i = 0; i < n; i++) {
+        e[i] = e16[i] == 0xFFFFu ? SG_NEVER : e16[i];
+        g[i] = (b16[i] != 0xFFFFu && e16[i] != 0xFFFFu) ? (uint32_t)e16[i] - b16[i] : SG_NEVER;
+    }
+}
+
+// end and grant ticks of traces [t_lo, t_hi) from the pack16 staging
+// (stage: npol rows of end ticks, then the busy ticks, n_apps_total each);
+// traces with a tick overflow are skipped and reported.
+void expand_ticks16(const sg_batch* in, const sg_out* out, const uint16_t* stage, uint32_t npol, uint64_t t_lo,
+                    uint64_t t_hi, std::vector<uint64_t>& overflow, bool avx2) {
+    const uint64_t N = in->n_traces;
+    const uint32_t napps = in->apps_per_trace, ndev = in->ndev;
+    const uint64_t total = N * napps;
+    const sg_trace_stats* st = static_cast<const sg_trace_stats*>(out->stats);
+    uint32_t* end = static_cast<uint32_t*>(out->end);
+    uint32_t* grant = static_cast<uint32_t*>(out->grant);
+    const uint16_t* b16 = stage + (uint64_t)npol * total;
+    const bool vec = avx2 && (napps % 8 == 0) && (reinterpret_cast<uintptr_t>(grant) & 31u) == 0 &&
+                     (reinterpret_cast<uintptr_t>(end) & 31u) == 0 && ((total * 4) & 31u) == 0;
+    for (uint64_t t = t_lo; t < t_hi; t++) {
+        bool ov = false;
+        for (uint32_t p = 0; p < npol; p++)
+            for (uint32_t d = 0; d < ndev; d++)
+                ov = ov || (st[((uint64_t)p * N + t) * ndev + d].status & SG_ST_TICK_OVERFLOW);
+        if (ov) { overflow.push_back(t); continue; }
+        for (uint32_t p = 0; p < npol; p++) {
+            const uint64_t o = (uint64_t)p * total + t * napps;
+            if (vec) tick_row16_avx2(b16 + t * napps, stage + o, grant + o, end + o, napps);
+            else tick_row16_scalar(b16 + t * napps, stage + o, grant + o, end + o, napps);
+        }
+    }
+    if (vec) _mm_sfence();
+}
+
+// grant[p][a] for traces [t_lo, t_hi) of the batch, from the end ticks and
+// the input records; overflowing (trace, policy) pairs are skipped and
+// reported.
 void derive_grants(const sg_batch* in, const sg_out* out, uint32_t p0, uint32_t npol, uint64_t t_lo, uint64_t t_hi,
                    std::vector<uint64_t>& overflow, bool avx2) {
     const uint64_t N = in->n_traces;
@@ -260,8 +348,26 @@ void derive_grants(const sg_batch* in, const sg_out* out, uint32_t p0, uint32_t 
 
 }  // namespace
 
+void sg_last_host_transfer(uint64_t* h2d_bytes, uint64_t* d2h_bytes) {
+    if (h2d_bytes) *h2d_bytes = t_h2d;
+    if (d2h_bytes) *d2h_bytes = t_d2h;
+}
+
+namespace {
+int simulate_host(const sg_batch* in, const sg_out* out, int cuda_device, uint64_t chunk_traces, bool allow_pack);
+}
+
 int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_device,
                            uint64_t chunk_traces) {
+    t_h2d = t_d2h = 0;
+    return simulate_host(in, out, cuda_device, chunk_traces, true);
+}
+
+}  // extern "C"
+
+namespace {
+
+int simulate_host(const sg_batch* in, const sg_out* out, int cuda_device, uint64_t chunk_traces, bool allow_pack) {
     Shape s;
     int rc = validate(in, s);
     if (rc) return rc;
@@ -292,7 +398,11 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
         if (host_grant && v >= 0) n_dma = (uint32_t)v < s.npol ? (uint32_t)v : s.npol;
     }
     const bool derive = host_grant && n_dma < s.npol;
-    constexpr int NBUF = kPipeBufs;
+    // All grants derived: end + busy ticks cross PCIe as u16 (K5 pack16)
+    // unless SGPU_PACK16=0; a chunk they do not fit is re-simulated after.
+    const bool use_p16 = allow_pack && derive && n_dma == 0 &&
+                         !(getenv("SGPU_PACK16") && atoi(getenv("SGPU_PACK16")) == 0);
+    const int NBUF = (int)std::min<uint64_t>(std::max<uint64_t>(env_u64("SGPU_PIPE_BUFS", 4), 2), kPipeBufs);
     const size_t app_b = chunk_traces * napps * sizeof(sg_app);
     const size_t tick_b = (size_t)s.npol * chunk_traces * napps * sizeof(uint32_t);
     const size_t st_b = (size_t)s.npol * chunk_traces * ndev * sizeof(sg_trace_stats);
@@ -305,7 +415,9 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
         uint32_t *grant = nullptr, *end = nullptr;
         sg_trace_stats* stats = nullptr;
         double *mem = nullptr, *dev = nullptr, *spd = nullptr;
-    } B[NBUF];
+        uint16_t *b16 = nullptr, *e16 = nullptr;
+        uint32_t* flag = nullptr;
+    } B[kPipeBufs];
     std::vector<HostChunk> chunks;
     // Pipeline buffers come from the device's stream-ordered memory pool
     // (cudaMallocAsync), kept cached between calls: repeated calls pay no
@@ -334,7 +446,8 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
             if (!b.st) continue;
             cudaFreeAsync(b.apps, b.st); cudaFreeAsync(b.grant, b.st); cudaFreeAsync(b.end, b.st);
             cudaFreeAsync(b.stats, b.st); cudaFreeAsync(b.mem, b.st); cudaFreeAsync(b.dev, b.st);
-            cudaFreeAsync(b.spd, b.st);
+            cudaFreeAsync(b.spd, b.st); cudaFreeAsync(b.b16, b.st); cudaFreeAsync(b.e16, b.st);
+            cudaFreeAsync(b.flag, b.st);
             cudaStreamSynchronize(b.st);
         }
         for (auto& c : chunks) cudaEventDestroy(c.done);
@@ -353,7 +466,16 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
         if (e == cudaSuccess && want_pct) e = cudaMallocAsync(&b.mem, pct_b, b.st);
         if (e == cudaSuccess && want_pct) e = cudaMallocAsync(&b.dev, pct_b, b.st);
         if (e == cudaSuccess && out->speedup) e = cudaMallocAsync(&b.spd, pct_b, b.st);
+        if (e == cudaSuccess && use_p16) e = cudaMallocAsync(&b.b16, chunk_traces * napps * 2u, b.st);
+        if (e == cudaSuccess && use_p16) e = cudaMallocAsync(&b.e16, tick_b / 2u, b.st);
+        if (e == cudaSuccess && use_p16) e = cudaMallocAsync(&b.flag, 16, b.st);
         if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "allocating pipeline buffers"); }
+    }
+    const uint64_t nch_max = (N + chunk_traces - 1) / chunk_traces;
+    if (use_p16) {
+        e = grow_pinned(reinterpret_cast<void**>(&ps.stage), ps.stage_cap, (s.npol + 1u) * N * napps * 2u);
+        if (e == cudaSuccess) e = grow_pinned(reinterpret_cast<void**>(&ps.flags), ps.flags_cap, nch_max * 4u + 64u);
+        if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "pinned pack16 staging"); }
     }
     const uint64_t n_apps_total = N * napps;
     // SGPU_PIPE_TRACE=1: print host-side pipeline timings (stderr)
@@ -394,6 +516,7 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
         const uint64_t a0 = t0 * napps, na = nt * napps;
         e = cudaMemcpyAsync(b.apps, in->apps + a0, na * sizeof(sg_app), cudaMemcpyHostToDevice, b.st);
         if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "H2D apps"); }
+        t_h2d += na * sizeof(sg_app);
         sg_batch cb = *in;
         cb.n_traces = nt;
         cb.apps = b.apps;
@@ -407,6 +530,19 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
         co.speedup = b.spd;
         rc = simulate_device(&cb, &co, b.st, na);
         if (rc) { cleanup(); return rc; }
+        if (use_p16) {  // the chunk's end + busy ticks as u16 (K5) into the pinned staging
+            e = sg::launch_pack16(b.apps, b.end, na, s.npol, b.b16, b.e16, b.flag, b.st);
+            for (uint32_t p = 0; p < s.npol && e == cudaSuccess; p++)
+                e = cudaMemcpyAsync(ps.stage + (uint64_t)p * n_apps_total + a0, b.e16 + (uint64_t)p * na, na * 2u,
+                                    cudaMemcpyDeviceToHost, b.st);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(ps.stage + (uint64_t)s.npol * n_apps_total + a0, b.b16, na * 2u,
+                                    cudaMemcpyDeviceToHost, b.st);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(ps.flags + (chunk - 1), b.flag, 4, cudaMemcpyDeviceToHost, b.st);
+            if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "K5 pack16"); }
+            t_d2h += (s.npol + 1u) * na * 2u + 4u;
+        }
         for (uint32_t p = 0; p < s.npol; p++) {
             const uint64_t ho = (uint64_t)p * n_apps_total + a0;
             const uint64_t hs = ((uint64_t)p * N + t0) * ndev;
@@ -414,7 +550,7 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
             if (b.grant && p < n_dma)
                 e = cudaMemcpyAsync(static_cast<uint32_t*>(out->grant) + ho, b.grant + (uint64_t)p * na,
                                     na * 4, cudaMemcpyDeviceToHost, b.st);
-            if (e == cudaSuccess && out->end)
+            if (e == cudaSuccess && out->end && !use_p16)
                 e = cudaMemcpyAsync(static_cast<uint32_t*>(out->end) + ho, b.end + (uint64_t)p * na,
                                     na * 4, cudaMemcpyDeviceToHost, b.st);
             if (e == cudaSuccess)
@@ -430,9 +566,11 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
                 e = cudaMemcpyAsync(out->speedup + hs, b.spd + dsrc, nt * ndev * 8,
                                     cudaMemcpyDeviceToHost, b.st);
             if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "D2H outputs"); }
+            t_d2h += (b.grant && p < n_dma ? na * 4u : 0u) + (out->end && !use_p16 ? na * 4u : 0u) +
+                     nt * ndev * (sizeof(sg_trace_stats) + 8u * (!!out->mem_pct + !!out->dev_pct + !!out->speedup));
         }
         if (derive) {
-            HostChunk c{t0, nt, nullptr};
+            HostChunk c{t0, nt, nullptr, (uint32_t)(chunk - 1)};
             e = cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming);
             if (e == cudaSuccess) e = cudaEventRecord(c.done, b.st);
             if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "chunk event"); }
@@ -467,7 +605,13 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
                     if (ce != cudaSuccess) { errs[w] = ce; return; }
                     const double tr = ms();
                     const uint64_t lo = c.t0 + c.nt * w / nthr, hi = c.t0 + c.nt * (w + 1) / nthr;
-                    derive_grants(in, out, n_dma, s.npol, lo, hi, ov[w], avx2);
+                    if (!use_p16) {
+                        derive_grants(in, out, n_dma, s.npol, lo, hi, ov[w], avx2);
+                    } else if (ps.flags[c.idx]) {  // not exact in 16 bits: re-simulated below
+                        for (uint64_t t = lo; t < hi; t++) ov[w].push_back(t);
+                    } else {
+                        expand_ticks16(in, out, ps.stage, s.npol, lo, hi, ov[w], avx2);
+                    }
                     if (trace && w == 0) fprintf(stderr, "[pipe] chunk at trace %llu ready %.2f derived %.2f ms\n", (unsigned long long)c.t0, tr, ms());
                 }
             });
@@ -485,8 +629,10 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
     }
     cleanup();
     if (!overflow.empty()) {
-        // exact grants of the (rare) tick-overflow traces: re-simulate them
-        // with device-side grant output
+        // the (rare) traces of a chunk whose ticks did not fit 16 bits (both
+        // tick arrays) or with a tick overflow (grants): re-simulate them
+        // with u32 ticks from the device
+        std::sort(overflow.begin(), overflow.end());
         const uint64_t no = overflow.size();
         std::vector<sg_app> h_apps(no * napps);
         for (uint64_t k = 0; k < no; k++)
@@ -494,21 +640,28 @@ int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_devic
         sg_batch rb = *in;
         rb.n_traces = no;
         rb.apps = h_apps.data();
-        std::vector<uint32_t> g((size_t)s.npol * no * napps);
+        std::vector<uint32_t> g((size_t)s.npol * no * napps), en(use_p16 ? (size_t)s.npol * no * napps : 0);
         std::vector<sg_trace_stats> rs((size_t)s.npol * no * ndev);
         sg_out ro;
         memset(&ro, 0, sizeof(ro));
-        ro.grant = g.data();  // no end buffer: this call copies device grants
+        ro.grant = g.data();
+        ro.end = use_p16 ? en.data() : nullptr;  // no end buffer: the call copies device grants
         ro.stats = rs.data();
-        rc = sg_simulate_batch_host(&rb, &ro, cuda_device, 0);
+        rc = simulate_host(&rb, &ro, cuda_device, 0, false);
         if (rc) return rc;
         for (uint64_t k = 0; k < no; k++)
-            for (uint32_t p = 0; p < s.npol; p++)
-                memcpy(static_cast<uint32_t*>(out->grant) + (uint64_t)p * n_apps_total + overflow[k] * napps,
-                       &g[((uint64_t)p * no + k) * napps], napps * sizeof(uint32_t));
+            for (uint32_t p = 0; p < s.npol; p++) {
+                const uint64_t o = (uint64_t)p * n_apps_total + overflow[k] * napps, r = ((uint64_t)p * no + k) * napps;
+                memcpy(static_cast<uint32_t*>(out->grant) + o, &g[r], napps * sizeof(uint32_t));
+                if (use_p16) memcpy(static_cast<uint32_t*>(out->end) + o, &en[r], napps * sizeof(uint32_t));
+            }
     }
     return 0;
 }
+
+}  // namespace
+
+extern "C" {
 
 // ---------------------------------------------------------------- small batches
 

@@ -239,3 +239,50 @@ cudaError_t launch_select(uint64_t n_queues, const uint64_t* qoff, const int64_t
 }
 
 }  // namespace sg
+
+namespace sg {
+
+// ------------------------------------------------------------ K5 pack16
+// Host pipeline transfer format of one chunk (after its simulation): per app
+// its busy ticks as u16 (0xFFFF = no memory request, hence no grant) and per
+// (policy, app) its end tick as u16 (0xFFFF = SG_NEVER).  Host threads
+// expand the end ticks into the caller's u32 array and derive every grant
+// as end - busy (sgpu_abi.cu), so 10 B per app cross PCIe instead of 16 B
+// of end ticks (and no 16-byte input record is re-read on the host).
+// *overflow = 1 if the chunk is not exactly representable (a requesting
+// app's busy >= 0xFFFF or an end tick >= 0xFFFF other than SG_NEVER): the
+// host then re-simulates it with u32 outputs.
+
+__global__ void __launch_bounds__(256)
+pack16_kernel(const uint4* __restrict__ apps, const uint32_t* __restrict__ end, uint64_t na, uint32_t npol,
+              uint16_t* __restrict__ b16, uint16_t* __restrict__ e16, uint32_t* overflow) {
+    uint32_t bad = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 f = __ldcs(apps + i);  // arrival, mem, busy, attr
+        bad |= (f.y != 0u) & (f.z >= 0xFFFFu);
+        b16[i] = f.y == 0u ? (uint16_t)0xFFFFu : (uint16_t)f.z;
+        for (uint32_t p = 0; p < npol; p++) {
+            const uint32_t e = __ldcs(end + p * na + i);
+            bad |= (e != SG_NEVER) & (e >= 0xFFFFu);
+            e16[p * na + i] = (uint16_t)(e == SG_NEVER ? 0xFFFFu : e);
+        }
+    }
+    if (__any_sync(FULL, bad != 0) && (threadIdx.x & 31) == 0) atomicOr(overflow, 1u);
+}
+
+cudaError_t launch_pack16(const sg_app* apps, const uint32_t* end, uint64_t na, uint32_t npol, uint16_t* b16,
+                          uint16_t* e16, uint32_t* overflow, cudaStream_t stream) {
+    cudaError_t e = cudaMemsetAsync(overflow, 0, sizeof(uint32_t), stream);
+    if (e != cudaSuccess || na == 0) return e;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    uint64_t blocks = (na + 255) / 256;
+    if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
+    pack16_kernel<<<(unsigned)blocks, 256, 0, stream>>>(reinterpret_cast<const uint4*>(apps), end, na, npol, b16,
+                                                         e16, overflow);
+    return cudaGetLastError();
+}
+
+}  // namespace sg

@@ -17,7 +17,7 @@ HEADER = os.path.join(ROOT, "include", "sgpu.h")
 
 def declared_functions():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(sg_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(sg_\w+)\s*\(", src, re.M)))
 
 
 def test_exports_every_declared_symbol():

@@ -354,14 +354,31 @@ def test_host_pipeline_matches_device(cuda):
     assert floats_equal(host.dev_pct, dres.dev_pct.cpu().numpy())
 
 
-@pytest.mark.parametrize("case", ["overflow", "c5", "long", "grant_only"])
+@pytest.mark.parametrize("case", ["overflow", "busy16", "end16", "c5", "long", "grant_only"])
 def test_host_pipeline_cases(case, cuda):
-    """The host pipeline derives grants on the host (end - busy); traces with
-    a tick overflow are re-simulated for exact grants; multi-device, long
+    """The host pipeline moves end and busy ticks as u16 (K5 pack16) and
+    derives the grants on the host (end - busy); a chunk they do not fit
+    exactly (a busy step >= 0xFFFF ticks, "busy16", or an end tick >= 0xFFFF,
+    "end16", beside chunks with apps that request no memory) and traces
+    with a tick overflow are re-simulated with u32 ticks; multi-device, long
     (warp-kernel) traces and a grant-only request follow the same contract."""
     rng = np.random.default_rng(21)
     caps = (184_320,)
-    if case == "overflow":
+    if case in ("busy16", "end16"):
+        # chunks of 128 traces: chunk 1 holds busy steps of 0xFFFF and more
+        # (or ends past 0xFFFF), chunk 3 apps without a memory request
+        # (busy16 = 0xFFFF marks them)
+        cfg = CONFIGS["C2"]
+        apps = as_u32x4(generate(cfg.gen, 0, 700))
+        if case == "busy16":
+            apps[130, 5, 2] = 0xFFFF
+            apps[131, 7, 2] = 0x10000
+        else:
+            apps[130, 5, 0] = 0xFFFF - apps[130, 5, 2]
+            apps[130, 5, 1] = 1
+            apps[200:202, :, 0] += 100_000
+        apps[400:402, ::3, 1] = 0
+    elif case == "overflow":
         n, nt = 40, 300
         apps = np.zeros((nt, n, 4), dtype=np.uint32)
         apps[:, :, 0] = rng.integers(0, 1000, (nt, n))
@@ -391,6 +408,27 @@ def test_host_pipeline_cases(case, cuda):
     np.testing.assert_array_equal(host.stats.view(np.uint8), dres.stats().view(np.uint8))
     if case == "overflow":
         assert (dres.stats()["status"] & 1).any()
+
+
+@pytest.mark.parametrize("thr", [1, 3])
+def test_host_pipeline_threads(thr, cuda, monkeypatch):
+    """One and three host threads deriving grants, ragged last chunk, two
+    calls in a row (the pinned busy16 staging and streams persist)."""
+    monkeypatch.setenv("SGPU_HOST_THREADS", str(thr))
+    cfg = CONFIGS["C2"]
+    apps = as_u32x4(generate(dataclasses.replace(cfg.gen, seed=77), 0, 3001))
+    dres = run(apps, POLICIES, cfg.cap_mib, cuda)
+    pin = B.pinned_apps(*apps.shape[:2])
+    pin[...] = apps
+    for _ in range(2):
+        host = B.simulate_batch_host(pin, POLICIES, cfg.cap_mib, chunk_traces=500)
+        np.testing.assert_array_equal(host.grant, dres.ticks("grant"))
+        np.testing.assert_array_equal(host.end, dres.ticks("end"))
+        np.testing.assert_array_equal(host.stats.view(np.uint8), dres.stats().view(np.uint8))
+        assert host.h2d_bytes == apps.nbytes
+        # end + busy ticks as u16 (K5 pack16), one overflow flag per chunk
+        assert host.d2h_bytes == 5 * apps.size // 2 + 4 * 7 + sum(
+            a.nbytes for a in (host.stats, host.mem_pct, host.dev_pct, host.speedup))
 
 
 def test_work_counters_across_streams_and_sizes(cuda):
@@ -467,8 +505,7 @@ def test_many_priority_classes(n, cuda):
 
 @pytest.mark.parametrize("pols", [("mmu",), ("fifo", "pfifo"), ("mmu", "pfifo", "pmmu")])
 def test_host_pipeline_policy_subsets(pols, cuda):
-    """Host-buffer pipeline with 1-3 policies (grants then all derived on the
-    host, or copied for npol // 4 of them) against the device path."""
+    """Host-buffer pipeline with 1-3 policies against the device path."""
     cfg = CONFIGS["C2"]
     apps = as_u32x4(generate(dataclasses.replace(cfg.gen, seed=41), 0, 3000))
     dres = run(apps, pols, cfg.cap_mib, cuda)
