@@ -39,7 +39,6 @@ namespace sg {
 
 constexpr uint32_t kLaneHeapN = 20;         // busy-end heap slots per lane: 4-ary, depth 2
 constexpr uint32_t kLaneHeapW = 10;         // the same 2.5 KB region with 64-bit keys (main pass)
-constexpr uint32_t kLaneFifo = 8;           // wake FIFO: 8 app positions, one byte each, in a u64 register
 // Fit table T[r] kept at every FS-th rank: every 2nd at <= 64 apps (one
 // extra position to OR in; fits C2's shared budget), every 4th above and in
 // the few-traces-per-warp variant (its staging is a larger share).
@@ -76,8 +75,7 @@ template <int K> struct LogN { static constexpr uint32_t v = K == 1 ? 5 : K == 2
 // Event keys (t, virtual counter, position).  NARROW: one u32, t << (2 LOGN
 // + 1) | counter << LOGN | q, usable when every event time of the trace is
 // below LIM = 2^(31 - 2 LOGN) - 1 (arrival max + busy sum, checked at
-// staging; time(INF) = LIM stays above every event time, which the wake-up
-// test relies on).  Each app pushes at most one busy end, so the counter of
+// staging).  Each app pushes at most one busy end, so the counter of
 // the initial pop of app i is i and later pushes count up from N (< 2N).
 // Wide: one u64, t << 32 | counter << 8 | q with the block counters
 // described above.  HW: heap capacity with 64-bit keys.
@@ -89,6 +87,7 @@ template <int K, bool NARROW, uint32_t HW = kLaneHeapW> struct LaneKey {
     static constexpr T INF = (T)~(T)0;
     static constexpr uint32_t HCAP = NARROW ? kLaneHeapN : HW;
     static constexpr uint32_t LIM = NARROW ? (1u << (32u - TS)) - 1u : ~0u;
+    static constexpr uint32_t CMAX = NARROW ? 2u << LOGN : 1u << 24;  // counters must stay below
     static SG_HD T make(uint32_t t, uint32_t c, uint32_t q) {
         return ((T)t << TS) | ((T)c << QB) | (T)q;
     }
@@ -125,9 +124,9 @@ struct LaneSim {
     uint32_t cap, used;
     bool prio_pol, mmu, fail;
     uint64_t mask[NW];
-    uint32_t hs, fhead, ftail;
+    uint32_t hs;
     Key kh;                  // heap top (KY::INF when empty)
-    uint32_t counter;
+    uint32_t counter;        // next virtual counter of a later push (from KY::c_base)
     // statistics (harness.py:373-461 integer forms)
     uint32_t last, mem_t, busy_prev, B;
     uint64_t I;
@@ -156,11 +155,11 @@ struct LaneSim {
     // 4-ary min-heap of at most kLaneHeapN = 20 keys (depth 2: root + 4 + 16
     // slots): every sift is at
     // most two levels, unrolled and predicated, and the four child loads of a
-    // level are independent
-    SG_HD void push(uint32_t t, uint32_t q) {
-        if (hs >= KY::HCAP) { fail = true; return; }
-        const Key key = KY::make(t, counter, q);
-        counter += 1;
+    // level are independent.  Entries: busy ends, and the resumption of a
+    // granted waiter without a busy step (its free).
+    SG_HD void push(uint32_t t, uint32_t c, uint32_t q) {
+        if (hs >= KY::HCAP || c >= KY::CMAX) { fail = true; return; }
+        const Key key = KY::make(t, c, q);
         const uint32_t i = hs++;
         // sift up at most two levels: i -> p1 -> p2
         const uint32_t p1 = i > 0 ? (i - 1) >> 2 : 0u;
@@ -208,17 +207,43 @@ struct LaneSim {
         kh = hs == 0 ? KY::INF : (down1 ? k1 : lastk);
     }
 
-    // ------------------------------------------------- wake FIFO
-    // one u64 register: slot j is byte j & 7 (a shared-memory byte ring cost
-    // a dependent load per woken waiter: C2 18.23 -> 18.12 ms, C5 16.74 ->
-    // 16.49 ms with the register)
-    uint64_t fq;
-    SG_HD uint32_t fifo_get(uint32_t j) const { return (uint32_t)(fq >> (8u * (j & 7u))) & 0xFFu; }
-    SG_HD void wake(uint32_t q) {
-        if (ftail - fhead >= kLaneFifo) { fail = true; return; }
-        const uint32_t sh = 8u * (ftail & 7u);
-        fq = (fq & ~(0xFFull << sh)) | ((uint64_t)q << sh);
-        ftail += 1;
+    // ------------------------------------------------- granted waiters
+    // grant_waiters pushes each granted waiter at (now, ++counter)
+    // (harness.py:558); its entry pops after every entry of tick `now`
+    // pushed before it and starts the busy step, which pushes the busy end
+    // (harness.py:514-520).  Until that pop, the only other pushes are
+    // those of the arrivals of tick `now` still pending (an app that ran
+    // inline at t = 0 owns an initial counter, so its busy end can pop
+    // before an arrival of the same tick); busy ends push nothing, and other
+    // granted waiters come later in grant order.  So the busy end is pushed
+    // at grant time, with a counter above those the pending arrivals of the
+    // tick may take: the first grant of a tick reserves one counter per
+    // pending arrival (cw = counter + R), granted waiters count up from cw,
+    // and a push in a later tick starts above both.  The busy start is
+    // accounted at `now` (a zero-length busy segment otherwise).  A waiter
+    // without a busy step frees when its entry pops: that entry goes into
+    // the heap at (now, its counter).  Pending push of this iteration:
+    // pp / pt / pc / pq; counters past CMAX send the lane to the fallback.
+    bool pp;
+    uint32_t pt, pc, pq;
+    uint32_t cw, wt;         // next granted-waiter counter / the tick it belongs to
+    uint32_t ap, ae;         // arrival stream: next position / end
+    SG_HD void start_granted(uint32_t q) {
+        const uint32_t b = bw_busy(s_bw[q]);
+        if (b) {
+            busy_point(last, +1);
+            pops += 1;  // the waiter's own entry
+        }
+        if (wt != last) {  // first grant of the tick: reserve the pending arrivals' counters
+            uint32_t r = 0;
+            while (ap + r < ae && s_a[ap + r] == last) r += 1;
+            cw = max(counter, cw) + r;
+            wt = last;
+        }
+        pp = true;
+        pt = last + b;
+        pc = cw++;
+        pq = q;
     }
 
     // ------------------------------------------------- wait queue
@@ -267,7 +292,9 @@ struct LaneSim {
             mask[w] &= w == (q >> 6) ? ~(1ull << (q & 63u)) : ~0ull;
         budget -= m;
         g += 1;
-        wake(q);
+        start_granted(q);  // several grants per call on this path: push each at once
+        push(pt, pc, pq);
+        pp = false;
     }
 
     // grant_waiters (harness.py:545-558) + select_grants (policy.py:52-74)
@@ -317,7 +344,7 @@ struct LaneSim {
                 grem[0] &= ~bit;
                 gbud -= s_mem[q];
                 gg += 1;
-                wake(q);
+                start_granted(q);
                 gcand[0] &= ~((bit << 1) - 1ull);
             }
             if (!pick || !gcand[0]) end_round(grem[0] == 0);
@@ -348,7 +375,7 @@ struct LaneSim {
             }
             gbud -= s_mem[q];
             gg += 1;
-            wake(q);
+            start_granted(q);
         }
         if (!more) {  // the round ends
             bool left = false;
@@ -457,16 +484,18 @@ struct LaneSim {
         if (P.grant)
             reinterpret_cast<uint32_t*>(P.grant)[o] = m ? now - bw_busy(bw) : SG_NEVER;
     }
-    SG_HD void run_from_busy(uint32_t q, uint32_t m, uint32_t bw, uint32_t now) {
+    // initial pop at t = 0 of an app without a cpu step; its busy end owns
+    // the app's initial virtual counter c
+    SG_HD void run_from_busy(uint32_t q, uint32_t m, uint32_t bw, uint32_t now, uint32_t c) {
         const uint32_t b = bw_busy(bw);
         if (b) {  // busy (harness.py:514-520)
             busy_point(now, +1);
-            push(now + b, q);
+            push(now + b, c, q);
             return;
         }
         end_app(m, bw, now);
     }
-    SG_HD void arrive(uint32_t q, uint32_t m, uint32_t bw, uint32_t now) {
+    SG_HD void arrive(uint32_t q, uint32_t m, uint32_t bw, uint32_t now, uint32_t c) {
         if (m) {
             if (m <= cap - used) {  // arrival bypass (harness.py:521-531)
                 mem_point(now);
@@ -479,7 +508,7 @@ struct LaneSim {
                 return;
             }
         }
-        run_from_busy(q, m, bw, now);
+        run_from_busy(q, m, bw, now, c);
     }
 
     // Simulate device range [s, e) of the slot's arrival order (z apps arrive
@@ -493,28 +522,38 @@ struct LaneSim {
         fail = false;
 #pragma unroll
         for (uint32_t w = 0; w < NW; w++) mask[w] = 0;
-        hs = fhead = ftail = 0;
-        fq = 0;
+        hs = 0;
         kh = KY::INF;
         last = mem_t = busy_prev = B = 0;
         I = 0;
         busy_level = holders = 0;
         maxh = grants = pops = 0;
-        gs = ginit = false;
+        gs = ginit = pp = false;
+        pt = pc = pq = 0;
         clsmask = 0;
+        // later pushes, including those of waiters granted at t = 0 (after
+        // every initial entry), count up from c_base
+        counter = cw = KY::c_base(n_trace);
+        wt = 0;
+        ap = ae = 0;  // no pending arrival of tick 0: those apps run inline
         // initial pops at t = 0: apps without a cpu step run inline, in index
         // order, each in its own virtual counter block
         for (uint32_t q = s; q < s + z; q++) {
             const uint32_t bw = s_bw[q];
-            counter = KY::c_init(bw_app(bw));
-            arrive(q, s_mem[q], bw, 0u);
+            arrive(q, s_mem[q], bw, 0u, KY::c_init(bw_app(bw)));
             if constexpr (TBL) {
-                while (gs && !fail) grant_step();
+                while (gs && !fail) {
+                    grant_step();
+                    if (pp) {
+                        push(pt, pc, pq);
+                        pp = false;
+                    }
+                }
             }
             if (fail) return false;
         }
-        counter = KY::c_base(n_trace);
-        uint32_t ap = s + z;
+        ap = s + z;
+        ae = e;
         Key ka = KY::INF;
         uint32_t bwa = 0;
         if (ap < e) {
@@ -524,33 +563,14 @@ struct LaneSim {
         while (true) {
             SG_LANE_ITER_HOOK(gs);
             if (!gs) {
-                // next event: a granted waiter resumes after every other entry of
-                // its tick; otherwise the smaller of the arrival / busy-end keys
-                Key kmin = ka < kh ? ka : kh;
-                if (fhead != ftail && KY::time(kmin) > last) {
-                    // every other entry of tick `last` is done: the woken
-                    // waiters resume in grant order, each starting its busy
-                    // step (harness.py:514-520, 558); a zero-length busy step
-                    // frees at once and is handled below as an event
-                    do {
-                        const uint32_t wq = fifo_get(fhead);
-                        const uint32_t wb = bw_busy(s_bw[wq]);
-                        if (wb == 0) break;
-                        fhead += 1;
-                        pops += 1;
-                        busy_point(last, +1);
-                        push(last + wb, wq);
-                    } while (fhead != ftail);
-                    kmin = ka < kh ? ka : kh;
-                }
-                const bool is_wake = fhead != ftail && KY::time(kmin) > last;
-                if (!is_wake && kmin == KY::INF) break;
-                const bool is_arr = !is_wake && ka < kh;
-                const bool is_end = !is_wake && !is_arr;
-                const uint32_t q = is_wake ? fifo_get(fhead) : KY::pos(kmin);
-                const uint32_t now = is_wake ? last : KY::time(kmin);
-                if (is_end) pop();
-                if (is_wake) fhead += 1;
+                // next event: the smaller of the arrival / heap keys (busy
+                // ends and the frees of granted waiters without a busy step)
+                const Key kmin = ka < kh ? ka : kh;
+                if (kmin == KY::INF) break;
+                const bool is_arr = ka < kh;
+                const uint32_t q = KY::pos(kmin);
+                const uint32_t now = KY::time(kmin);
+                if (!is_arr) pop();
                 if (is_arr) {
                     ap += 1;
                     if (ap < e) {
@@ -577,19 +597,27 @@ struct LaneSim {
                     maxh = max(maxh, (uint32_t)holders);
                     grants += 1;
                 }
-                // busy (harness.py:514-520) or its end
-                const bool to_busy = !is_end && !enq;
-                const bool start = to_busy && b != 0;
-                busy_point(now, start ? 1 : (is_end ? -1 : 0));
-                if (start) push(now + b, q);
-                if ((to_busy && b == 0) || is_end) end_app(m, bw, now);
+                // busy (harness.py:514-520), its end, or a granted waiter's free
+                const bool start = is_arr && !enq && b != 0;
+                busy_point(now, start ? 1 : (!is_arr && b != 0 ? -1 : 0));
+                pp = start;
+                pt = now + b;
+                pq = q;
+                // an arrival's busy end: above every counter of earlier ticks
+                pc = wt == now ? counter : max(counter, cw);
+                counter = pc + (start ? 1u : 0u);
+                if ((is_arr && !enq && b == 0) || !is_arr) end_app(m, bw, now);
             }
             if constexpr (TBL) {
                 if (gs) grant_step();
             }
+            // at most one push per iteration: an arrival's busy end, or the
+            // entry of the waiter this iteration's grant step granted
+            if (pp) push(pt, pc, pq);
+            pp = false;
             if (fail) return false;
         }
-        return !fail;  // a resumed waiter's push can fail just before the queue runs dry
+        return !fail;
     }
 
 #ifdef __CUDACC__
