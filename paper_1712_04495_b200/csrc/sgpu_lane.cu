@@ -512,7 +512,9 @@ __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const
     sim.s_cm = reinterpret_cast<const uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW) + c0 * NW;
     sim.ncls = c1 - c0;
     sim.heap = reinterpret_cast<typename LaneSim<K, NARROW, HW, FS>::Key*>(ws + L.off_fb) + lane;
-    sim.out_base = (uint64_t)pslot * P.n_apps_total + a0;
+    const uint64_t out_base = (uint64_t)pslot * P.n_apps_total + a0;
+    sim.gp = P.grant ? reinterpret_cast<uint32_t*>(P.grant) + out_base : nullptr;
+    sim.ep = P.end ? reinterpret_cast<uint32_t*>(P.end) + out_base : nullptr;
     if (!sim.run(na, s0, s1, z, policy, cap_d)) return false;
     // S = cpu + busy ticks of the lane's device range (arrival < 2^31 and
     // busy < 2^21 on this path), only when the speed-up is requested

@@ -120,7 +120,8 @@ struct LaneSim {
     uint32_t ncls;
     // this lane's columns
     Key* heap;               // heap[h * 32]
-    uint64_t out_base;       // grant/end index of app 0 of the trace under this policy
+    uint32_t* gp;            // grant / end ticks of app 0 of the trace under this policy
+    uint32_t* ep;            // (nullptr: not requested)
     uint32_t cap, used;
     bool prio_pol, mmu, fail;
     uint64_t mask[NW];
@@ -228,6 +229,7 @@ struct LaneSim {
     uint32_t pt, pc, pq;
     uint32_t cw, wt;         // next granted-waiter counter / the tick it belongs to
     uint32_t ap, ae;         // arrival stream: next position / end
+    Key ka;                  // key of the next arrival (KY::INF: none)
     SG_HD void start_granted(uint32_t q) {
         const uint32_t b = bw_busy(s_bw[q]);
         if (b) {
@@ -236,7 +238,8 @@ struct LaneSim {
         }
         if (wt != last) {  // first grant of the tick: reserve the pending arrivals' counters
             uint32_t r = 0;
-            while (ap + r < ae && s_a[ap + r] == last) r += 1;
+            if (KY::time(ka) == last)  // (rare) arrivals of this tick still pending
+                while (ap + r < ae && s_a[ap + r] == last) r += 1;
             cw = max(counter, cw) + r;
             wt = last;
         }
@@ -478,11 +481,10 @@ struct LaneSim {
             holders -= 1;
             grant_waiters();
         }
-        const uint64_t o = out_base + bw_app(bw);  // end (harness.py:543)
-        if (P.end) reinterpret_cast<uint32_t*>(P.end)[o] = now;
+        const uint32_t o = bw_app(bw);  // end (harness.py:543)
+        if (ep) ep[o] = now;
         // the grant is the busy start: busy runs [grant, grant + busy]
-        if (P.grant)
-            reinterpret_cast<uint32_t*>(P.grant)[o] = m ? now - bw_busy(bw) : SG_NEVER;
+        if (gp) gp[o] = m ? now - bw_busy(bw) : SG_NEVER;
     }
     // initial pop at t = 0 of an app without a cpu step; its busy end owns
     // the app's initial virtual counter c
@@ -536,6 +538,7 @@ struct LaneSim {
         counter = cw = KY::c_base(n_trace);
         wt = 0;
         ap = ae = 0;  // no pending arrival of tick 0: those apps run inline
+        ka = KY::INF;
         // initial pops at t = 0: apps without a cpu step run inline, in index
         // order, each in its own virtual counter block
         for (uint32_t q = s; q < s + z; q++) {
@@ -554,7 +557,6 @@ struct LaneSim {
         }
         ap = s + z;
         ae = e;
-        Key ka = KY::INF;
         uint32_t bwa = 0;
         if (ap < e) {
             bwa = s_bw[ap];
@@ -627,9 +629,9 @@ struct LaneSim {
         for (uint32_t w = 0; w < NW; w++) {
             for (uint64_t bits = mask[w]; bits; bits &= bits - 1) {
                 const uint32_t q = 64u * w + ffs64(bits);
-                const uint64_t o = out_base + bw_app(s_bw[q]);
-                if (P.grant) reinterpret_cast<uint32_t*>(P.grant)[o] = SG_NEVER;
-                if (P.end) reinterpret_cast<uint32_t*>(P.end)[o] = SG_NEVER;
+                const uint32_t o = bw_app(s_bw[q]);
+                if (gp) gp[o] = SG_NEVER;
+                if (ep) ep[o] = SG_NEVER;
                 unf += 1;
             }
         }

@@ -89,7 +89,8 @@ static void run_case(int n, uint32_t policy, uint32_t cap, const std::vector<uin
     sim.s_cm = s_cm.data();
     sim.ncls = (uint32_t)pl.size();
     sim.heap = reinterpret_cast<typename Sim::Key*>(heap.data());
-    sim.out_base = 0;
+    sim.gp = grant.data();
+    sim.ep = end.data();
     if (!sim.run((uint32_t)n, 0, (uint32_t)n, z, policy, cap)) { printf("0\n"); return; }
     uint32_t unf = 0;
     for (uint64_t bits = sim.mask[0]; bits; bits &= bits - 1) unf++;
