@@ -73,8 +73,10 @@ cudaError_t work_release(cudaStream_t stream, WorkLease& lease, cudaError_t err)
 // launches pay no attribute call or occupancy query.
 cudaError_t kernel_config(const void* kern, int threads, size_t smem, int* per_sm, int* sms);
 
-// Shared-memory layout for one warp simulating traces of up to n_pad apps.
-void sim_layout(SimParams& p, bool program_mode, bool f64);
+// Shared-memory layout for one warp simulating traces of up to n_pad apps
+// (single_app_buf: one staged trace instead of the T0 double buffer, for the
+// in-kernel fallbacks of the lane / octet kernels).
+void sim_layout(SimParams& p, bool program_mode, bool f64, bool single_app_buf = false);
 
 // Launch K1 (trace simulation).  Returns a cudaError_t.
 cudaError_t launch_sim(const SimParams& p, bool program_mode, bool f64, cudaStream_t stream,
@@ -84,6 +86,11 @@ cudaError_t launch_sim(const SimParams& p, bool program_mode, bool f64, cudaStre
 // (sgpu_lane.cu), with an in-kernel exact fallback to TraceSim.
 bool lane_eligible(const SimParams& p, bool program_mode, bool f64, bool forced);
 cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_out);
+// K1 v8: octet-per-(trace, policy) kernel for T0 tick-mode batches of
+// 129..256-app single-device traces (sgpu_octet.cu), with an in-kernel exact
+// fallback to TraceSim.
+bool octet_eligible(const SimParams& p, bool program_mode, bool f64);
+cudaError_t launch_sim_octet(const SimParams& p, cudaStream_t stream, int* grid_out);
 // K1 v6: lane-per-(trace, policy) kernel for step-program tick-mode batches
 // (sgpu_proglane.cu), with an in-kernel exact fallback to TraceSim.
 bool prog_lane_eligible(const SimParams& p, bool program_mode, bool f64, bool forced);

@@ -50,6 +50,7 @@
 #include <cstring>
 
 #include "sgpu_lanesim.cuh"
+#include "sgpu_warpsort.cuh"
 
 namespace sg {
 
@@ -106,69 +107,6 @@ static_assert(meta_baddev(2) < meta_u16(2) && meta_baddev(3) < meta_u16(3) && me
                   meta_baddev(5) < meta_u16(5) && meta_baddev(6) < meta_u16(6) && meta_baddev(7) < meta_u16(7) &&
                   meta_baddev(8) < meta_u16(8),
               "meta layout");
-
-__device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
-    const uint32_t lo = __shfl_xor_sync(FULL, (uint32_t)v, m);
-    const uint32_t hi = __shfl_xor_sync(FULL, (uint32_t)(v >> 32), m);
-    return ((uint64_t)hi << 32) | lo;
-}
-__device__ __forceinline__ uint64_t shfl_up_u64(uint64_t v, int m) {
-    const uint32_t lo = __shfl_up_sync(FULL, (uint32_t)v, m);
-    const uint32_t hi = __shfl_up_sync(FULL, (uint32_t)(v >> 32), m);
-    return ((uint64_t)hi << 32) | lo;
-}
-__device__ __forceinline__ uint32_t shfl_xor_key(uint32_t v, int m) { return __shfl_xor_sync(FULL, v, m); }
-__device__ __forceinline__ uint64_t shfl_xor_key(uint64_t v, int m) { return shfl_xor_u64(v, m); }
-
-// Ascending bitonic sort of 32*K keys held K per lane (element k*32 + lane).
-template <int K, class KeyT>
-__device__ __forceinline__ void warp_bitonic_sort(KeyT (&v)[K], uint32_t lane) {
-    constexpr uint32_t N = 32u * K;
-#pragma unroll
-    for (uint32_t size = 2; size <= N; size <<= 1) {
-#pragma unroll
-        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-            if (stride >= 32) {
-                const uint32_t ks = stride >> 5;
-#pragma unroll
-                for (int k = 0; k < K; k++) {
-                    if ((k & ks) == 0) {
-                        const int kp = k | ks;
-                        const bool up = (((uint32_t)k * 32u + lane) & size) == 0;
-                        const KeyT a = v[k], b = v[kp];
-                        const bool sw = up ? (a > b) : (a < b);
-                        v[k] = sw ? b : a;
-                        v[kp] = sw ? a : b;
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < K; k++) {
-                    const KeyT o = shfl_xor_key(v[k], (int)stride);
-                    const bool up = (((uint32_t)k * 32u + lane) & size) == 0;
-                    const bool low = (lane & stride) == 0;
-                    v[k] = (up == low) ? (v[k] < o ? v[k] : o) : (v[k] < o ? o : v[k]);
-                }
-            }
-        }
-    }
-}
-
-// Sort 64-bit keys (kInf = padding) with 32-bit compare-exchanges when every
-// real key is below 2^32 - 1 (warp-uniform `narrow`): half the shuffles.
-template <int K>
-__device__ __forceinline__ void warp_sort_keys(uint64_t (&v)[K], bool narrow, uint32_t lane) {
-    if (narrow) {
-        uint32_t w[K];
-#pragma unroll
-        for (int k = 0; k < K; k++) w[k] = v[k] == kInf ? ~0u : (uint32_t)v[k];
-        warp_bitonic_sort<K>(w, lane);
-#pragma unroll
-        for (int k = 0; k < K; k++) v[k] = w[k] == ~0u ? kInf : (uint64_t)w[k];
-    } else {
-        warp_bitonic_sort<K>(v, lane);
-    }
-}
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));

@@ -162,12 +162,13 @@ struct LaneSim {
         if (hs >= KY::HCAP || c >= KY::CMAX) { fail = true; return; }
         const Key key = KY::make(t, c, q);
         const uint32_t i = hs++;
-        // sift up at most two levels: i -> p1 -> p2
+        // sift up at most two levels: i -> p1 -> p2; both parent loads are
+        // issued at once (their indices follow from the size alone)
         const uint32_t p1 = i > 0 ? (i - 1) >> 2 : 0u;
-        const Key k1 = i > 0 ? heap[p1 * 32] : (Key)0;
-        const bool up1 = i > 0 && key < k1;
         const uint32_t p2 = p1 > 0 ? (p1 - 1) >> 2 : 0u;
-        const Key k2 = up1 && p1 > 0 ? heap[p2 * 32] : (Key)0;
+        const Key k1 = heap[p1 * 32];
+        const Key k2 = heap[p2 * 32];
+        const bool up1 = i > 0 && key < k1;
         const bool up2 = up1 && p1 > 0 && key < k2;
         if (up1) heap[i * 32] = k1;
         if (up2) heap[p1 * 32] = k2;

@@ -323,13 +323,13 @@ cudaError_t kernel_config(const void* kern, int threads, size_t smem, int* per_s
 
 static inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
-void sim_layout(SimParams& p, bool program_mode, bool f64) {
+void sim_layout(SimParams& p, bool program_mode, bool f64, bool single_app_buf) {
     const uint32_t N = p.n_pad;
     const uint32_t tsz = f64 ? 8u : 4u;
     const bool multi = p.ndev > 1;
     uint32_t o = 0;
     p.off_app = o;
-    o = align16(o + N * 16u * (program_mode ? 1u : 2u));
+    o = align16(o + N * 16u * (program_mode || single_app_buf ? 1u : 2u));
     p.off_sub = o;
     o = align16(o + (multi ? N * 16u : 0u));
     p.off_idx = o;

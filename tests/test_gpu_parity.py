@@ -20,7 +20,8 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(params=["auto", "warp"], autouse=True)
 def engine(request, monkeypatch):
     """Every parity test runs on both K1 engines: `auto` takes the lane kernel
-    (v5) wherever the batch is eligible (T0, <= 128 apps), `warp` forces the
+    (v5) wherever the batch is eligible (T0, <= 128 apps) and the octet
+    kernel (v8) for 129..256-app single-device T0 traces, `warp` forces the
     warp-per-trace kernel (v3)."""
     if request.param == "warp":
         monkeypatch.setenv("SGPU_K1", "warp")
@@ -185,6 +186,59 @@ def test_lane_kernel_long_traces_forced(n, cuda, monkeypatch):
     g = GenParams(seed=n, apps_per_trace=n, arr_hi=3 * n, mem_lo=1, mem_hi=60_000, prio_levels=5)
     apps = as_u32x4(generate(g, 0, 64))
     check_against_oracle(apps, (184_320,), cuda)
+
+
+@pytest.mark.parametrize("pols", [POLICIES, ("pfifo", "pmmu"), ("mmu",), ("fifo", "mmu", "pmmu")])
+def test_octet_kernel_shapes(pols, cuda):
+    """K1 v8 (octet per simulation, 129..256-app traces): C3-shaped traces,
+    edge traces (zero fields, simultaneous arrivals, stuck requests, ties),
+    and the shapes its exact fallback takes over (more than 32 busy apps at
+    once, more than eight priority classes, priorities of 32 and above)."""
+    rng = np.random.default_rng(808)
+    cfg = CONFIGS["C3"]
+    c3 = as_u32x4(generate(dataclasses.replace(cfg.gen, seed=808), 0, 24))
+    edge = np.zeros((24, 256, 4), dtype=np.uint32)
+    edge[..., 0] = rng.choice([0, 0, 1, 5, 9, 40, 41], (24, 256))
+    edge[..., 1] = rng.choice([0, 100, 250, 500, 1000, 1001], (24, 256))
+    edge[..., 2] = rng.choice([0, 0, 1, 3, 7, 30], (24, 256))
+    edge[..., 3] = rng.integers(0, 4, (24, 256))
+    many = np.zeros((16, 256, 4), dtype=np.uint32)   # tiny requests: up to 256 busy at once
+    many[..., 0] = rng.integers(0, 64, (16, 256))
+    many[..., 1] = rng.integers(1, 8, (16, 256))
+    many[..., 2] = rng.integers(50, 400, (16, 256))
+    many[..., 3] = rng.integers(0, 4, (16, 256))
+    many[:8, :, 2] = rng.integers(1, 3, (8, 256))      # ... or only a few
+    many[:4, :, 3] = rng.integers(0, 12, (4, 256))     # > 8 classes
+    many[4:6, :, 3] = rng.integers(30, 40, (2, 256))   # priorities >= 32
+    for apps, caps in ((c3, cfg.cap_mib), (edge, (1000,)), (many, (300,))):
+        check_against_oracle(apps, caps, cuda, policies=pols)
+    for n in (129, 200, 255):   # shorter traces on the same kernel (n_pad 256)
+        g = GenParams(seed=n, apps_per_trace=n, arr_hi=2 * n, mem_lo=1, mem_hi=30_000, prio_levels=5)
+        check_against_oracle(as_u32x4(generate(g, 0, 16)), (100_000,), cuda, policies=pols)
+
+
+def test_octet_kernel_ragged(cuda):
+    """Ragged batches up to 256 apps per trace on the octet kernel."""
+    rng = np.random.default_rng(19)
+    lens = rng.integers(129, 257, 40)
+    total = int(lens.sum())
+    g = GenParams(seed=5, apps_per_trace=1, arr_hi=500, mem_lo=1000, mem_hi=60_000)
+    flat = as_u32x4(generate(dataclasses.replace(g, apps_per_trace=total), 0, 1))[0]
+    offs = np.zeros(len(lens) + 1, dtype=np.int64)
+    np.cumsum(lens, out=offs[1:])
+    res = B.simulate_batch(to_dev(flat, cuda), POLICIES, 184_320,
+                           trace_offsets=torch.from_numpy(offs).to(cuda),
+                           apps_total=total, max_apps=int(lens.max()))
+    torch.cuda.synchronize()
+    st = res.stats()
+    for pi, pol in enumerate(res.policies):
+        for t in range(len(lens)):
+            a = flat[offs[t]:offs[t + 1]][None]
+            gg, ee, ss = O.simulate_burst(a, (184_320,), pol.value)
+            np.testing.assert_array_equal(res.ticks("grant")[pi][offs[t]:offs[t + 1]], gg[0])
+            np.testing.assert_array_equal(res.ticks("end")[pi][offs[t]:offs[t + 1]], ee[0])
+            for f in ("makespan", "busy", "mem_integral", "max_holders", "pops", "grants", "unfinished"):
+                assert st[pi][t, 0][f] == ss[0, 0][f], (pol, t, f)
 
 
 def test_edge_cases(cuda):
