@@ -693,6 +693,7 @@ cudaError_t small_grow(SmallCtx& c, size_t in_b, size_t out_b) {
         c.cap_in = std::max<size_t>(in_b, 1u << 16);
         e = cudaMallocHost(reinterpret_cast<void**>(&c.h_in), c.cap_in);
         if (e != cudaSuccess) { c.h_in = nullptr; c.cap_in = 0; }
+
     }
     if (e == cudaSuccess && out_b > c.cap_out) {
         if (c.h_out) cudaFreeHost(c.h_out);
@@ -708,6 +709,8 @@ cudaError_t small_grow(SmallCtx& c, size_t in_b, size_t out_b) {
         c.cap_d = std::max<size_t>(in_b + out_b, 1u << 17);
         e = cudaMalloc(reinterpret_cast<void**>(&c.d_buf), c.cap_d);
         if (e != cudaSuccess) { c.d_buf = nullptr; c.cap_d = 0; }
+        // defined bytes in the alignment gaps of the packed output (copied back whole)
+        else e = cudaMemsetAsync(c.d_buf, 0, c.cap_d, c.st);
     }
     return e;
 }
@@ -751,11 +754,17 @@ int sg_simulate_small_host(const sg_batch* in, const sg_out* out, int cuda_devic
     e = small_grow(c, in_b, out_b);
     if (e != cudaSuccess) return cuda_fail(e, "small-batch buffers");
     memcpy(c.h_in + o_apps, in->apps, A * sizeof(sg_app));
+    size_t filled = A * sizeof(sg_app);
     if (s.program) {
+        memset(c.h_in + filled, 0, o_so - filled);  // alignment gap (no uninitialised bytes go H2D)
         uint32_t* so = reinterpret_cast<uint32_t*>(c.h_in + o_so);
         for (uint64_t i = 0; i <= A; i++) so[i] = in->step_offsets[i] - so0;
+        filled = o_so + (A + 1) * 4;
+        memset(c.h_in + filled, 0, o_steps - filled);
         memcpy(c.h_in + o_steps, in->steps, n_steps * sizeof(sg_step));
+        filled = o_steps + n_steps * sizeof(sg_step);
     }
+    memset(c.h_in + filled, 0, in_b - filled);
     uint8_t* d_in = c.d_buf;
     uint8_t* d_out = c.d_buf + in_b;
     e = cudaMemcpyAsync(d_in, c.h_in, in_b, cudaMemcpyHostToDevice, c.st);

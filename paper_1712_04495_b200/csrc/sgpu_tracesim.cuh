@@ -631,11 +631,10 @@ struct TraceSim {
                     held += (int32_t)mib;
                     maxh = max(maxh, (uint32_t)max(holders, 0));
                     grants += 1;
-                    {   // first grant of the app: read by the warp, then one lane writes
-                        const bool first = TM::is_never(s_grant[app]);
-                        __syncwarp();
-                        if (first && lane == 0) s_grant[app] = now;
-                    }
+                    // first grant of the app: one lane reads and writes, and the
+                    // warp syncs before any later read of s_grant
+                    if (lane == 0 && TM::is_never(s_grant[app])) s_grant[app] = now;
+                    __syncwarp();
                     emit(now, app, SG_EV_GRANT, mib);
                     emit(now, app, SG_EV_ALLOC, mib);
                     pc += 1;
