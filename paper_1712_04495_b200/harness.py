@@ -29,6 +29,7 @@ import ctypes
 import json
 import math
 import struct
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -173,29 +174,27 @@ class EncodedTrace:
     cap_mib: int
 
 
-def _flatten(spec: WorkloadSpec) -> list[list[tuple[int, object]]]:
+def _flatten_profile(prof: AppProfile, time_scale: float) -> list[tuple[int, object]]:
     """harness.py:478-490: cpu -> alloc -> busy -> free per phase, zero fields
     skipped, durations with the reference's float expression."""
-    progs = []
-    for prof in spec.instances:
-        flat = []
-        for ph in prof.phases:
-            if ph.cpu_ms:
-                flat.append((_lib.OP_CPU, ph.cpu_ms * spec.time_scale / 1000.0))
-            if ph.alloc_mib:
-                flat.append((_lib.OP_ALLOC, ph.alloc_mib))
-            if ph.busy_ms:
-                flat.append((_lib.OP_BUSY, ph.busy_ms * spec.time_scale / 1000.0))
-            if ph.free_mib:
-                flat.append((_lib.OP_FREE, ph.free_mib))
-        progs.append(flat)
-    return progs
+    flat = []
+    for ph in prof.phases:
+        if ph.cpu_ms:
+            flat.append((_lib.OP_CPU, ph.cpu_ms * time_scale / 1000.0))
+        if ph.alloc_mib:
+            flat.append((_lib.OP_ALLOC, ph.alloc_mib))
+        if ph.busy_ms:
+            flat.append((_lib.OP_BUSY, ph.busy_ms * time_scale / 1000.0))
+        if ph.free_mib:
+            flat.append((_lib.OP_FREE, ph.free_mib))
+    return flat
 
 
-def _tick_grid(durations: list[float], cap_mib: int):
+def _tick_grid(durations: list[float], cap_mib: int, counts=None):
     """Smallest e such that every duration is an integer number of 2^-e s
     ticks and every reference float sum is exact (all times < 2^32 ticks,
-    memory integral < 2^53).  None => use float64 mode."""
+    memory integral < 2^53).  None => use float64 mode.  counts[i]: how many
+    times durations[i] occurs (default once)."""
     if not durations:
         return 10
     # a finite double is num / 2^k exactly (float.as_integer_ratio)
@@ -203,38 +202,53 @@ def _tick_grid(durations: list[float], cap_mib: int):
     e = max(den.bit_length() - 1 for _, den in fr)
     if e > 62:
         return None
-    total = sum(num << (e - (den.bit_length() - 1)) for num, den in fr)
+    cnt = counts or [1] * len(fr)
+    total = sum(c * (num << (e - (den.bit_length() - 1))) for (num, den), c in zip(fr, cnt))
     if total >= 0xFFFFFFFE or cap_mib * total >= (1 << 53):
         return None
     return e
 
 
 def encode_spec(spec: WorkloadSpec) -> EncodedTrace:
-    progs = _flatten(spec)
+    """Step programs of the spec's instances for the C ABI.  Instances that
+    share an AppProfile object (12 x "ara-like") are flattened, checked and
+    encoded once per call."""
     cap_mib = spec.devices[0].total_bytes // MIB
     if spec.devices[0].total_bytes % MIB:
         raise ValueError("device capacity must be a whole number of MiB")
-    durations = []
-    for flat in progs:
+    uniq: dict[int, int] = {}      # id(profile) -> index into flats
+    flats: list[list[tuple[int, object]]] = []
+    which = []
+    for prof in spec.instances:
+        k = uniq.get(id(prof))
+        if k is None:
+            k = uniq[id(prof)] = len(flats)
+            flats.append(_flatten_profile(prof, spec.time_scale))
+        which.append(k)
+    uses = [0] * len(flats)
+    for k in which:
+        uses[k] += 1
+    durations, counts = [], []
+    for flat, u in zip(flats, uses):
         for op, arg in flat:
             if op in (_lib.OP_CPU, _lib.OP_BUSY):
                 if not (arg >= 0) or math.isinf(arg):
                     raise ValueError(f"step durations must be finite and >= 0 (got {arg!r})")
                 durations.append(arg)
+                counts.append(u)
             else:
                 if int(arg) != arg or not 0 < int(arg) < 0x7FFFFFFF:
                     raise ValueError(f"memory sizes must be whole MiB in (0, 2^31) (got {arg!r})")
-    e = _tick_grid(durations, cap_mib)
+    e = _tick_grid(durations, cap_mib, counts)
     mode = _lib.TIME_TICKS if e is not None else _lib.TIME_F64
     # priorities: only order and equality matter (policy.py:58-63) -> dense ranks
     prios = sorted({int(p.priority) for p in spec.instances})
     if len(prios) > 256:
         raise ValueError("at most 256 distinct priorities per workload")
     rank = {p: i for i, p in enumerate(prios)}
-    n = len(progs)
-    offs = np.zeros(n + 1, dtype=np.uint32)
-    rows = []
-    for i, flat in enumerate(progs):
+    enc_rows = []
+    for flat in flats:
+        rows = []
         for op, arg in flat:
             if op in (_lib.OP_CPU, _lib.OP_BUSY):
                 if mode == _lib.TIME_TICKS:
@@ -245,8 +259,14 @@ def encode_spec(spec: WorkloadSpec) -> EncodedTrace:
                 rows.append((op, 0, dur))
             else:
                 rows.append((op, int(arg), 0))
-        offs[i + 1] = len(rows)
-    steps = np.array(rows, dtype=STEP_DTYPE) if rows else np.zeros(1, dtype=STEP_DTYPE)
+        enc_rows.append(rows)
+    offs_l = [0]
+    all_rows = []
+    for k in which:
+        all_rows += enc_rows[k]
+        offs_l.append(len(all_rows))
+    offs = np.array(offs_l, dtype=np.uint32)
+    steps = np.array(all_rows, dtype=STEP_DTYPE) if all_rows else np.zeros(1, dtype=STEP_DTYPE)
     attr = np.array([rank[int(p.priority)] for p in spec.instances], dtype=np.uint32)
     return EncodedTrace(steps, offs, attr, mode, e if e is not None else 0, cap_mib)
 
@@ -254,6 +274,7 @@ def encode_spec(spec: WorkloadSpec) -> EncodedTrace:
 # ------------------------------------------------------------------ simulate
 
 _CUDA_OK = None
+_TLS = threading.local()
 
 
 def _gpu_device() -> int:
@@ -289,7 +310,12 @@ def run_encoded(enc: EncodedTrace, policy) -> dict:
     pct = np.empty(2, dtype=np.float64)
     events = np.empty(ev_cap, dtype=_EVENT_DTYPE)
     count = np.zeros(1, dtype=np.uint32)
-    b = _lib.SgBatch()
+    cache = getattr(_TLS, "abi", None)
+    if cache is None:  # the ctypes argument structs, reused per thread
+        cache = _TLS.abi = (_lib.SgBatch(), _lib.SgOut())
+    b, o = cache
+    ctypes.memset(ctypes.byref(b), 0, ctypes.sizeof(b))
+    ctypes.memset(ctypes.byref(o), 0, ctypes.sizeof(o))
     b.n_traces = 1
     b.apps_per_trace = n
     b.max_apps = n
@@ -301,7 +327,6 @@ def run_encoded(enc: EncodedTrace, policy) -> dict:
     b.cap_mib[0] = enc.cap_mib
     b.time_mode = enc.time_mode
     b.tick_log2 = enc.tick_log2
-    o = _lib.SgOut()
     o.stats = stats.ctypes.data
     o.mem_pct = pct.ctypes.data
     o.dev_pct = pct.ctypes.data + 8
@@ -320,15 +345,14 @@ def _time_of(enc: EncodedTrace, raw: int) -> float:
     return struct.unpack("<d", struct.pack("<Q", int(raw)))[0]
 
 
-_BYTES_KINDS = np.zeros(8, dtype=bool)
-_BYTES_KINDS[[_lib.EV_REQUEST, _lib.EV_GRANT, _lib.EV_ALLOC, _lib.EV_FREE]] = True
+_BYTES_KIND_SET = frozenset((_lib.EV_REQUEST, _lib.EV_GRANT, _lib.EV_ALLOC, _lib.EV_FREE))
 
 
 def simulate(spec: WorkloadSpec) -> MetricsReport:
     """Discrete-event prediction of `spec` (memshare/harness.py:475-572) on
     the GPU.  Deterministic; bit-identical to the reference's report.  The
-    report is assembled from the GPU's event log with numpy (every float is
-    produced by the same IEEE operation the reference performs)."""
+    report is assembled from the GPU's event log (every float is produced by
+    the same IEEE operation the reference performs)."""
     if not spec.instances:
         return MetricsReport(0.0, {}, [], [], 0.0, 0.0, 0, 0)
     enc = encode_spec(spec)
@@ -341,34 +365,47 @@ def simulate(spec: WorkloadSpec) -> MetricsReport:
         raise _lib.SgpuError(f"simulation status 0x{status:x}")
     capacity = spec.devices[0].total_bytes
     ev = out["events"]
+    kind_l = ev["kind"].tolist()
+    app_l = ev["app"].tolist()
+    mib_l = ev["mib"].tolist()
     if enc.time_mode == _lib.TIME_TICKS:
-        # t = ticks * 2^-e exactly (math.ldexp(float(ticks), -e))
-        t_all = ev["t"].astype(np.float64) * (2.0 ** -enc.tick_log2)
+        # t = ticks * 2^-e exactly (as math.ldexp(float(ticks), -e))
+        sc = 2.0 ** -enc.tick_log2
+        t_all = [float(x) * sc for x in ev["t"].tolist()]
         t_end = math.ldexp(float(st["makespan"]), -enc.tick_log2)
     else:
-        t_all = ev["t"].view(np.float64)
+        t_all = ev["t"].view(np.float64).tolist()
         t_end = float(st["makespan_s"])
-    order = np.argsort(t_all, kind="stable")  # harness.py:567 (stable sort by t)
-    t_s = t_all[order]
-    kind = ev["kind"][order]
-    app = ev["app"][order]
-    nbytes = np.where(_BYTES_KINDS[kind], ev["mib"][order].astype(np.int64) * MIB, 0)
-    makespan_s = max(t_end - 0.0, 1e-9)
-    t_ms = (t_s - 0.0) * 1000.0
-    t_ms_l, app_l, kind_l, nb_l = t_ms.tolist(), app.tolist(), kind.tolist(), nbytes.tolist()
+    # plain Python below: a workload's log is short, and list operations beat
+    # numpy's per-call overhead at this size
+    order = sorted(range(len(t_all)), key=t_all.__getitem__)  # harness.py:567 (stable sort by t)
     names = _lib.EVENT_NAMES
-    out_events = [{"t_ms": a, "instance": b, "event": names[k], "device": 0, "bytes": c}
-                  for a, b, k, c in zip(t_ms_l, app_l, kind_l, nb_l)]
+    byte_kinds = _BYTES_KIND_SET
+    makespan_s = max(t_end - 0.0, 1e-9)
+    out_events = []
+    n = len(enc.attr)
+    starts = [None] * n
+    ends = [None] * n
+    mem_pts = []  # (t, delta bytes) of alloc / free, in sorted event order
+    ev_start, ev_end, ev_alloc, ev_free = _lib.EV_START, _lib.EV_END, _lib.EV_ALLOC, _lib.EV_FREE
+    for k in order:
+        t = t_all[k]
+        kd = kind_l[k]
+        a = app_l[k]
+        nb = mib_l[k] * MIB if kd in byte_kinds else 0
+        t_ms = (t - 0.0) * 1000.0
+        out_events.append({"t_ms": t_ms, "instance": a, "event": names[kd], "device": 0, "bytes": nb})
+        if kd == ev_start:
+            starts[a] = t_ms
+        elif kd == ev_end:
+            ends[a] = t_ms
+        elif kd == ev_alloc:
+            mem_pts.append((t, nb))
+        elif kd == ev_free:
+            mem_pts.append((t, -nb))
     # every app emits start at t = 0 (index order, first in the sorted log)
     # and at most one end: the reference's setdefault walk gives
     # {i: {"start_ms": .., "end_ms": ..}} in index order
-    n = len(enc.attr)
-    ends = [None] * n
-    for i, a in zip(app[kind == _lib.EV_END].tolist(), t_ms[kind == _lib.EV_END].tolist()):
-        ends[i] = a
-    starts = [None] * n
-    for i, a in zip(app[kind == _lib.EV_START].tolist(), t_ms[kind == _lib.EV_START].tolist()):
-        starts[i] = a
     instances: dict[int, dict] = {}
     for i in range(n):
         d = {}
@@ -379,22 +416,20 @@ def simulate(spec: WorkloadSpec) -> MetricsReport:
         instances[i] = d
     # 100 ms memory-utilisation samples (harness.py:439-450): the level at a
     # sample is the sum of every alloc/free delta at or before it
-    memsel = (kind == _lib.EV_ALLOC) | (kind == _lib.EV_FREE)
-    pt_t = t_s[memsel]
-    pt_d = np.where(kind[memsel] == _lib.EV_ALLOC, nbytes[memsel], -nbytes[memsel])
-    po = np.argsort(pt_t, kind="stable")
-    pt_t = pt_t[po]
-    cum = np.concatenate(([0], np.cumsum(pt_d[po])))
-    ts = []
+    mem_pts.sort(key=lambda x: x[0])
+    trace = []
+    level = 0
+    j = 0
+    npts = len(mem_pts)
     t = 0.0
     lim = makespan_s + 1e-9
     step = TICK_MS / 1000.0
     while t <= lim:
-        ts.append(t)
+        while j < npts and mem_pts[j][0] <= t:
+            level += mem_pts[j][1]
+            j += 1
+        trace.append((t * 1000.0, level / capacity))
         t += step
-    ts_a = np.array(ts)
-    level = cum[np.searchsorted(pt_t, ts_a, side="right")]
-    trace = list(zip((ts_a * 1000.0).tolist(), (level / capacity).tolist()))
     report = MetricsReport(makespan_ms=makespan_s * 1000.0, instances=instances,
                            events=out_events, mem_trace=trace,
                            avg_mem_util_pct=out["mem_pct"], avg_device_util_pct=out["dev_pct"],
