@@ -408,7 +408,7 @@ def test_host_pipeline_matches_device(cuda):
     assert floats_equal(host.dev_pct, dres.dev_pct.cpu().numpy())
 
 
-@pytest.mark.parametrize("case", ["overflow", "busy16", "end16", "c5", "long", "grant_only"])
+@pytest.mark.parametrize("case", ["overflow", "busy16", "end16", "c5", "long", "c3", "grant_only"])
 def test_host_pipeline_cases(case, cuda):
     """The host pipeline moves end and busy ticks as u16 (K5 pack16) and
     derives the grants on the host (end - busy); a chunk they do not fit
@@ -446,6 +446,9 @@ def test_host_pipeline_cases(case, cuda):
     elif case == "long":
         cfg = CONFIGS["C4"]
         apps, caps = as_u32x4(generate(cfg.gen, 0, 400)), cfg.cap_mib
+    elif case == "c3":   # 256-app traces: the octet kernel behind the pipeline
+        cfg = CONFIGS["C3"]
+        apps, caps = as_u32x4(generate(cfg.gen, 0, 300)), cfg.cap_mib
     else:
         apps = as_u32x4(generate(CONFIGS["C2"].gen, 0, 900))
     dres = run(apps, POLICIES, caps, cuda)
@@ -598,6 +601,31 @@ def test_cuda_graph_replay(tick_scale, cuda):
         st = res.stats()
         for pi, pol in enumerate(res.policies):
             gr, e, sref = O.simulate_burst(apps, cfg.cap_mib, pol.value)
+            np.testing.assert_array_equal(res.ticks("end")[pi].reshape(e.shape), e, err_msg=f"replay {k}")
+            np.testing.assert_array_equal(st[pi].view(np.uint8), sref.view(np.uint8))
+
+
+def test_octet_kernel_graph_replay(cuda):
+    """The octet kernel (C3-shaped 256-app traces) inside a captured CUDA
+    graph, replayed on fresh inputs: each replay simulates the whole batch."""
+    cfg = CONFIGS["C3"]
+    n = 600
+    apps_t = B.generate_traces(cfg.gen, 0, n, device=0)
+    B.simulate_batch(apps_t, cfg.policies, cfg.cap_mib)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        res = B.simulate_batch(apps_t, cfg.policies, cfg.cap_mib, stream=s)
+    for k in range(2):
+        apps_t.copy_(B.generate_traces(dataclasses.replace(cfg.gen, seed=700 + k), 0, n, device=0))
+        g.replay()
+        torch.cuda.synchronize()
+        apps = apps_t.cpu().numpy().view(np.uint32)
+        st = res.stats()
+        for pi, pol in enumerate(res.policies):
+            gr, e, sref = O.simulate_burst(apps, cfg.cap_mib, pol.value)
+            np.testing.assert_array_equal(res.ticks("grant")[pi].reshape(gr.shape), gr, err_msg=f"replay {k}")
             np.testing.assert_array_equal(res.ticks("end")[pi].reshape(e.shape), e, err_msg=f"replay {k}")
             np.testing.assert_array_equal(st[pi].view(np.uint8), sref.view(np.uint8))
 
