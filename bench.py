@@ -492,9 +492,9 @@ def main():
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e = {"value": units_per_step * e2e_steps / float(dt[0]), "unit": "traces/s",
                "h2d_bytes_per_step": hr.h2d_bytes, "d2h_bytes_per_step": hr.d2h_bytes,
-               "api": "sg_simulate_batch_host (C ABI, pinned host buffers, 3-stream pipeline; "
-                      "grant ticks derived on host threads from the end ticks and a 2 B/app busy16 "
-                      "side channel)",
+               "api": "sg_simulate_batch_host (C ABI, pinned host buffers, 4-stream pipeline; "
+                      "end and busy ticks cross PCIe as u16 (K5 pack16) and host threads write "
+                      "the grant and end arrays)",
                "steps": e2e_steps}
 
     cpu = None
