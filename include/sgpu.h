@@ -250,8 +250,8 @@ int sg_simulate_batch(const sg_batch* in, const sg_out* out, void* stream);
  * chunk_traces traces (0 = automatic), simulates, copies outputs back,
  * overlapping the three with streams.  Synchronous.  Event logs unsupported.
  * With both tick arrays requested, a chunk whose ticks all fit 16 bits
- * crosses PCIe as packed (grant, end) u16 pairs (4 B per app and policy)
- * and is expanded by host threads; other chunks as u32 arrays. */
+ * crosses PCIe as u16 end and busy ticks and host threads write both u32
+ * arrays (grant = end - busy); other chunks cross as u32 end ticks. */
 int sg_simulate_batch_host(const sg_batch* in, const sg_out* out, int cuda_device,
                            uint64_t chunk_traces);
 

@@ -174,21 +174,24 @@ int sg_simulate_batch(const sg_batch* in, const sg_out* out, void* stream) {
 }
 
 // Host-buffer pipeline: chunks of traces cycle through NBUF device buffer
-// sets on NBUF streams; each chunk is H2D -> trace_sim -> D2H on its stream,
-// so the copies of one chunk overlap the simulation of the next.
+// sets on NBUF streams; each chunk is H2D -> trace_sim -> K5 pack16 -> D2H
+// on its stream, so the copies of one chunk overlap the simulation of the
+// next.
 //
 // The per-app grant ticks are not copied back: for T0 traces the grant is
 // the start of the busy step, so grant = end - busy for apps that request
-// memory and end, NEVER otherwise (memshare/harness.py:514-531) — host
-// threads derive it from the end ticks while later chunks are still on the
-// GPU.  The busy ticks come from a 2-byte-per-app side channel (K5 busy16:
-// 0xFFFF = no request) rather than from the caller's 16-byte records, so a
-// derivation reads 2 B of busy + 4 B of end per app and policy instead of
-// 16 B of records per app (the pipeline is bound by host memory bandwidth:
-// DESIGN.md, "End to end").  A chunk with a busy step >= 0xFFFF ticks is
-// derived from the records; traces whose record reports a tick overflow
-// (where grant = end - busy does not hold) are re-simulated with device
-// grants afterwards.
+// memory and end, NEVER otherwise (memshare/harness.py:514-531).  With both
+// tick arrays requested, K5 packs a chunk's end ticks and its per-app busy
+// ticks as u16 (10 B per app at four policies instead of 16 B of u32 end
+// ticks) into pinned staging, and host threads write the caller's grant and
+// end arrays from it (streaming stores) while later chunks are still on the
+// GPU: the pipeline is bound by host memory bandwidth ("End to
+// end").  A chunk whose ticks do not fit 16 bits is copied as u32 end rows
+// (the batch's end ticks stay on the device for the call) and its grants
+// derived from the input records; when most chunks of a call did not fit,
+// the next call of that shape copies u32 end ticks from the start.  Traces
+// whose record reports a tick overflow (where grant = end - busy does not
+// hold) are re-simulated with device grants afterwards.
 namespace {
 
 thread_local uint64_t t_h2d = 0, t_d2h = 0;  // sg_last_host_transfer
@@ -209,6 +212,9 @@ struct PipeStreams {
     size_t stage_cap = 0;
     uint32_t* flags = nullptr;
     size_t flags_cap = 0;
+    // per (apps per trace, policies, devices): the last call found most
+    // chunks beyond 16-bit ticks, so the next one copies u32 end ticks
+    std::map<uint64_t, bool> prefer_u32;
 };
 uint64_t env_u64(const char* name, uint64_t dflt) {
     const char* v = getenv(name);
@@ -405,8 +411,10 @@ int simulate_host(const sg_batch* in, const sg_out* out, int cuda_device, uint64
     }
     const bool derive = host_grant && n_dma < s.npol;
     // All grants derived: end + busy ticks cross PCIe as u16 (K5 pack16)
-    // unless SGPU_PACK16=0; a chunk they do not fit is re-simulated after.
-    const bool use_p16 = allow_pack && derive && n_dma == 0 &&
+    // unless SGPU_PACK16=0 or the last call of this shape on the device found
+    // most chunks beyond 16 bits (then u32 end ticks, with K5 still flagging
+    // each chunk so the choice is re-made on the next call).
+    const bool pack_ok = allow_pack && derive && n_dma == 0 &&
                          !(getenv("SGPU_PACK16") && atoi(getenv("SGPU_PACK16")) == 0);
     const int NBUF = (int)std::min<uint64_t>(std::max<uint64_t>(env_u64("SGPU_PIPE_BUFS", 4), 2), kPipeBufs);
     const size_t app_b = chunk_traces * napps * sizeof(sg_app);
@@ -447,7 +455,17 @@ int simulate_host(const sg_batch* in, const sg_out* out, int cuda_device, uint64
     // bandwidth anyway).
     PipeStreams& ps = pipe_streams(cuda_device);
     std::unique_lock<std::mutex> pipe_lk(ps.mu);
+    const uint64_t shape_key = (uint64_t)napps | (uint64_t)s.npol << 32 | (uint64_t)ndev << 40;
+    const bool use_p16 = pack_ok && !ps.prefer_u32[shape_key];
+    const bool flag_only = pack_ok && !use_p16;  // u32 transfer, K5 overflow flags only
+    uint32_t* d_end_all_c = nullptr;  // (set below; freed here)
     auto cleanup = [&]() {
+        if (d_end_all_c) {  // every stream wrote it: drain them all first
+            for (auto& b : B)
+                if (b.st) cudaStreamSynchronize(b.st);
+            cudaFreeAsync(d_end_all_c, B[0].st);
+        }
+        d_end_all_c = nullptr;
         for (auto& b : B) {
             if (!b.st) continue;
             cudaFreeAsync(b.apps, b.st); cudaFreeAsync(b.grant, b.st); cudaFreeAsync(b.end, b.st);
@@ -467,19 +485,30 @@ int simulate_host(const sg_batch* in, const sg_out* out, int cuda_device, uint64
         b.st = ps.st[i];
         if (e == cudaSuccess) e = cudaMallocAsync(&b.apps, app_b, b.st);
         if (e == cudaSuccess && out->grant && n_dma > 0) e = cudaMallocAsync(&b.grant, tick_b, b.st);
-        if (e == cudaSuccess && out->end) e = cudaMallocAsync(&b.end, tick_b, b.st);
+        if (e == cudaSuccess && out->end && !use_p16) e = cudaMallocAsync(&b.end, tick_b, b.st);
         if (e == cudaSuccess) e = cudaMallocAsync(&b.stats, st_b, b.st);
         if (e == cudaSuccess && want_pct) e = cudaMallocAsync(&b.mem, pct_b, b.st);
         if (e == cudaSuccess && want_pct) e = cudaMallocAsync(&b.dev, pct_b, b.st);
         if (e == cudaSuccess && out->speedup) e = cudaMallocAsync(&b.spd, pct_b, b.st);
-        if (e == cudaSuccess && use_p16) e = cudaMallocAsync(&b.b16, chunk_traces * napps * 2u, b.st);
-        if (e == cudaSuccess && use_p16) e = cudaMallocAsync(&b.e16, tick_b / 2u, b.st);
-        if (e == cudaSuccess && use_p16) e = cudaMallocAsync(&b.flag, 16, b.st);
+        if (e == cudaSuccess && pack_ok) e = cudaMallocAsync(&b.b16, chunk_traces * napps * 2u, b.st);
+        if (e == cudaSuccess && pack_ok) e = cudaMallocAsync(&b.e16, tick_b / 2u, b.st);
+        if (e == cudaSuccess && pack_ok) e = cudaMallocAsync(&b.flag, 16, b.st);
         if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "allocating pipeline buffers"); }
     }
     const uint64_t nch_max = (N + chunk_traces - 1) / chunk_traces;
+    // pack16: the end ticks of the whole batch stay on the device for the
+    // call (a chunk whose ticks do not fit 16 bits is then copied as u32
+    // rows by the host thread that meets it, with no re-simulation)
+    uint32_t* d_end_all = nullptr;
     if (use_p16) {
-        e = grow_pinned(reinterpret_cast<void**>(&ps.stage), ps.stage_cap, (s.npol + 1u) * N * napps * 2u);
+        e = cudaMallocAsync(&d_end_all, (size_t)s.npol * N * napps * sizeof(uint32_t), B[0].st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(B[0].st);
+        if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "allocating the batch's end ticks"); }
+        d_end_all_c = d_end_all;
+    }
+    if (pack_ok) {
+        e = use_p16 ? grow_pinned(reinterpret_cast<void**>(&ps.stage), ps.stage_cap, (s.npol + 1u) * N * napps * 2u)
+                    : cudaSuccess;
         if (e == cudaSuccess) e = grow_pinned(reinterpret_cast<void**>(&ps.flags), ps.flags_cap, nch_max * 4u + 64u);
         if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "pinned pack16 staging"); }
     }
@@ -529,15 +558,15 @@ int simulate_host(const sg_batch* in, const sg_out* out, int cuda_device, uint64
         sg_out co;
         memset(&co, 0, sizeof(co));
         co.grant = b.grant;
-        co.end = b.end;
+        co.end = use_p16 ? d_end_all + a0 : b.end;  // pack16: the batch-wide rows (stride n_apps_total)
         co.stats = b.stats;
         co.mem_pct = out->mem_pct ? b.mem : nullptr;
         co.dev_pct = out->dev_pct ? b.dev : nullptr;
         co.speedup = b.spd;
-        rc = simulate_device(&cb, &co, b.st, na);
+        rc = simulate_device(&cb, &co, b.st, use_p16 ? n_apps_total : na);
         if (rc) { cleanup(); return rc; }
         if (use_p16) {  // the chunk's end + busy ticks as u16 (K5) into the pinned staging
-            e = sg::launch_pack16(b.apps, b.end, na, s.npol, b.b16, b.e16, b.flag, b.st);
+            e = sg::launch_pack16(b.apps, d_end_all + a0, na, n_apps_total, s.npol, b.b16, b.e16, b.flag, b.st);
             for (uint32_t p = 0; p < s.npol && e == cudaSuccess; p++)
                 e = cudaMemcpyAsync(ps.stage + (uint64_t)p * n_apps_total + a0, b.e16 + (uint64_t)p * na, na * 2u,
                                     cudaMemcpyDeviceToHost, b.st);
@@ -548,6 +577,12 @@ int simulate_host(const sg_batch* in, const sg_out* out, int cuda_device, uint64
                 e = cudaMemcpyAsync(ps.flags + (chunk - 1), b.flag, 4, cudaMemcpyDeviceToHost, b.st);
             if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "K5 pack16"); }
             t_d2h += (s.npol + 1u) * na * 2u + 4u;
+        } else if (flag_only) {  // does this chunk fit 16 bits?  (re-decides the next call)
+            e = sg::launch_pack16(b.apps, b.end, na, na, s.npol, b.b16, b.e16, b.flag, b.st);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(ps.flags + (chunk - 1), b.flag, 4, cudaMemcpyDeviceToHost, b.st);
+            if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "K5 flags"); }
+            t_d2h += 4u;
         }
         for (uint32_t p = 0; p < s.npol; p++) {
             const uint64_t ho = (uint64_t)p * n_apps_total + a0;
@@ -613,8 +648,17 @@ int simulate_host(const sg_batch* in, const sg_out* out, int cuda_device, uint64
                     const uint64_t lo = c.t0 + c.nt * w / nthr, hi = c.t0 + c.nt * (w + 1) / nthr;
                     if (!use_p16) {
                         derive_grants(in, out, n_dma, s.npol, lo, hi, ov[w], avx2);
-                    } else if (ps.flags[c.idx]) {  // not exact in 16 bits: re-simulated below
-                        for (uint64_t t = lo; t < hi; t++) ov[w].push_back(t);
+                    } else if (ps.flags[c.idx]) {
+                        // not exact in 16 bits: this thread's traces as u32 end rows
+                        // from the device, grants from the input records
+                        cudaError_t ce2 = cudaSuccess;
+                        for (uint32_t p = 0; p < s.npol && ce2 == cudaSuccess && hi > lo; p++) {
+                            const uint64_t o = (uint64_t)p * n_apps_total + lo * napps;
+                            ce2 = cudaMemcpy(static_cast<uint32_t*>(out->end) + o, d_end_all + o,
+                                             (hi - lo) * napps * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+                        }
+                        if (ce2 != cudaSuccess) { errs[w] = ce2; return; }
+                        derive_grants(in, out, 0, s.npol, lo, hi, ov[w], avx2);
                     } else {
                         expand_ticks16(in, out, ps.stage, s.npol, lo, hi, ov[w], avx2);
                     }
@@ -624,6 +668,11 @@ int simulate_host(const sg_batch* in, const sg_out* out, int cuda_device, uint64
         }
         for (auto& th : pool) th.join();
         if (trace) fprintf(stderr, "[pipe] joined %.2f ms\n", ms());
+        if (pack_ok) {  // most chunks beyond 16 bits: the next call of this shape copies u32 ticks
+            uint64_t wide = 0;
+            for (const auto& c : chunks) wide += ps.flags[c.idx] ? 1u : 0u;
+            ps.prefer_u32[shape_key] = 2 * wide > chunks.size();
+        }
         for (unsigned w = 0; w < nthr; w++) {
             if (errs[w] != cudaSuccess) { cleanup(); return cuda_fail(errs[w], "pipeline"); }
             overflow.insert(overflow.end(), ov[w].begin(), ov[w].end());

@@ -251,11 +251,12 @@ namespace sg {
 // of end ticks (and no 16-byte input record is re-read on the host).
 // *overflow = 1 if the chunk is not exactly representable (a requesting
 // app's busy >= 0xFFFF or an end tick >= 0xFFFF other than SG_NEVER): the
-// host then re-simulates it with u32 outputs.
+// host then copies that chunk's u32 end rows instead.  The end rows of
+// policy p start at end + p * stride.
 
 __global__ void __launch_bounds__(256)
-pack16_kernel(const uint4* __restrict__ apps, const uint32_t* __restrict__ end, uint64_t na, uint32_t npol,
-              uint16_t* __restrict__ b16, uint16_t* __restrict__ e16, uint32_t* overflow) {
+pack16_kernel(const uint4* __restrict__ apps, const uint32_t* __restrict__ end, uint64_t na, uint64_t stride,
+              uint32_t npol, uint16_t* __restrict__ b16, uint16_t* __restrict__ e16, uint32_t* overflow) {
     uint32_t bad = 0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -263,7 +264,7 @@ pack16_kernel(const uint4* __restrict__ apps, const uint32_t* __restrict__ end, 
         bad |= (f.y != 0u) & (f.z >= 0xFFFFu);
         b16[i] = f.y == 0u ? (uint16_t)0xFFFFu : (uint16_t)f.z;
         for (uint32_t p = 0; p < npol; p++) {
-            const uint32_t e = __ldcs(end + p * na + i);
+            const uint32_t e = __ldcs(end + p * stride + i);
             bad |= (e != SG_NEVER) & (e >= 0xFFFFu);
             e16[p * na + i] = (uint16_t)(e == SG_NEVER ? 0xFFFFu : e);
         }
@@ -271,8 +272,8 @@ pack16_kernel(const uint4* __restrict__ apps, const uint32_t* __restrict__ end, 
     if (__any_sync(FULL, bad != 0) && (threadIdx.x & 31) == 0) atomicOr(overflow, 1u);
 }
 
-cudaError_t launch_pack16(const sg_app* apps, const uint32_t* end, uint64_t na, uint32_t npol, uint16_t* b16,
-                          uint16_t* e16, uint32_t* overflow, cudaStream_t stream) {
+cudaError_t launch_pack16(const sg_app* apps, const uint32_t* end, uint64_t na, uint64_t stride, uint32_t npol,
+                          uint16_t* b16, uint16_t* e16, uint32_t* overflow, cudaStream_t stream) {
     cudaError_t e = cudaMemsetAsync(overflow, 0, sizeof(uint32_t), stream);
     if (e != cudaSuccess || na == 0) return e;
     int dev = 0, sms = 0;
@@ -280,8 +281,8 @@ cudaError_t launch_pack16(const sg_app* apps, const uint32_t* end, uint64_t na, 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     uint64_t blocks = (na + 255) / 256;
     if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
-    pack16_kernel<<<(unsigned)blocks, 256, 0, stream>>>(reinterpret_cast<const uint4*>(apps), end, na, npol, b16,
-                                                         e16, overflow);
+    pack16_kernel<<<(unsigned)blocks, 256, 0, stream>>>(reinterpret_cast<const uint4*>(apps), end, na, stride,
+                                                         npol, b16, e16, overflow);
     return cudaGetLastError();
 }
 

@@ -107,9 +107,10 @@ cudaError_t launch_select(uint64_t n_queues, const uint64_t* qoff, const int64_t
                           const int32_t* prio, const int64_t* free_bytes, const uint32_t* kind,
                           uint8_t* granted, cudaStream_t stream);
 // K5: host-pipeline transfer format of a simulated chunk: b16[i] = busy of
-// app i as u16 (0xFFFF = no memory request), e16[p * na + i] = end tick as
-// u16 (0xFFFF = SG_NEVER); *overflow = 1 if that is not exact.
-cudaError_t launch_pack16(const sg_app* apps, const uint32_t* end, uint64_t na, uint32_t npol, uint16_t* b16,
-                          uint16_t* e16, uint32_t* overflow, cudaStream_t stream);
+// app i as u16 (0xFFFF = no memory request), e16[p * na + i] = end tick
+// end[p * stride + i] as u16 (0xFFFF = SG_NEVER); *overflow = 1 if that is
+// not exact.
+cudaError_t launch_pack16(const sg_app* apps, const uint32_t* end, uint64_t na, uint64_t stride, uint32_t npol,
+                          uint16_t* b16, uint16_t* e16, uint32_t* overflow, cudaStream_t stream);
 
 }  // namespace sg

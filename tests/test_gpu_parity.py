@@ -467,6 +467,24 @@ def test_host_pipeline_cases(case, cuda):
         assert (dres.stats()["status"] & 1).any()
 
 
+def test_host_pipeline_transfer_format_switch(cuda):
+    """The pipeline's transfer format follows the data: C4-shaped traces
+    (ticks beyond 16 bits in every chunk) make the next call of that shape
+    copy u32 end ticks, a batch of the same shape that fits 16 bits switches
+    it back; every call is bit-exact with the device path."""
+    wide = as_u32x4(generate(CONFIGS["C4"].gen, 0, 600))
+    g = dataclasses.replace(CONFIGS["C4"].gen, arr_hi=2000, busy_hi=300, mem_lo=1000, mem_hi=30_000)
+    narrow = as_u32x4(generate(g, 0, 600))
+    for apps in (wide, wide, narrow, narrow, wide):
+        dres = run(apps, POLICIES, (184_320,), cuda)
+        pin = B.pinned_apps(*apps.shape[:2])
+        pin[...] = apps
+        host = B.simulate_batch_host(pin, POLICIES, (184_320,), chunk_traces=128)
+        np.testing.assert_array_equal(host.grant, dres.ticks("grant"))
+        np.testing.assert_array_equal(host.end, dres.ticks("end"))
+        np.testing.assert_array_equal(host.stats.view(np.uint8), dres.stats().view(np.uint8))
+
+
 @pytest.mark.parametrize("thr", [1, 3])
 def test_host_pipeline_threads(thr, cuda, monkeypatch):
     """One and three host threads deriving grants, ragged last chunk, two
