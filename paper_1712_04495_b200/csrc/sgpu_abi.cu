@@ -216,6 +216,10 @@ struct PipeStreams {
     // chunks beyond 16-bit ticks, so the next one copies u32 end ticks
     std::map<uint64_t, bool> prefer_u32;
 };
+uint64_t env_u64z(const char* name, uint64_t dflt) {  // accepts 0
+    const char* v = getenv(name);
+    return v && atoll(v) >= 0 ? (uint64_t)atoll(v) : dflt;
+}
 uint64_t env_u64(const char* name, uint64_t dflt) {
     const char* v = getenv(name);
     return v && atoll(v) > 0 ? (uint64_t)atoll(v) : dflt;
@@ -293,18 +297,19 @@ void tick_row16_scalar(const uint16_t* b16, const uint16_t* e16, uint32_t* g, ui
     }
 }
 
-// end and grant ticks of traces [t_lo, t_hi) from the pack16 staging
-// (stage: npol rows of end ticks, then the busy ticks, n_apps_total each);
+// end and grant ticks of policies [p0, npol) for traces [t_lo, t_hi) from
+// the pack16 staging (stage: npol - p0 rows of end ticks, then the busy
+// ticks, n_apps_total each);
 // traces with a tick overflow are skipped and reported.
-void expand_ticks16(const sg_batch* in, const sg_out* out, const uint16_t* stage, uint32_t npol, uint64_t t_lo,
-                    uint64_t t_hi, std::vector<uint64_t>& overflow, bool avx2) {
+void expand_ticks16(const sg_batch* in, const sg_out* out, const uint16_t* stage, uint32_t p0, uint32_t npol,
+                    uint64_t t_lo, uint64_t t_hi, std::vector<uint64_t>& overflow, bool avx2) {
     const uint64_t N = in->n_traces;
     const uint32_t napps = in->apps_per_trace, ndev = in->ndev;
     const uint64_t total = N * napps;
     const sg_trace_stats* st = static_cast<const sg_trace_stats*>(out->stats);
     uint32_t* end = static_cast<uint32_t*>(out->end);
     uint32_t* grant = static_cast<uint32_t*>(out->grant);
-    const uint16_t* b16 = stage + (uint64_t)npol * total;
+    const uint16_t* b16 = stage + (uint64_t)(npol - p0) * total;
     const bool vec = avx2 && (napps % 8 == 0) && (reinterpret_cast<uintptr_t>(grant) & 31u) == 0 &&
                      (reinterpret_cast<uintptr_t>(end) & 31u) == 0 && ((total * 4) & 31u) == 0;
     for (uint64_t t = t_lo; t < t_hi; t++) {
@@ -313,10 +318,10 @@ void expand_ticks16(const sg_batch* in, const sg_out* out, const uint16_t* stage
             for (uint32_t d = 0; d < ndev; d++)
                 ov = ov || (st[((uint64_t)p * N + t) * ndev + d].status & SG_ST_TICK_OVERFLOW);
         if (ov) { overflow.push_back(t); continue; }
-        for (uint32_t p = 0; p < npol; p++) {
-            const uint64_t o = (uint64_t)p * total + t * napps;
-            if (vec) tick_row16_avx2(b16 + t * napps, stage + o, grant + o, end + o, napps);
-            else tick_row16_scalar(b16 + t * napps, stage + o, grant + o, end + o, napps);
+        for (uint32_t p = p0; p < npol; p++) {
+            const uint64_t o = (uint64_t)p * total + t * napps, so = (uint64_t)(p - p0) * total + t * napps;
+            if (vec) tick_row16_avx2(b16 + t * napps, stage + so, grant + o, end + o, napps);
+            else tick_row16_scalar(b16 + t * napps, stage + so, grant + o, end + o, napps);
         }
     }
     if (vec) _mm_sfence();
@@ -458,14 +463,21 @@ int simulate_host(const sg_batch* in, const sg_out* out, int cuda_device, uint64
     const uint64_t shape_key = (uint64_t)napps | (uint64_t)s.npol << 32 | (uint64_t)ndev << 40;
     const bool use_p16 = pack_ok && !ps.prefer_u32[shape_key];
     const bool flag_only = pack_ok && !use_p16;  // u32 transfer, K5 overflow flags only
+    // pack16: the first k policies still cross as u32 grant + end rows
+    // straight into the caller's arrays (PCIe instead of host memory: the
+    // two are balanced at k ~ npol / 2 on a host-memory-bound box;
+    // SGPU_DIRECT_POLS=k)
+    const uint32_t k_dir = use_p16 ? (uint32_t)std::min<uint64_t>(env_u64z("SGPU_DIRECT_POLS", 0), s.npol - 1u) : 0u;
     uint32_t* d_end_all_c = nullptr;  // (set below; freed here)
+    uint32_t* d_grant_all_c = nullptr;
     auto cleanup = [&]() {
-        if (d_end_all_c) {  // every stream wrote it: drain them all first
+        if (d_end_all_c || d_grant_all_c) {  // every stream wrote them: drain them all first
             for (auto& b : B)
                 if (b.st) cudaStreamSynchronize(b.st);
-            cudaFreeAsync(d_end_all_c, B[0].st);
+            if (d_end_all_c) cudaFreeAsync(d_end_all_c, B[0].st);
+            if (d_grant_all_c) cudaFreeAsync(d_grant_all_c, B[0].st);
         }
-        d_end_all_c = nullptr;
+        d_end_all_c = d_grant_all_c = nullptr;
         for (auto& b : B) {
             if (!b.st) continue;
             cudaFreeAsync(b.apps, b.st); cudaFreeAsync(b.grant, b.st); cudaFreeAsync(b.end, b.st);
@@ -500,6 +512,12 @@ int simulate_host(const sg_batch* in, const sg_out* out, int cuda_device, uint64
     // call (a chunk whose ticks do not fit 16 bits is then copied as u32
     // rows by the host thread that meets it, with no re-simulation)
     uint32_t* d_end_all = nullptr;
+    uint32_t* d_grant_all = nullptr;
+    if (use_p16 && k_dir > 0) {  // the kernel writes grants of every policy when asked for any
+        e = cudaMallocAsync(&d_grant_all, (size_t)s.npol * N * napps * sizeof(uint32_t), B[0].st);
+        if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "allocating the batch's grant ticks"); }
+        d_grant_all_c = d_grant_all;
+    }
     if (use_p16) {
         e = cudaMallocAsync(&d_end_all, (size_t)s.npol * N * napps * sizeof(uint32_t), B[0].st);
         if (e == cudaSuccess) e = cudaStreamSynchronize(B[0].st);
@@ -507,7 +525,8 @@ int simulate_host(const sg_batch* in, const sg_out* out, int cuda_device, uint64
         d_end_all_c = d_end_all;
     }
     if (pack_ok) {
-        e = use_p16 ? grow_pinned(reinterpret_cast<void**>(&ps.stage), ps.stage_cap, (s.npol + 1u) * N * napps * 2u)
+        e = use_p16 ? grow_pinned(reinterpret_cast<void**>(&ps.stage), ps.stage_cap,
+                                  (s.npol - k_dir + 1u) * N * napps * 2u)
                     : cudaSuccess;
         if (e == cudaSuccess) e = grow_pinned(reinterpret_cast<void**>(&ps.flags), ps.flags_cap, nch_max * 4u + 64u);
         if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "pinned pack16 staging"); }
@@ -557,7 +576,7 @@ int simulate_host(const sg_batch* in, const sg_out* out, int cuda_device, uint64
         cb.apps = b.apps;
         sg_out co;
         memset(&co, 0, sizeof(co));
-        co.grant = b.grant;
+        co.grant = use_p16 && k_dir ? d_grant_all + a0 : b.grant;
         co.end = use_p16 ? d_end_all + a0 : b.end;  // pack16: the batch-wide rows (stride n_apps_total)
         co.stats = b.stats;
         co.mem_pct = out->mem_pct ? b.mem : nullptr;
@@ -566,17 +585,28 @@ int simulate_host(const sg_batch* in, const sg_out* out, int cuda_device, uint64
         rc = simulate_device(&cb, &co, b.st, use_p16 ? n_apps_total : na);
         if (rc) { cleanup(); return rc; }
         if (use_p16) {  // the chunk's end + busy ticks as u16 (K5) into the pinned staging
-            e = sg::launch_pack16(b.apps, d_end_all + a0, na, n_apps_total, s.npol, b.b16, b.e16, b.flag, b.st);
-            for (uint32_t p = 0; p < s.npol && e == cudaSuccess; p++)
+            const uint32_t np16 = s.npol - k_dir;
+            e = sg::launch_pack16(b.apps, d_end_all + (uint64_t)k_dir * n_apps_total + a0, na, n_apps_total, np16,
+                                  b.b16, b.e16, b.flag, b.st);
+            for (uint32_t p = 0; p < np16 && e == cudaSuccess; p++)
                 e = cudaMemcpyAsync(ps.stage + (uint64_t)p * n_apps_total + a0, b.e16 + (uint64_t)p * na, na * 2u,
                                     cudaMemcpyDeviceToHost, b.st);
             if (e == cudaSuccess)
-                e = cudaMemcpyAsync(ps.stage + (uint64_t)s.npol * n_apps_total + a0, b.b16, na * 2u,
+                e = cudaMemcpyAsync(ps.stage + (uint64_t)np16 * n_apps_total + a0, b.b16, na * 2u,
                                     cudaMemcpyDeviceToHost, b.st);
+            // the first k_dir policies: u32 rows straight into the caller's arrays
+            for (uint32_t p = 0; p < k_dir && e == cudaSuccess; p++) {
+                const uint64_t o = (uint64_t)p * n_apps_total + a0;
+                e = cudaMemcpyAsync(static_cast<uint32_t*>(out->end) + o, d_end_all + o, na * 4u,
+                                    cudaMemcpyDeviceToHost, b.st);
+                if (e == cudaSuccess)
+                    e = cudaMemcpyAsync(static_cast<uint32_t*>(out->grant) + o, d_grant_all + o, na * 4u,
+                                        cudaMemcpyDeviceToHost, b.st);
+            }
             if (e == cudaSuccess)
                 e = cudaMemcpyAsync(ps.flags + (chunk - 1), b.flag, 4, cudaMemcpyDeviceToHost, b.st);
             if (e != cudaSuccess) { cleanup(); return cuda_fail(e, "K5 pack16"); }
-            t_d2h += (s.npol + 1u) * na * 2u + 4u;
+            t_d2h += (np16 + 1u) * na * 2u + 4u + (uint64_t)k_dir * na * 8u;
         } else if (flag_only) {  // does this chunk fit 16 bits?  (re-decides the next call)
             e = sg::launch_pack16(b.apps, b.end, na, na, s.npol, b.b16, b.e16, b.flag, b.st);
             if (e == cudaSuccess)
@@ -652,15 +682,15 @@ int simulate_host(const sg_batch* in, const sg_out* out, int cuda_device, uint64
                         // not exact in 16 bits: this thread's traces as u32 end rows
                         // from the device, grants from the input records
                         cudaError_t ce2 = cudaSuccess;
-                        for (uint32_t p = 0; p < s.npol && ce2 == cudaSuccess && hi > lo; p++) {
+                        for (uint32_t p = k_dir; p < s.npol && ce2 == cudaSuccess && hi > lo; p++) {
                             const uint64_t o = (uint64_t)p * n_apps_total + lo * napps;
                             ce2 = cudaMemcpy(static_cast<uint32_t*>(out->end) + o, d_end_all + o,
                                              (hi - lo) * napps * sizeof(uint32_t), cudaMemcpyDeviceToHost);
                         }
                         if (ce2 != cudaSuccess) { errs[w] = ce2; return; }
-                        derive_grants(in, out, 0, s.npol, lo, hi, ov[w], avx2);
+                        derive_grants(in, out, k_dir, s.npol, lo, hi, ov[w], avx2);
                     } else {
-                        expand_ticks16(in, out, ps.stage, s.npol, lo, hi, ov[w], avx2);
+                        expand_ticks16(in, out, ps.stage, k_dir, s.npol, lo, hi, ov[w], avx2);
                     }
                     if (trace && w == 0) fprintf(stderr, "[pipe] chunk at trace %llu ready %.2f derived %.2f ms\n", (unsigned long long)c.t0, tr, ms());
                 }

@@ -467,6 +467,26 @@ def test_host_pipeline_cases(case, cuda):
         assert (dres.stats()["status"] & 1).any()
 
 
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_host_pipeline_direct_policies(k, cuda, monkeypatch):
+    """SGPU_DIRECT_POLS=k: the first k policies cross PCIe as u32 grant + end
+    rows, the others as pack16; with chunks that fit 16 bits, a chunk that
+    does not, apps without a request and a tick overflow."""
+    monkeypatch.setenv("SGPU_DIRECT_POLS", str(k))
+    apps = as_u32x4(generate(CONFIGS["C2"].gen, 0, 700))
+    apps[200:202, :, 0] += 100_000          # chunk 1: ends beyond 16 bits
+    apps[400:402, ::3, 1] = 0               # apps without a memory request
+    apps[600, :, 2] = np.uint32(0x7FFFFFF)  # sum(busy) past 2^32 ticks
+    dres = run(apps, POLICIES, (184_320,), cuda)
+    pin = B.pinned_apps(*apps.shape[:2])
+    pin[...] = apps
+    for _ in range(2):
+        host = B.simulate_batch_host(pin, POLICIES, (184_320,), chunk_traces=128)
+        np.testing.assert_array_equal(host.grant, dres.ticks("grant"))
+        np.testing.assert_array_equal(host.end, dres.ticks("end"))
+        np.testing.assert_array_equal(host.stats.view(np.uint8), dres.stats().view(np.uint8))
+
+
 def test_host_pipeline_transfer_format_switch(cuda):
     """The pipeline's transfer format follows the data: C4-shaped traces
     (ticks beyond 16 bits in every chunk) make the next call of that shape
