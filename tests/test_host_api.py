@@ -67,6 +67,29 @@ def test_encode_dyadic_grid_and_flattening():
     assert np.frombuffer(np.uint64(enc.steps[0]["dur"]).tobytes(), np.float64)[0] == 0.9
 
 
+def test_encode_shared_profiles_like_distinct_ones():
+    """Instances sharing an AppProfile object are encoded once per call; the
+    encoding equals that of a spec whose instances are distinct copies
+    (steps, offsets, attributes, tick grid), including the tick-grid bound
+    that counts every instance (harness.py:478-490)."""
+    import copy
+    P = S.builtin_profiles()
+    shared = [P["ara-like"]] * 5 + [P["mummer-like"]] * 3 + [P["blast-like"]] * 2 + [P["ara-like"]]
+    distinct = [copy.deepcopy(p) for p in shared]
+    for t_scale in (1.0, 0.75, 1000 / 1024):
+        a = encode_spec(S.WorkloadSpec(instances=shared, time_scale=t_scale))
+        b = encode_spec(S.WorkloadSpec(instances=distinct, time_scale=t_scale))
+        assert (a.time_mode, a.tick_log2, a.cap_mib) == (b.time_mode, b.tick_log2, b.cap_mib)
+        assert a.steps.tobytes() == b.steps.tobytes()
+        assert a.step_offsets.tolist() == b.step_offsets.tolist()
+        assert a.attr.tolist() == b.attr.tolist()
+    # the exact-sum bound counts every instance: many copies push a dyadic
+    # grid past 2^32 ticks and into float64 mode
+    long = S.AppProfile("long", [S.Phase(cpu_ms=2 ** 21 * 1000.0)])
+    assert encode_spec(S.WorkloadSpec(instances=[long] * 2)).time_mode == _lib.TIME_TICKS
+    assert encode_spec(S.WorkloadSpec(instances=[long] * 4096)).time_mode == _lib.TIME_F64
+
+
 def test_priorities_become_dense_ranks():
     prof = lambda p: S.AppProfile("x", [S.Phase(alloc_mib=1, free_mib=1)], priority=p)
     enc = encode_spec(S.WorkloadSpec(instances=[prof(100), prof(-5), prof(100), prof(7)]))
