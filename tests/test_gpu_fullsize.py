@@ -2,9 +2,9 @@
 C3: 1M x 256, C4: 4M x 128, C5: one GPU's 2M-trace shard of 16M x 64 apps
 on 8 simulated devices), where the CPU oracle cannot check every trace:
 
-* the two K1 engines (lane kernel v5 and warp kernel v3: different
-  algorithms, shared only the output record code) agree bit for bit on
-  every output of the whole batch;
+* the K1 engines (lane kernel v7, warp kernel v3 and, at 256 apps, the
+  octet kernel v8: different algorithms sharing only the output record
+  code) agree bit for bit on every output of the whole batch;
 * a stratified sample of traces across the batch matches the oracle
   (oracle/, the C restatement of memshare.harness.simulate) bit for bit;
 * size-independent invariants hold on every record: every app is granted
@@ -29,6 +29,11 @@ pytestmark = pytest.mark.gpu
 SHARD = {"C2": 1 << 20, "C3": 1 << 20, "C4": 4 << 20, "C5": (16 << 20) // 8}
 
 
+def bits(t):
+    """Bit pattern of a float64 tensor (NaN-safe exact comparison)."""
+    return t.view(torch.int64) if t.dtype == torch.float64 else t
+
+
 def run_engine(apps, cfg, engine, monkeypatch):
     monkeypatch.setenv("SGPU_K1", engine)
     res = B.simulate_batch(apps, cfg.policies, cfg.cap_mib)
@@ -45,8 +50,13 @@ def test_full_size(cname, cuda, monkeypatch):
     apps = B.generate_traces(cfg.gen, 0, n, device=0)
     lane = run_engine(apps, cfg, "lane", monkeypatch)
     warp = run_engine(apps, cfg, "warp", monkeypatch)
-    for f in ("grant", "end", "stats_raw", "mem_pct", "dev_pct"):
-        assert torch.equal(getattr(lane, f), getattr(warp, f)), f"{cname}: engines differ in {f}"
+    for f in ("grant", "end", "stats_raw", "mem_pct", "dev_pct", "speedup"):
+        assert torch.equal(bits(getattr(lane, f)), bits(getattr(warp, f))), f"{cname}: engines differ in {f}"
+    if cname == "C3":  # 256-app traces: the octet kernel (v8) is the default engine there
+        octet = run_engine(apps, cfg, "octet", monkeypatch)
+        for f in ("grant", "end", "stats_raw", "mem_pct", "dev_pct", "speedup"):
+            assert torch.equal(bits(getattr(octet, f)), bits(getattr(warp, f))), f"C3: octet and warp engines differ in {f}"
+        del octet
     del warp
 
     # stratified oracle sample: 1,200 traces spread over the batch
