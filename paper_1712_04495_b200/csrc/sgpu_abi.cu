@@ -1,6 +1,7 @@
 // sgpu_abi.cu — extern "C" entry points of libsgpu.so (include/sgpu.h):
 // argument validation, kernel dispatch, and the host-buffer pipeline.
 #include <algorithm>
+#include <cctype>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -10,6 +11,8 @@
 #include <mutex>
 #include <thread>
 #include <immintrin.h>
+#include <pthread.h>
+#include <sched.h>
 #include <map>
 #include <memory>
 #include <vector>
@@ -216,6 +219,36 @@ struct PipeStreams {
     // chunks beyond 16-bit ticks, so the next one copies u32 end ticks
     std::map<uint64_t, bool> prefer_u32;
 };
+// The CPUs local to a GPU (its PCI device's NUMA node, from sysfs): the host
+// pipeline's threads run there, next to the memory the GPU's DMA uses.
+// Returns the number of CPUs in `set` (0: unknown, leave affinity alone).
+int gpu_local_cpus(int dev, cpu_set_t* set) {
+    CPU_ZERO(set);
+    char bus[32] = {0};
+    if (cudaDeviceGetPCIBusId(bus, sizeof(bus), dev) != cudaSuccess) return 0;
+    for (char* c = bus; *c; c++) *c = (char)tolower(*c);
+    char path[128];
+    snprintf(path, sizeof(path), "/sys/bus/pci/devices/%s/local_cpulist", bus);
+    FILE* f = fopen(path, "r");
+    if (!f) return 0;
+    char buf[1024] = {0};
+    const size_t got = fread(buf, 1, sizeof(buf) - 1, f);
+    fclose(f);
+    buf[got] = 0;
+    // "0-15,32-47"
+    for (char* tok = strtok(buf, ",\n"); tok; tok = strtok(nullptr, ",\n")) {
+        int a = -1, b = -1;
+        if (sscanf(tok, "%d-%d", &a, &b) == 2) {
+        } else if (sscanf(tok, "%d", &a) == 1) {
+            b = a;
+        } else {
+            continue;
+        }
+        for (int c = a; c <= b && c >= 0 && c < CPU_SETSIZE; c++) CPU_SET(c, set);
+    }
+    return CPU_COUNT(set);
+}
+
 uint64_t env_u64z(const char* name, uint64_t dflt) {  // accepts 0
     const char* v = getenv(name);
     return v && atoll(v) >= 0 ? (uint64_t)atoll(v) : dflt;
@@ -665,12 +698,18 @@ int simulate_host(const sg_batch* in, const sg_out* out, int cuda_device, uint64
             const int v = atoi(ev);
             if (v > 0 && v <= 256) nthr = (unsigned)v;
         }
+        // threads on the GPU's NUMA node (SGPU_NUMA_BIND=0: no binding)
+        cpu_set_t local;
+        const bool bind = !(getenv("SGPU_NUMA_BIND") && atoi(getenv("SGPU_NUMA_BIND")) == 0) &&
+                          gpu_local_cpus(cuda_device, &local) > 0;
         std::vector<std::vector<uint64_t>> ov(nthr);
         std::vector<cudaError_t> errs(nthr, cudaSuccess);
         std::vector<std::thread> pool;
-        if (trace) fprintf(stderr, "[pipe] enqueued %zu chunks at %.2f ms\n", chunks.size(), ms());
+        if (trace) fprintf(stderr, "[pipe] enqueued %zu chunks at %.2f ms (threads %u, numa bind %d)\n",
+                           chunks.size(), ms(), nthr, (int)bind);
         for (unsigned w = 0; w < nthr; w++) {
             pool.emplace_back([&, w]() {
+                if (bind) pthread_setaffinity_np(pthread_self(), sizeof(local), &local);
                 for (const auto& c : chunks) {
                     const cudaError_t ce = cudaEventSynchronize(c.done);
                     if (ce != cudaSuccess) { errs[w] = ce; return; }
