@@ -20,9 +20,10 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB_NAME = "libsgpu.so"
 LIB_PATH = os.path.join(HERE, LIB_NAME)
 
-SOURCES = ["sgpu_sim.cu", "sgpu_lane.cu", "sgpu_octet.cu", "sgpu_proglane.cu", "sgpu_aux.cu", "sgpu_abi.cu"]
+SOURCES = ["sgpu_sim.cu", "sgpu_lane.cu", "sgpu_octet.cu", "sgpu_lane256.cu", "sgpu_proglane.cu", "sgpu_aux.cu",
+           "sgpu_abi.cu"]
 DEPS = SOURCES + ["sgpu_common.cuh", "sgpu_internal.h", "sgpu_tracesim.cuh", "sgpu_lanesim.cuh",
-                  "sgpu_proglanesim.cuh", "sgpu_warpsort.cuh"]
+                  "sgpu_proglanesim.cuh", "sgpu_warpsort.cuh", "sgpu_stage256.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -145,15 +145,21 @@ static int simulate_device(const sg_batch* in, const sg_out* out, cudaStream_t s
     const bool want_warp = eng && strcmp(eng, "warp") == 0;
     const bool want_lane = eng && strcmp(eng, "lane") == 0;
     const bool want_octet = eng && strcmp(eng, "octet") == 0;
+    const bool want_l256 = eng && strcmp(eng, "lane256") == 0;
     const bool lane_ok = sg::lane_eligible(p, s.program, s.f64, want_lane);
     const bool prog_ok = sg::prog_lane_eligible(p, s.program, s.f64, want_lane);
     const bool oct_ok = !want_lane && sg::octet_eligible(p, s.program, s.f64);
     if (want_lane && !lane_ok && !prog_ok) return fail(E_ARG, "SGPU_K1=lane: batch not eligible for a lane kernel");
     if (want_octet && !oct_ok) return fail(E_ARG, "SGPU_K1=octet: batch not eligible for the octet kernel");
+    const bool l256_ok = want_l256 && sg::lane256_eligible(p, s.program, s.f64);
+    if (want_l256 && !l256_ok) return fail(E_ARG, "SGPU_K1=lane256: batch not eligible for the lane256 kernel");
     cudaError_t e;
     if (prog_ok && !want_warp) {
         e = sg::launch_sim_prog_lane(p, stream, nullptr);
         if (e != cudaSuccess) return cuda_fail(e, "trace_prog_lane launch");
+    } else if (l256_ok) {
+        e = sg::launch_sim_lane256(p, stream, nullptr);
+        if (e != cudaSuccess) return cuda_fail(e, "trace_sim_lane256 launch");
     } else if (oct_ok && !want_warp) {
         e = sg::launch_sim_octet(p, stream, nullptr);
         if (e != cudaSuccess) return cuda_fail(e, "trace_sim_octet launch");

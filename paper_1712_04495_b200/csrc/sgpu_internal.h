@@ -91,6 +91,11 @@ cudaError_t launch_sim_lane(const SimParams& p, cudaStream_t stream, int* grid_o
 // fallback to TraceSim.
 bool octet_eligible(const SimParams& p, bool program_mode, bool f64);
 cudaError_t launch_sim_octet(const SimParams& p, cudaStream_t stream, int* grid_out);
+// K1 v9: lane-per-(trace, policy) kernel for the same batches as v8, its
+// staged trace tables in global memory (sgpu_lane256.cu), with an in-kernel
+// exact fallback to TraceSim.
+bool lane256_eligible(const SimParams& p, bool program_mode, bool f64);
+cudaError_t launch_sim_lane256(const SimParams& p, cudaStream_t stream, int* grid_out);
 // K1 v6: lane-per-(trace, policy) kernel for step-program tick-mode batches
 // (sgpu_proglane.cu), with an in-kernel exact fallback to TraceSim.
 bool prog_lane_eligible(const SimParams& p, bool program_mode, bool f64, bool forced);

@@ -85,7 +85,9 @@ template <int K, bool NARROW, uint32_t HW = kLaneHeapW> struct LaneKey {
     static constexpr uint32_t QB = NARROW ? LOGN : 8u;
     static constexpr uint32_t TS = NARROW ? 2u * LOGN + 1u : 32u;
     static constexpr T INF = (T)~(T)0;
-    static constexpr uint32_t HCAP = NARROW ? kLaneHeapN : HW;
+    // heap capacity: kLaneHeapN with 32-bit keys (or HW if larger), HW with
+    // 64-bit keys
+    static constexpr uint32_t HCAP = NARROW ? (HW > kLaneHeapN ? HW : kLaneHeapN) : HW;
     static constexpr uint32_t LIM = NARROW ? (1u << (32u - TS)) - 1u : ~0u;
     static constexpr uint32_t CMAX = NARROW ? 2u << LOGN : 1u << 24;  // counters must stay below
     static SG_HD T make(uint32_t t, uint32_t c, uint32_t q) {
@@ -98,22 +100,40 @@ template <int K, bool NARROW, uint32_t HW = kLaneHeapW> struct LaneKey {
     static SG_HD uint32_t c_base(uint32_t n) { return NARROW ? 32u * K : n << LOGN; }
 };
 
-template <int K, bool NARROW, uint32_t HW = kLaneHeapW, uint32_t FSt = FitStride<K>::v>
+template <int K, bool NARROW, uint32_t HW = kLaneHeapW, uint32_t FSt = FitStride<K>::v, bool TB = (K <= 4),
+          bool SY = false>
 struct LaneSim {
     static constexpr uint32_t N = 32u * K;
     static constexpr uint32_t NW = (N + 63u) / 64u;  // queue mask words
     static constexpr uint32_t LOGN = LogN<K>::v;
-    static constexpr bool TBL = K <= 4;              // fit table (one or two mask words)
+    // fit table (one to four mask words): up to 128 apps in the lane kernel,
+    // 256 in the global-table kernel (sgpu_lane256.cu); else a queue scan
+    static constexpr bool TBL = TB;
     using KY = LaneKey<K, NARROW, HW>;
     using Key = typename KY::T;
+    // rank / position tables: u8 up to 128 apps, u16 at 256 (rank N = 256)
+    using PT = typename std::conditional<(K > 4 && TB), uint16_t, uint8_t>::type;
+    // heaps of more than 21 keys sift over three levels (root + 4 + 16 + 64)
+    static constexpr bool DEEP = KY::HCAP > 21;
+    // SY: the lanes running the main loop (smask, set by the caller) meet
+    // at a ballot at the end of every iteration, so they re-converge per
+    // event (without it the 256-app instantiation let lanes drift into
+    // different iterations: 3 active lanes per instruction)
+    uint32_t smask;
+    SG_HD void sync_iter(bool stop) {
+#ifdef __CUDACC__
+        if constexpr (SY) smask = __ballot_sync(smask, !stop);
+#endif
+        (void)stop;
+    }
 
     const SimParams& P;
     // trace slot (shared by the trace's lanes), arrival-position order
     const uint32_t* s_a;     // arrival tick
     const uint32_t* s_mem;   // request MiB
     const uint32_t* s_bw;    // busy | app << kBusyBits | class << kClsShift
-    const uint8_t* s_por;    // position of the r-th smallest request (N past the end)
-    const uint8_t* s_lt;     // s_lt[j] = #requests in buckets < j
+    const PT* s_por;         // position of the r-th smallest request (N past the end)
+    const PT* s_lt;          // s_lt[j] = #requests in buckets < j
     uint32_t lt_lo, lt_hi, lt_scale;
     const uint64_t* s_t4;    // T[FS j] (NW words): positions of the FS j smallest requests
     const uint64_t* s_cm;    // class masks (NW words each) of this lane's device, top class first
@@ -162,8 +182,8 @@ struct LaneSim {
         if (hs >= KY::HCAP || c >= KY::CMAX) { fail = true; return; }
         const Key key = KY::make(t, c, q);
         const uint32_t i = hs++;
-        // sift up at most two levels: i -> p1 -> p2; both parent loads are
-        // issued at once (their indices follow from the size alone)
+        // sift up at most two (three) levels: i -> p1 -> p2 (-> p3); the
+        // parent loads are issued at once (their indices follow from the size)
         const uint32_t p1 = i > 0 ? (i - 1) >> 2 : 0u;
         const uint32_t p2 = p1 > 0 ? (p1 - 1) >> 2 : 0u;
         const Key k1 = heap[p1 * 32];
@@ -172,7 +192,14 @@ struct LaneSim {
         const bool up2 = up1 && p1 > 0 && key < k2;
         if (up1) heap[i * 32] = k1;
         if (up2) heap[p1 * 32] = k2;
-        const uint32_t dst = up2 ? p2 : (up1 ? p1 : i);
+        uint32_t dst = up2 ? p2 : (up1 ? p1 : i);
+        if constexpr (DEEP) {
+            const uint32_t p3 = p2 > 0 ? (p2 - 1) >> 2 : 0u;
+            const Key k3 = heap[p3 * 32];
+            const bool up3 = up2 && p2 > 0 && key < k3;
+            if (up3) heap[p2 * 32] = k3;
+            dst = up3 ? p3 : dst;
+        }
         heap[dst * 32] = key;
         if (dst == 0) kh = key;
     }
@@ -204,8 +231,17 @@ struct LaneSim {
         const Key k2 = min_child(4u * m1 + 1u, m2);
         const bool down2 = down1 && k2 < lastk;
         heap[0] = down1 ? k1 : lastk;
-        if (down1) heap[m1 * 32] = down2 ? k2 : lastk;
-        if (down2) heap[m2 * 32] = lastk;
+        if constexpr (DEEP) {  // level 3: children of m2 (21..84)
+            uint32_t m3;
+            const Key k3 = min_child(4u * m2 + 1u, m3);
+            const bool down3 = down2 && k3 < lastk;
+            if (down1) heap[m1 * 32] = down2 ? k2 : lastk;
+            if (down2) heap[m2 * 32] = down3 ? k3 : lastk;
+            if (down3) heap[m3 * 32] = lastk;
+        } else {
+            if (down1) heap[m1 * 32] = down2 ? k2 : lastk;
+            if (down2) heap[m2 * 32] = lastk;
+        }
         kh = hs == 0 ? KY::INF : (down1 ? k1 : lastk);
     }
 
@@ -279,11 +315,13 @@ struct LaneSim {
             for (uint32_t w = 0; w < NW; w++)
                 t[w] |= (r & 1u) && (NW == 1 || w == (p >> 6)) ? 1ull << (p & 63u) : 0ull;
         } else {
-            const uint32_t pw = *reinterpret_cast<const uint32_t*>(s_por + (r & ~3u));
+            // the 4 entries from rank r & ~3 in one load (u8: 32 bits, u16: 64)
+            using PW = typename std::conditional<sizeof(PT) == 1, uint32_t, uint64_t>::type;
+            const PW pw = *reinterpret_cast<const PW*>(s_por + (r & ~3u));
             const uint32_t k = r & 3u;
 #pragma unroll
             for (uint32_t j = 0; j < 3; j++) {
-                const uint32_t p = (pw >> (8u * j)) & 0xFFu;
+                const uint32_t p = (uint32_t)(pw >> (8u * sizeof(PT) * j)) & ((1u << (8u * sizeof(PT))) - 1u);
 #pragma unroll
                 for (uint32_t w = 0; w < NW; w++)
                     t[w] |= k > j && (NW == 1 || w == (p >> 6)) ? 1ull << (p & 63u) : 0ull;
@@ -554,7 +592,7 @@ struct LaneSim {
                     }
                 }
             }
-            if (fail) return false;
+            if (fail) break;  // (into the main loop, which stops at once: SY lanes meet there)
         }
         ap = s + z;
         ae = e;
@@ -565,11 +603,15 @@ struct LaneSim {
         }
         while (true) {
             SG_LANE_ITER_HOOK(gs);
-            if (!gs) {
+            bool stop = fail;
+            if (!gs && !stop) {
                 // next event: the smaller of the arrival / heap keys (busy
                 // ends and the frees of granted waiters without a busy step)
                 const Key kmin = ka < kh ? ka : kh;
-                if (kmin == KY::INF) break;
+                stop = kmin == KY::INF;
+            }
+            if (!gs && !stop) {
+                const Key kmin = ka < kh ? ka : kh;
                 const bool is_arr = ka < kh;
                 const uint32_t q = KY::pos(kmin);
                 const uint32_t now = KY::time(kmin);
@@ -611,14 +653,18 @@ struct LaneSim {
                 counter = pc + (start ? 1u : 0u);
                 if ((is_arr && !enq && b == 0) || !is_arr) end_app(m, bw, now);
             }
-            if constexpr (TBL) {
-                if (gs) grant_step();
+            if (!stop) {
+                if constexpr (TBL) {
+                    if (gs) grant_step();
+                }
+                // at most one push per iteration: an arrival's busy end, or the
+                // entry of the waiter this iteration's grant step granted
+                if (pp) push(pt, pc, pq);
+                pp = false;
             }
-            // at most one push per iteration: an arrival's busy end, or the
-            // entry of the waiter this iteration's grant step granted
-            if (pp) push(pt, pc, pq);
-            pp = false;
-            if (fail) return false;
+            stop = stop || fail;
+            sync_iter(stop);
+            if (stop) break;
         }
         return !fail;
     }

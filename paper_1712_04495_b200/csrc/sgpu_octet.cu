@@ -30,15 +30,16 @@
 #include <cstring>
 
 #include "sgpu_lanesim.cuh"
+#include "sgpu_stage256.cuh"
 #include "sgpu_warpsort.cuh"
 
 namespace sg {
 
 constexpr uint32_t kOctN = 256;       // positions per trace (n_pad)
-constexpr uint32_t kOctFS = 4;        // fit-table stride (ranks)
+constexpr uint32_t kOctFS = kStage256FS;  // fit-table stride (ranks)
 constexpr uint32_t kOctLB = 256;      // rank-lookup buckets
 constexpr uint32_t kOctSlots = 4;     // busy-set keys per lane (32 per simulation)
-constexpr uint32_t kOctMaxCls = 8;    // priority classes per trace on this path
+constexpr uint32_t kOctMaxCls = kStage256MaxCls;  // priority classes per trace on this path
 constexpr int kOctWarpsPerBlock = 2;
 constexpr int kOctMinBlocks = 8;      // 16 warps/SM: <= 128 registers
 
@@ -57,7 +58,7 @@ struct OctSlot {
     static constexpr uint32_t LTB = kOctLB + 8;            // u16 buckets, then lo / hi / scale (u32)
     static constexpr uint32_t TBL = (kOctN / kOctFS + 1) * 8;  // fit rows, 8 u32 words each
     static constexpr uint32_t CM = kOctMaxCls * 8;         // class masks, 8 u32 words each
-    static constexpr uint32_t META = 8;                    // u32: n, fail, z, ncls, seq lo, seq hi
+    static constexpr uint32_t META = 8;                    // u32 (sgpu_stage256.cuh)
 };
 
 // ------------------------------------------------------------ octet ops
@@ -405,181 +406,19 @@ struct OctSim {
 };
 
 // ------------------------------------------------------------ staging
-// Stage trace t into slot g: SoA records in (arrival, index) order, class
-// masks (distinct priorities, highest first), the fit table (rows of 8
-// words at every kOctFS-th rank), the rank-lookup buckets, and meta.
-// Warp-collective.
+// Stage trace t into slot g (sgpu_stage256.cuh, in this warp's shared memory).
 __device__ __forceinline__ void oct_stage(const OctParams& L, uint8_t* ws, uint32_t g, uint64_t t, uint32_t lane) {
-    const SimParams& P = L.sp;
-    constexpr uint32_t N = kOctN;
-    constexpr int K = 8;  // apps per lane
-    uint64_t a0;
-    uint32_t na;
-    if (P.trace_offsets) {
-        const uint64_t o0 = P.trace_offsets[0];
-        a0 = P.trace_offsets[t] - o0;
-        na = (uint32_t)(P.trace_offsets[t + 1] - P.trace_offsets[t]);
-    } else {
-        a0 = t * P.apps_per_trace;
-        na = P.apps_per_trace;
-    }
-    const uint4* src = reinterpret_cast<const uint4*>(P.apps + a0);
-    uint32_t* s_a = reinterpret_cast<uint32_t*>(ws + L.off_a) + g * OctSlot::S32;
-    uint32_t* s_mem = reinterpret_cast<uint32_t*>(ws + L.off_mem) + g * OctSlot::S32;
-    uint32_t* s_bw = reinterpret_cast<uint32_t*>(ws + L.off_bw) + g * OctSlot::S32;
-    uint16_t* s_por = reinterpret_cast<uint16_t*>(ws + L.off_por) + g * OctSlot::POR;
-    uint16_t* s_lt = reinterpret_cast<uint16_t*>(ws + L.off_lt) + g * OctSlot::LTB;
-    uint32_t* s_tbl = reinterpret_cast<uint32_t*>(ws + L.off_tbl) + g * OctSlot::TBL;
-    uint32_t* s_cm = reinterpret_cast<uint32_t*>(ws + L.off_cm) + g * OctSlot::CM;
-    uint32_t* meta = reinterpret_cast<uint32_t*>(ws + L.off_meta) + g * OctSlot::META;
-    uint16_t* s_rank = reinterpret_cast<uint16_t*>(ws + L.off_scr);  // position -> rank (scratch)
-
-    uint64_t key[K];
-    bool big = false;
-    uint32_t amax = 0, seq_lo = 0, seq_hi = 0;
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-        const uint32_t i = (uint32_t)k * 32u + lane;
-        key[k] = kInf;
-        if (i < na) {
-            const uint4 f = ldg_stream(src + i, l2_policy_evict_first());
-            key[k] = ((uint64_t)f.x << 10) | i;
-            big = big || f.x >= (1u << 31) || f.z >= (1u << kBusyBits);
-            amax = max(amax, f.x);
-            // speed-up numerator (arrival + busy), summed in 16-bit halves
-            seq_lo += (f.x & 0xFFFFu) + (f.z & 0xFFFFu);
-            seq_hi += (f.x >> 16) + min(f.z >> 16, 1u << 16);
-        }
-    }
-    uint32_t fail = __any_sync(FULL, big) ? 1u : 0u;
-    seq_lo = __reduce_add_sync(FULL, seq_lo);
-    seq_hi = __reduce_add_sync(FULL, seq_hi);
-    amax = __reduce_max_sync(FULL, amax);
-    warp_sort_keys<K>(key, amax < (1u << 22), lane);
-    __syncwarp();
-    // SoA records in arrival order
-    uint32_t memk[K], prk[K];
-    uint32_t zc = 0;
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-        const uint32_t e = (uint32_t)k * 32u + lane;
-        memk[k] = ~0u;
-        prk[k] = 0;
-        const bool v = key[k] != kInf;
-        if (v) {
-            const uint32_t i = (uint32_t)key[k] & kAppMask;
-            const uint4 f = __ldg(src + i);  // just loaded: an L1 hit
-            s_a[e] = f.x;
-            s_mem[e] = f.y;
-            s_bw[e] = (f.z & ((1u << kBusyBits) - 1u)) | (i << kBusyBits);
-            memk[k] = f.y;
-            prk[k] = f.w & 0xFFu;
-        }
-        zc += __popc(__ballot_sync(FULL, v && (key[k] >> 10) == 0));
-    }
-    // priority classes (policy.py:58-63): the distinct priorities, highest
-    // first; class word k of class c = the ballot of position k*32 + lane
-    if (L.need_cls) {
-        uint32_t pmax = 0, pres = 0;
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-            pmax = max(pmax, key[k] != kInf ? prk[k] : 0u);
-            pres |= key[k] != kInf && prk[k] < 32 ? 1u << prk[k] : 0u;
-        }
-        pmax = __reduce_max_sync(FULL, pmax);
-        pres = __reduce_or_sync(FULL, pres);
-        const uint32_t ncls = __popc(pres);
-        if (pmax >= 32 || ncls > kOctMaxCls) {
-            fail = 1;
-        } else {
-            uint32_t cls[K];
-#pragma unroll
-            for (int k = 0; k < K; k++) {
-                cls[k] = ~0u;
-                if (key[k] != kInf) {
-                    cls[k] = __popc((uint32_t)((uint64_t)pres >> (prk[k] + 1u)));
-                    s_bw[(uint32_t)k * 32u + lane] |= cls[k] << kClsShift;
-                }
-            }
-            for (uint32_t c = 0; c < ncls; c++) {
-#pragma unroll
-                for (int k = 0; k < K; k++) {
-                    const uint32_t w = __ballot_sync(FULL, cls[k] == c);
-                    if (lane == 0) s_cm[c * 8u + (uint32_t)k] = w;
-                }
-            }
-            if (lane == 0) meta[3] = ncls;
-        }
-    }
-    // fit table: requests ascending; T[r] = positions of the r smallest
-    uint64_t mk[K];
-    uint32_t mx = 0, mn = ~0u;
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-        const uint32_t e = (uint32_t)k * 32u + lane;
-        mk[k] = memk[k] != ~0u ? (((uint64_t)memk[k] << 8) | e) : kInf;
-        mx = max(mx, memk[k] != ~0u ? memk[k] : 0u);
-        mn = min(mn, memk[k]);
-    }
-    mx = __reduce_max_sync(FULL, mx);
-    mn = __reduce_min_sync(FULL, mn);
-    if (mn > mx) mn = mx;  // empty trace
-    warp_sort_keys<K>(mk, mx < (1u << 24), lane);
-    const uint64_t sc = ((uint64_t)kOctLB << 32) / ((uint64_t)(mx - mn) + 1ull);
-    const uint32_t scale = sc > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)sc;
-    uint32_t bcarry = 0;  // bucket of the last rank of the previous row (+1)
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-        const uint32_t r = (uint32_t)k * 32u + lane;
-        const bool valid = mk[k] != kInf;
-        const uint32_t pos = (uint32_t)mk[k] & 0xFFu;
-        s_por[r] = valid ? (uint16_t)pos : (uint16_t)N;
-        if (valid) s_rank[pos] = (uint16_t)r;
-        // LT[j] = first rank whose bucket is >= j: rank r owns (b[r-1], b[r]]
-        const uint32_t b = valid ? min((uint32_t)(((uint64_t)((uint32_t)(mk[k] >> 8) - mn) * scale) >> 32),
-                                       kOctLB - 1u) + 1u
-                                 : kOctLB + 1u;
-        uint32_t bp = __shfl_up_sync(FULL, b, 1);
-        if (lane == 0) bp = bcarry;
-        for (uint32_t j = bp; j < min(b, kOctLB + 1u); j++)
-            if (j < kOctLB) s_lt[j] = (uint16_t)r;
-        bcarry = __shfl_sync(FULL, b, 31);
-    }
-    for (uint32_t j = bcarry + lane; j < kOctLB; j += 32u) s_lt[j] = (uint16_t)N;
-    __syncwarp();
-    // rows R = 0..N/FS: word w of T[FS R] = positions 32w + b whose rank < FS R
-    {
-        uint32_t myrank[8];
-#pragma unroll
-        for (uint32_t w = 0; w < 8; w++) {
-            const uint32_t p = 32u * w + lane;
-            myrank[w] = p < na ? s_rank[p] : 0xFFFFu;
-        }
-        for (uint32_t R = 0; R <= N / kOctFS; R++) {
-            uint32_t word = 0;
-#pragma unroll
-            for (uint32_t w = 0; w < 8; w++) {
-                const uint32_t b = __ballot_sync(FULL, myrank[w] < kOctFS * R);
-                word = lane == w ? b : word;
-            }
-            if (lane < 8) s_tbl[R * 8u + lane] = word;
-        }
-    }
-    if (lane == 0) {
-        uint32_t* prm = reinterpret_cast<uint32_t*>(s_lt + kOctLB);
-        prm[0] = mn;
-        prm[1] = mx;
-        prm[2] = scale;
-        s_mem[N] = ~0u;
-        meta[0] = na;
-        meta[1] = fail;
-        meta[2] = zc;
-        const uint64_t seq = (uint64_t)seq_lo + ((uint64_t)seq_hi << 16);
-        meta[4] = (uint32_t)seq;
-        meta[5] = (uint32_t)(seq >> 32);
-    }
-    if (lane < 4) s_por[N + lane] = (uint16_t)N;
-    __syncwarp();
+    Slot256 S;
+    S.s_a = reinterpret_cast<uint32_t*>(ws + L.off_a) + g * OctSlot::S32;
+    S.s_mem = reinterpret_cast<uint32_t*>(ws + L.off_mem) + g * OctSlot::S32;
+    S.s_bw = reinterpret_cast<uint32_t*>(ws + L.off_bw) + g * OctSlot::S32;
+    S.s_por = reinterpret_cast<uint16_t*>(ws + L.off_por) + g * OctSlot::POR;
+    S.s_lt = reinterpret_cast<uint16_t*>(ws + L.off_lt) + g * OctSlot::LTB;
+    S.s_tbl = reinterpret_cast<uint32_t*>(ws + L.off_tbl) + g * OctSlot::TBL;
+    S.s_cm = reinterpret_cast<uint32_t*>(ws + L.off_cm) + g * OctSlot::CM;
+    S.meta = reinterpret_cast<uint32_t*>(ws + L.off_meta) + g * OctSlot::META;
+    S.s_rank = reinterpret_cast<uint16_t*>(ws + L.off_scr);
+    stage256<kOctLB>(L.sp, L.need_cls != 0, S, t, lane);
 }
 
 // ------------------------------------------------------------ kernel

@@ -17,12 +17,13 @@
 
 using namespace sg;
 
-template <int K, bool NAR, uint32_t HW = kLaneHeapW>
+template <int K, bool NAR, uint32_t HW = kLaneHeapW, bool TB = (K <= 4)>
 static void run_case(int n, uint32_t policy, uint32_t cap, const std::vector<uint32_t>& A,
                      const std::vector<uint32_t>& M, const std::vector<uint32_t>& Bz,
                      const std::vector<uint32_t>& Pr) {
     constexpr uint32_t N = 32u * K;
-    using Sim = LaneSim<K, NAR, HW>;  // fit table stride FitStride<K>
+    using Sim = LaneSim<K, NAR, HW, FitStride<K>::v, TB>;  // fit table stride FitStride<K>
+    using PT = typename Sim::PT;
     constexpr uint32_t NW = Sim::NW;
     // arrival order: (arrival, index)
     std::vector<int> ord(n);
@@ -55,15 +56,15 @@ static void run_case(int n, uint32_t policy, uint32_t cap, const std::vector<uin
     std::vector<int> rk(n);
     for (int e = 0; e < n; e++) rk[e] = e;
     std::stable_sort(rk.begin(), rk.end(), [&](int x, int y) { return s_mem[x] < s_mem[y]; });
-    std::vector<uint8_t> s_por(N + 16, (uint8_t)N), s_lt(LtBuckets<FitStride<K>::v>::v + 16, 0);  // (host: roomier than the kernel slots)
-    for (int r = 0; r < n; r++) s_por[r] = (uint8_t)rk[r];
+    std::vector<PT> s_por(N + 16, (PT)N), s_lt(LtBuckets<FitStride<K>::v>::v + 16, 0);  // (host: roomier than the kernel slots)
+    for (int r = 0; r < n; r++) s_por[r] = (PT)rk[r];
     const uint32_t mn = n ? s_mem[rk[0]] : 0, mx = n ? s_mem[rk[n - 1]] : 0;
     const uint64_t sc = ((uint64_t)LtBuckets<FitStride<K>::v>::v << 32) / ((uint64_t)(mx - mn) + 1);
     const uint32_t scale = sc > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)sc;
     for (uint32_t j = 0; j < LtBuckets<FitStride<K>::v>::v; j++) {  // first rank whose bucket is >= j
         uint32_t r = 0;
         while (r < (uint32_t)n && lt_bucket<FitStride<K>::v>(s_mem[rk[r]] - mn, scale) + 1 <= j) r++;
-        s_lt[j] = (uint8_t)r;
+        s_lt[j] = (PT)r;
     }
     constexpr uint32_t FS = FitStride<K>::v;
     std::vector<uint64_t> s_t4((N / FS + 2) * NW, 0);
@@ -73,7 +74,7 @@ static void run_case(int n, uint32_t policy, uint32_t cap, const std::vector<uin
         if ((r + 1) % FS == 0)
             for (uint32_t w = 0; w < NW; w++) s_t4[((r + 1) / FS) * NW + w] = T[w];
     }
-    std::vector<uint64_t> heap(32 * 32, 0);  // column 0 of the [slot][lane] layout
+    std::vector<uint64_t> heap(96 * 32, 0);  // column 0 of the [slot][lane] layout
     std::vector<uint32_t> grant(n, SG_NEVER), end(n, SG_NEVER);
     SimParams P{grant.data(), end.data()};
     Sim sim(P);
@@ -120,10 +121,15 @@ int main() {
             if (narrow == 1) run_case<2, true>(n, policy, cap, A, M, Bz, Pr);
             else if (narrow == 2) run_case<2, false, kLaneHeapN>(n, policy, cap, A, M, Bz, Pr);
             else run_case<2, false>(n, policy, cap, A, M, Bz, Pr);
-        } else {
+        } else if (n <= 128) {
             if (narrow == 1) run_case<4, true>(n, policy, cap, A, M, Bz, Pr);
             else if (narrow == 2) run_case<4, false, kLaneHeapN>(n, policy, cap, A, M, Bz, Pr);
             else run_case<4, false>(n, policy, cap, A, M, Bz, Pr);
+        } else {
+            // 256 apps: the global-table kernel's simulator (fit table, u16
+            // rank tables, 32-key three-level heap) for both key widths
+            if (narrow == 1) run_case<8, true, 32, true>(n, policy, cap, A, M, Bz, Pr);
+            else run_case<8, false, 32, true>(n, policy, cap, A, M, Bz, Pr);
         }
         fflush(stdout);
     }

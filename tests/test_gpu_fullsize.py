@@ -57,6 +57,10 @@ def test_full_size(cname, cuda, monkeypatch):
         for f in ("grant", "end", "stats_raw", "mem_pct", "dev_pct", "speedup"):
             assert torch.equal(bits(getattr(octet, f)), bits(getattr(warp, f))), f"C3: octet and warp engines differ in {f}"
         del octet
+        l256 = run_engine(apps, cfg, "lane256", monkeypatch)
+        for f in ("grant", "end", "stats_raw", "mem_pct", "dev_pct", "speedup"):
+            assert torch.equal(bits(getattr(l256, f)), bits(getattr(warp, f))), f"C3: lane256 and warp engines differ in {f}"
+        del l256
     del warp
 
     # stratified oracle sample: 1,200 traces spread over the batch

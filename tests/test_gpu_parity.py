@@ -188,12 +188,14 @@ def test_lane_kernel_long_traces_forced(n, cuda, monkeypatch):
     check_against_oracle(apps, (184_320,), cuda)
 
 
+@pytest.mark.parametrize("k1", ["octet", "lane256"])
 @pytest.mark.parametrize("pols", [POLICIES, ("pfifo", "pmmu"), ("mmu",), ("fifo", "mmu", "pmmu")])
-def test_octet_kernel_shapes(pols, cuda):
+def test_octet_kernel_shapes(pols, k1, cuda, monkeypatch):
     """K1 v8 (octet per simulation, 129..256-app traces): C3-shaped traces,
     edge traces (zero fields, simultaneous arrivals, stuck requests, ties),
     and the shapes its exact fallback takes over (more than 32 busy apps at
     once, more than eight priority classes, priorities of 32 and above)."""
+    monkeypatch.setenv("SGPU_K1", k1)  # (both 129..256-app kernels; the fixture's warp run covers v3)
     rng = np.random.default_rng(808)
     cfg = CONFIGS["C3"]
     c3 = as_u32x4(generate(dataclasses.replace(cfg.gen, seed=808), 0, 24))
@@ -217,8 +219,10 @@ def test_octet_kernel_shapes(pols, cuda):
         check_against_oracle(as_u32x4(generate(g, 0, 16)), (100_000,), cuda, policies=pols)
 
 
-def test_octet_kernel_ragged(cuda):
-    """Ragged batches up to 256 apps per trace on the octet kernel."""
+@pytest.mark.parametrize("k1", ["octet", "lane256"])
+def test_octet_kernel_ragged(k1, cuda, monkeypatch):
+    """Ragged batches up to 256 apps per trace on the octet and lane256 kernels."""
+    monkeypatch.setenv("SGPU_K1", k1)
     rng = np.random.default_rng(19)
     lens = rng.integers(129, 257, 40)
     total = int(lens.sum())
@@ -643,9 +647,12 @@ def test_cuda_graph_replay(tick_scale, cuda):
             np.testing.assert_array_equal(st[pi].view(np.uint8), sref.view(np.uint8))
 
 
-def test_octet_kernel_graph_replay(cuda):
-    """The octet kernel (C3-shaped 256-app traces) inside a captured CUDA
-    graph, replayed on fresh inputs: each replay simulates the whole batch."""
+@pytest.mark.parametrize("k1", ["octet", "lane256"])
+def test_octet_kernel_graph_replay(k1, cuda, monkeypatch):
+    """The 256-app kernels (C3-shaped traces) inside a captured CUDA graph,
+    replayed on fresh inputs: each replay simulates the whole batch (lane256:
+    its global staging scratch is a graph allocation)."""
+    monkeypatch.setenv("SGPU_K1", k1)
     cfg = CONFIGS["C3"]
     n = 600
     apps_t = B.generate_traces(cfg.gen, 0, n, device=0)

@@ -68,7 +68,7 @@ def check(exe, apps, pol, cap, narrow, min_checked):
 
 def narrow_lim(n):
     """LaneKey<K, true>::LIM: every event time of a 32-bit-key lane stays below it."""
-    logn = 5 if n <= 32 else 6 if n <= 64 else 7
+    logn = 5 if n <= 32 else 6 if n <= 64 else 7 if n <= 128 else 8
     return (1 << (31 - 2 * logn)) - 1
 
 
@@ -196,6 +196,25 @@ def test_lanesim_c4_traces(lanesim, pol):
     check(lanesim, apps[ok], pol, cfg.cap_mib[0], NARROW, int(ok.sum()))
     check(lanesim, apps, pol, cfg.cap_mib[0], WIDE, 40)
     check(lanesim, apps, pol, cfg.cap_mib[0], WIDE_RETRY, 40)
+
+
+@pytest.mark.parametrize("pol", POLICIES)
+def test_lanesim_256_apps(lanesim, pol):
+    """The global-table lane kernel's simulator at 129..256 apps (fit table
+    of four words, u16 rank tables, 32-key three-level heap): C3 traces and
+    edge shapes, both key widths, against the oracle."""
+    cfg = CONFIGS["C3"]
+    apps = as_u32x4(generate(cfg.gen, 31_000, 24))
+    ok = narrow_mask(apps, 256)
+    if ok.any():
+        check(lanesim, apps[ok], pol, cfg.cap_mib[0], NARROW, int(ok.sum()))
+    check(lanesim, apps, pol, cfg.cap_mib[0], WIDE, 20)
+    rng = np.random.default_rng(256)
+    for n in (129, 200, 256):
+        edge = random_edge_traces(rng, 40, n, 1000)
+        check(lanesim, edge, pol, 1000, WIDE, 30)
+        okn = narrow_mask(edge, n)
+        check(lanesim, edge[okn], pol, 1000, NARROW, int(okn.sum()) * 3 // 4)
 
 
 def test_header_is_shared_with_the_kernel():
