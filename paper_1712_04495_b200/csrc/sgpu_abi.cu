@@ -148,10 +148,12 @@ static int simulate_device(const sg_batch* in, const sg_out* out, cudaStream_t s
     const bool want_l256 = eng && strcmp(eng, "lane256") == 0;
     const bool lane_ok = sg::lane_eligible(p, s.program, s.f64, want_lane);
     const bool prog_ok = sg::prog_lane_eligible(p, s.program, s.f64, want_lane);
-    const bool oct_ok = !want_lane && sg::octet_eligible(p, s.program, s.f64);
+    const bool oct_ok = want_octet && sg::octet_eligible(p, s.program, s.f64);
     if (want_lane && !lane_ok && !prog_ok) return fail(E_ARG, "SGPU_K1=lane: batch not eligible for a lane kernel");
     if (want_octet && !oct_ok) return fail(E_ARG, "SGPU_K1=octet: batch not eligible for the octet kernel");
-    const bool l256_ok = want_l256 && sg::lane256_eligible(p, s.program, s.f64);
+    // 129..256-app single-device T0 traces: the lane256 kernel (v9) by
+    // default, the octet kernel (v8) when asked for
+    const bool l256_ok = !want_octet && !want_lane && !want_warp && sg::lane256_eligible(p, s.program, s.f64);
     if (want_l256 && !l256_ok) return fail(E_ARG, "SGPU_K1=lane256: batch not eligible for the lane256 kernel");
     cudaError_t e;
     if (prog_ok && !want_warp) {

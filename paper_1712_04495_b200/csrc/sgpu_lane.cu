@@ -421,10 +421,14 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
 // One lane's simulation of (trace t, device d, policy slot pslot) from the
 // staged slot g with a heap of HW 64-bit keys (or kLaneHeapN 32-bit keys).
 // Returns false if the lane must be re-run (retry pass / fallback).
+// kLaneSync: the lanes re-converge at a ballot every iteration
+// (LaneSim's SY; the lane256 kernel needs it, here it is measured)
+constexpr bool kLaneSync = false;
+
 template <int K, uint32_t FS, bool NARROW, uint32_t HW = kLaneHeapW>
 __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const uint16_t* meta, uint32_t g,
                                          uint32_t d, uint32_t pslot, uint32_t policy, uint32_t cap_d,
-                                         uint64_t t, uint32_t lane) {
+                                         uint64_t t, uint32_t lane, uint32_t runmask) {
     const SimParams& P = L.sp;
     constexpr uint32_t N = 32u * K;
     constexpr uint32_t NW = (N + 63u) / 64u;
@@ -435,7 +439,8 @@ __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const
     uint64_t a0;
     uint32_t na_unused;
     lane_trace_range(P, t, a0, na_unused);
-    LaneSim<K, NARROW, HW, FS> sim(P);
+    LaneSim<K, NARROW, HW, FS, (K <= 4), kLaneSync> sim(P);
+    sim.smask = runmask;
     sim.s_a = reinterpret_cast<const uint32_t*>(ws + L.off_a) + g * SS::S32;
     sim.s_mem = reinterpret_cast<const uint32_t*>(ws + L.off_mem) + g * SS::S32;
     sim.s_bw = reinterpret_cast<const uint32_t*>(ws + L.off_bw) + g * SS::S32;
@@ -449,7 +454,7 @@ __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const
     if (L.need_cls) { c0 = meta[meta_cls(ndev, d)]; c1 = meta[meta_cls(ndev, d + 1)]; }
     sim.s_cm = reinterpret_cast<const uint64_t*>(ws + L.off_cm) + g * (L.cm_per_trace * NW) + c0 * NW;
     sim.ncls = c1 - c0;
-    sim.heap = reinterpret_cast<typename LaneSim<K, NARROW, HW, FS>::Key*>(ws + L.off_fb) + lane;
+    sim.heap = reinterpret_cast<typename LaneSim<K, NARROW, HW, FS, (K <= 4), kLaneSync>::Key*>(ws + L.off_fb) + lane;
     const uint64_t out_base = (uint64_t)pslot * P.n_apps_total + a0;
     sim.gp = P.grant ? reinterpret_cast<uint32_t*>(P.grant) + out_base : nullptr;
     sim.ep = P.end ? reinterpret_cast<uint32_t*>(P.end) + out_base : nullptr;
@@ -517,17 +522,20 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, MB) trace_sim_lane_ke
         const uint64_t my_t = trace_of(t0 + min(g, gcount - 1));
         // 32-bit event keys when every trace of the group allows them (warp-uniform)
         const bool narrow = !RETRY && __all_sync(FULL, g >= gcount || meta[2] == 1);
+        // the lanes that enter a LaneSim main loop (for kLaneSync)
+        const uint32_t runmask =
+            __ballot_sync(FULL, g < gcount && !meta[1] && (RETRY || narrow || meta[2] != 2));
         if (g < gcount) {
             if (meta[1])
                 fail = true;
             else if (RETRY)
-                fail = !lane_run<K, FS, false, kLaneHeapN>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane);
+                fail = !lane_run<K, FS, false, kLaneHeapN>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane, runmask);
             else if (narrow)
-                fail = !lane_run<K, FS, true>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane);
+                fail = !lane_run<K, FS, true>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane, runmask);
             else if (meta[2] == 2)
                 defer = true;
             else
-                defer = !lane_run<K, FS, false>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane);
+                defer = !lane_run<K, FS, false>(L, ws, meta, g, d, pslot, policy, cap_d, my_t, lane, runmask);
         }
         if (!RETRY) {
             // a trace with a failed lane goes to the retry pass whole: one

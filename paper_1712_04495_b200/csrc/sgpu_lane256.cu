@@ -29,7 +29,9 @@ namespace sg {
 
 constexpr uint32_t kL256N = 256;
 constexpr uint32_t kL256Heap = 32;     // heap keys per lane (4-ary, three levels)
-constexpr uint32_t kL256LB = LtBuckets<kStage256FS>::v;
+constexpr uint32_t kL256FS = kStage256FS;  // fit-table stride (the table lives in global memory)
+constexpr uint32_t kL256LB = 256;     // rank-lookup buckets (about one request each)
+constexpr bool kL256Sorted = true;    // requests in rank order: one load per rank-lookup step
 constexpr int kL256WarpsPerBlock = 2;
 constexpr int kL256MinBlocks = 4;      // 8 warps/SM
 
@@ -42,9 +44,10 @@ struct L256Slot {
     static constexpr uint32_t POR = (BW + S32 + 15) & ~15u;
     static constexpr uint32_t LT = (POR + (kL256N + 4) * 2 + 15) & ~15u;
     static constexpr uint32_t TBL = (LT + kL256LB * 2 + 12 + 15) & ~15u;
-    static constexpr uint32_t CM = (TBL + (kL256N / kStage256FS + 1) * 32 + 15) & ~15u;
+    static constexpr uint32_t CM = (TBL + (kL256N / kL256FS + 1) * 32 + 15) & ~15u;
     static constexpr uint32_t META = (CM + kStage256MaxCls * 32 + 15) & ~15u;
-    static constexpr uint32_t RANK = (META + 32 + 15) & ~15u;
+    static constexpr uint32_t MS = (META + 32 + 15) & ~15u;
+    static constexpr uint32_t RANK = (MS + (kL256N + 4) * 4 + 15) & ~15u;
     static constexpr uint32_t BYTES = (RANK + kL256N * 2 + 127) & ~127u;
 };
 
@@ -67,6 +70,7 @@ __device__ __forceinline__ Slot256 l256_slot(uint8_t* base) {
     S.s_cm = reinterpret_cast<uint32_t*>(base + L256Slot::CM);
     S.meta = reinterpret_cast<uint32_t*>(base + L256Slot::META);
     S.s_rank = reinterpret_cast<uint16_t*>(base + L256Slot::RANK);
+    S.s_ms = kL256Sorted ? reinterpret_cast<uint32_t*>(base + L256Slot::MS) : nullptr;
     return S;
 }
 
@@ -74,7 +78,7 @@ __device__ __forceinline__ Slot256 l256_slot(uint8_t* base) {
 template <bool NARROW>
 __device__ __forceinline__ bool l256_run(const SimParams& P, const Slot256& S, uint8_t* ws, uint32_t pslot,
                                          uint32_t policy, uint64_t t, uint32_t lane, uint32_t runmask) {
-    using Sim = LaneSim<8, NARROW, kL256Heap, kStage256FS, true, true>;
+    using Sim = LaneSim<8, NARROW, kL256Heap, kL256FS, true, true, kL256LB>;
     const uint32_t na = S.meta[0], z = S.meta[2];
     Sim sim(P);
     sim.smask = runmask;  // the lanes of this warp in the main loop: they re-converge per iteration
@@ -83,6 +87,7 @@ __device__ __forceinline__ bool l256_run(const SimParams& P, const Slot256& S, u
     sim.s_bw = S.s_bw;
     sim.s_por = S.s_por;
     sim.s_lt = S.s_lt;
+    sim.s_ms = S.s_ms;
     const uint32_t* prm = reinterpret_cast<const uint32_t*>(S.s_lt + kL256LB);
     sim.lt_lo = prm[0];
     sim.lt_hi = prm[1];
@@ -124,7 +129,7 @@ __global__ void __launch_bounds__(kL256WarpsPerBlock * 32, MB) trace_sim_lane256
         const uint64_t t0 = grp * L.G;
         const uint32_t gcount = (uint32_t)min((uint64_t)L.G, P.n_traces - t0);
         for (uint32_t s = 0; s < gcount; s++)
-            stage256<kL256LB>(P, L.need_cls != 0, l256_slot(scr + (size_t)s * L256Slot::BYTES), t0 + s, lane);
+            stage256<kL256LB, kL256FS>(P, L.need_cls != 0, l256_slot(scr + (size_t)s * L256Slot::BYTES), t0 + s, lane);
         // 32-bit lane keys when every trace of the group allows them (warp-uniform)
         const uint32_t gi = min(g, gcount - 1);
         const Slot256 S = l256_slot(scr + (size_t)gi * L256Slot::BYTES);

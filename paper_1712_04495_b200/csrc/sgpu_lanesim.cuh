@@ -101,7 +101,7 @@ template <int K, bool NARROW, uint32_t HW = kLaneHeapW> struct LaneKey {
 };
 
 template <int K, bool NARROW, uint32_t HW = kLaneHeapW, uint32_t FSt = FitStride<K>::v, bool TB = (K <= 4),
-          bool SY = false>
+          bool SY = false, uint32_t LBt = LtBuckets<FSt>::v>
 struct LaneSim {
     static constexpr uint32_t N = 32u * K;
     static constexpr uint32_t NW = (N + 63u) / 64u;  // queue mask words
@@ -133,7 +133,8 @@ struct LaneSim {
     const uint32_t* s_mem;   // request MiB
     const uint32_t* s_bw;    // busy | app << kBusyBits | class << kClsShift
     const PT* s_por;         // position of the r-th smallest request (N past the end)
-    const PT* s_lt;          // s_lt[j] = #requests in buckets < j
+    const PT* s_lt;          // s_lt[j] = #requests in buckets < j (LBt buckets)
+    const uint32_t* s_ms;    // requests in rank order (s_ms[N] = ~0), or nullptr: s_mem[s_por[r]]
     uint32_t lt_lo, lt_hi, lt_scale;
     const uint64_t* s_t4;    // T[FS j] (NW words): positions of the FS j smallest requests
     const uint64_t* s_cm;    // class masks (NW words each) of this lane's device, top class first
@@ -160,7 +161,7 @@ struct LaneSim {
     uint32_t gc, gbud, gb0, gg;
     uint64_t gcand[NW], grem[NW];  // unscanned candidates / waiting members of the round's class
 
-    SG_HD LaneSim(const SimParams& p) : P(p) {}
+    SG_HD LaneSim(const SimParams& p) : P(p), s_ms(nullptr) {}
 
     SG_HD void mem_point(uint32_t now) {
         I += (uint64_t)used * (now - mem_t);
@@ -298,8 +299,15 @@ struct LaneSim {
     // forward scan of the sorted requests inside the bucket
     SG_HD uint32_t fit_rank(uint32_t budget) const {
         if (budget > lt_hi) return N;
-        const uint32_t bi = budget < lt_lo ? 0u : lt_bucket<FS>(budget - lt_lo, lt_scale);
+        const uint32_t bi = budget < lt_lo ? 0u
+                                           : min((uint32_t)(((uint64_t)(budget - lt_lo) * lt_scale) >> 32), LBt - 1u);
         uint32_t r = s_lt[bi];
+        if constexpr (K > 4 && TB) {
+            if (s_ms) {  // one load per step
+                while (s_ms[r] <= budget) r += 1;
+                return r;
+            }
+        }
         while (s_mem[s_por[r]] <= budget) r += 1;  // s_mem[N] = ~0 ends the scan
         return r;
     }

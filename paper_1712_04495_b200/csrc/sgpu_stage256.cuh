@@ -2,7 +2,7 @@
 // for the octet kernel (K1 v8, shared memory) and the global-table lane
 // kernel (K1 v9, global memory): SoA records in (arrival, index) order,
 // class masks of the distinct priorities (highest first), the fit table
-// (256-bit rows at every kStage256FS-th rank, as 8 u32 = 4 u64 words), the
+// (256-bit rows at every FS-th rank, as 8 u32 = 4 u64 words), the
 // rank-lookup buckets (u16, LB of them, then lo / hi / scale as u32), and
 // meta (u32): [0] n, [1] fail, [2] apps arriving at t = 0, [3] classes,
 // [4..5] sum(arrival + busy) (the speed-up numerator), [6] 32-bit lane keys
@@ -19,16 +19,17 @@ constexpr uint32_t kStage256MaxCls = 8;  // priority classes per trace
 
 struct Slot256 {
     uint32_t *s_a, *s_mem, *s_bw;  // N + 1 entries (s_mem[N] = ~0)
+    uint32_t* s_ms;                // optional: requests in rank order, N + 4 (~0 past the end)
     uint16_t *s_por, *s_lt;        // N + 4 ranks; LB buckets + 3 u32
     uint32_t *s_tbl, *s_cm, *meta; // (N / FS + 1) x 8; classes x 8; 8
     uint16_t* s_rank;              // scratch, N entries
 };
 
-template <uint32_t LB>
+template <uint32_t LB, uint32_t FS = kStage256FS>
 __device__ __forceinline__ void stage256(const SimParams& P, bool need_cls, const Slot256& S, uint64_t t,
                                          uint32_t lane) {
     constexpr uint32_t N = 256;
-    constexpr uint32_t kOctFS = kStage256FS;
+    constexpr uint32_t kOctFS = FS;
     constexpr int K = 8;  // apps per lane
     uint64_t a0;
     uint32_t na;
@@ -153,6 +154,7 @@ __device__ __forceinline__ void stage256(const SimParams& P, bool need_cls, cons
         const bool valid = mk[k] != kInf;
         const uint32_t pos = (uint32_t)mk[k] & 0xFFu;
         s_por[r] = valid ? (uint16_t)pos : (uint16_t)N;
+        if (S.s_ms) S.s_ms[r] = valid ? (uint32_t)(mk[k] >> 8) : ~0u;
         if (valid) s_rank[pos] = (uint16_t)r;
         // LT[j] = first rank whose bucket is >= j: rank r owns (b[r-1], b[r]]
         const uint32_t b = valid ? min((uint32_t)(((uint64_t)((uint32_t)(mk[k] >> 8) - mn) * scale) >> 32),
@@ -201,6 +203,7 @@ __device__ __forceinline__ void stage256(const SimParams& P, bool need_cls, cons
         meta[6] = (uint64_t)amax + bsum < LaneKey<8, true>::LIM ? 1u : 0u;
     }
     if (lane < 4) s_por[N + lane] = (uint16_t)N;
+    if (lane < 4 && S.s_ms) S.s_ms[N + lane] = ~0u;
     __syncwarp();
 }
 
