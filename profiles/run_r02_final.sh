@@ -16,7 +16,7 @@ timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"; cat gpurun_out/bench_ref.json
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/b_ncu.log 2>&1; echo "ncu list rc=$?"
 python profiles/summarize_launches.py gpurun_out/launches.csv > gpurun_out/launches_summary.txt 2>&1; cat gpurun_out/launches_summary.txt
-timeout 1200 $NCU -k regex:trace_sim_octet_kernel -s 2 -o gpurun_out/fin_c3 python bench.py --config C3 --steps 1 --warmup 2 --no-cpu --no-e2e > gpurun_out/ncu_c3.log 2>&1; echo "ncu c3 rc=$?"
+timeout 1500 $NCU -k regex:trace_sim_lane256_kernel -s 2 -o gpurun_out/fin_c3 python bench.py --config C3 --steps 1 --warmup 2 --no-cpu --no-e2e > gpurun_out/ncu_c3.log 2>&1; echo "ncu c3 rc=$?"
 timeout 900 $NCU -k regex:trace_sim_lane_kernelILi4ELb0 -s 3 -o gpurun_out/fin_c4 python bench.py --config C4 --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_c4.log 2>&1; echo "ncu c4 rc=$?"
 timeout 600 $NCU -k regex:trace_sim_lane_kernelILi2ELb0 -s 3 -o gpurun_out/fin_c5 python bench.py --config C5 --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_c5.log 2>&1; echo "ncu c5 rc=$?"
 timeout 600 $NCU -k regex:trace_prog_lane_kernel -s 2 -o gpurun_out/fin_prog python profiles/program_bench.py 262144 > gpurun_out/ncu_prog.log 2>&1; echo "ncu prog rc=$?"
