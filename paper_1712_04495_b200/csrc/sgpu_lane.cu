@@ -338,7 +338,7 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
         uint64_t carry[NW];
 #pragma unroll
         for (uint32_t w = 0; w < NW; w++) carry[w] = 0;
-        uint32_t bcarry = 0;  // bucket of the last rank of the previous row (+1)
+        uint32_t bk1[K];  // per rank: its bucket + 1
 #pragma unroll
         for (int k = 0; k < K; k++) {
             const uint32_t r = (uint32_t)k * 32u + lane;
@@ -359,16 +359,46 @@ __device__ __forceinline__ void stage_trace(const LaneParams& L, uint8_t* ws, ui
                 carry[w] = __shfl_sync(FULL, (uint32_t)v, 31) |
                            ((uint64_t)__shfl_sync(FULL, (uint32_t)(v >> 32), 31) << 32);
             }
-            // LT[j] = first rank whose bucket is >= j: rank r owns (b[r-1], b[r]]
-            const uint32_t b = valid ? lt_bucket<FS>((uint32_t)(mk[k] >> 8) - mn, scale) + 1u : LtBuckets<FS>::v + 1u;
-            uint32_t bp = __shfl_up_sync(FULL, b, 1);
-            if (lane == 0) bp = bcarry;
-            for (uint32_t j = bp; j < min(b, LtBuckets<FS>::v + 1u); j++)
-                if (j < LtBuckets<FS>::v) s_lt[j] = (uint8_t)r;
-            bcarry = __shfl_sync(FULL, b, 31);
+            // bucket of rank r, + 1 (LB + 1 past the valid ranks)
+            bk1[k] = valid ? lt_bucket<FS>((uint32_t)(mk[k] >> 8) - mn, scale) + 1u : LtBuckets<FS>::v + 1u;
         }
-        // buckets above the largest request (all ranks valid) -> N
-        for (uint32_t j = bcarry + lane; j < LtBuckets<FS>::v; j += 32u) s_lt[j] = (uint8_t)N;
+        // LT[j] = first rank whose bucket is >= j = #ranks with bucket < j:
+        // the last rank r of each bucket value leaves r + 1 at index
+        // bucket + 1, and a prefix maximum over the buckets fills the rest
+        // (no loop whose trip count varies across lanes)
+        {
+            constexpr uint32_t LB = LtBuckets<FS>::v, CH = LB / 32u;
+            static_assert(LB % 32u == 0, "buckets per lane");
+            uint8_t* lt = s_lt + lane * CH;
+#pragma unroll
+            for (uint32_t c = 0; c < CH; c++) lt[c] = 0;
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < K; k++) {
+                const uint32_t r = (uint32_t)k * 32u + lane;
+                uint32_t bn = __shfl_down_sync(FULL, bk1[k], 1);
+                const uint32_t nx = __shfl_sync(FULL, bk1[k + 1 < K ? k + 1 : k], 0);
+                if (lane == 31) bn = k + 1 < K ? nx : LB + 1u;
+                if (bn != bk1[k] && bk1[k] < LB) s_lt[bk1[k]] = (uint8_t)(r + 1u);
+            }
+            __syncwarp();
+            uint32_t v[CH], m = 0;
+#pragma unroll
+            for (uint32_t c = 0; c < CH; c++) {
+                m = max(m, (uint32_t)lt[c]);
+                v[c] = m;
+            }
+            uint32_t x = m;  // inclusive max scan over the lanes' chunks
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t u = __shfl_up_sync(FULL, x, o);
+                if (lane >= (uint32_t)o) x = max(x, u);
+            }
+            uint32_t ex = __shfl_up_sync(FULL, x, 1);
+            if (lane == 0) ex = 0;
+#pragma unroll
+            for (uint32_t c = 0; c < CH; c++) lt[c] = (uint8_t)max(v[c], ex);
+        }
         if (!narrow && ndev == 1) {
             // busy apps at once <= apps without a request + the most requests
             // that fit the device together (the k smallest): ranks whose
