@@ -395,8 +395,7 @@ def main():
     launches = 0
     # K1 (lane engine: main pass + 64-bit-key retry pass) + K2 stats_reduce
     k1_launches = B.k1_launches(cfg.gen.apps_per_trace, npol, cfg.ndev)
-    k1_kernel = {"lane": "trace_sim_lane_kernel", "warp": "trace_sim_kernel"}[
-        B.k1_engine(cfg.gen.apps_per_trace, npol, cfg.ndev)]
+    k1_kernel = B.K1_KERNELS[B.k1_engine(cfg.gen.apps_per_trace, npol, cfg.ndev)]
 
     def step(i=None):
         nonlocal launches

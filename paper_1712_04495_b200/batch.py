@@ -284,25 +284,36 @@ def simulate_batch_host(apps: np.ndarray, policies: Iterable = ("fifo",), cap_mi
 
 
 def k1_engine(apps_per_trace: int, n_policies: int, ndev: int = 1) -> str:
-    """K1 engine of a T0 simulate_batch call: "lane" (trace_sim_lane) or
-    "warp" (trace_sim).  Mirrors the default choice of sgpu_lane.cu
-    lane_eligible and the SGPU_K1 override."""
+    """K1 engine of a T0 simulate_batch call: "lane" (trace_sim_lane, <= 128
+    apps), "lane256" (trace_sim_lane256, 129..256 apps on one device),
+    "octet" (trace_sim_octet, SGPU_K1=octet) or "warp" (trace_sim).
+    Mirrors the choice in sgpu_abi.cu simulate_device and the SGPU_K1
+    override."""
     n_pad = 32
     while n_pad < apps_per_trace:
         n_pad *= 2
     eng = os.environ.get("SGPU_K1", "")
     if eng == "warp" or n_policies * ndev > 32:
         return "warp"
-    lane = n_pad <= 64 or (n_pad <= 128 and n_policies * ndev >= 2)
+    wide_ok = n_pad == 256 and ndev == 1 and n_policies <= 4
+    if eng == "octet" and wide_ok:
+        return "octet"
     if eng == "lane":
-        lane = n_pad <= 256
+        return "lane" if n_pad <= 256 else "warp"
+    if wide_ok:
+        return "lane256"
+    lane = n_pad <= 64 or (n_pad <= 128 and n_policies * ndev >= 2)
     return "lane" if lane else "warp"
+
+
+K1_KERNELS = {"lane": "trace_sim_lane_kernel", "lane256": "trace_sim_lane256_kernel",
+              "octet": "trace_sim_octet_kernel", "warp": "trace_sim_kernel"}
 
 
 def k1_launches(apps_per_trace: int, n_policies: int, ndev: int = 1) -> int:
     """Kernel launches of one T0 simulate_batch call: two on the lane engine
     (the main pass + the 64-bit-key retry pass, sgpu_lane.cu
-    launch_sim_lane), one on the warp engine."""
+    launch_sim_lane), one on the others."""
     return 2 if k1_engine(apps_per_trace, n_policies, ndev) == "lane" else 1
 
 

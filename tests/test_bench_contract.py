@@ -31,12 +31,12 @@ def test_reference_arm_json_line():
 
 def test_k1_engine_and_launch_count(monkeypatch):
     """bench.py's gpu_launches and roofline kernel name follow the engine
-    sg_simulate_batch picks (sgpu_lane.cu lane_eligible)."""
+    sg_simulate_batch picks (sgpu_abi.cu simulate_device)."""
     sys.path.insert(0, ROOT)
     from paper_1712_04495_b200 import batch as B
     from paper_1712_04495_b200.tracegen import CONFIGS
     monkeypatch.delenv("SGPU_K1", raising=False)
-    want = {"C2": "lane", "C3": "warp", "C4": "lane", "C5": "lane"}
+    want = {"C2": "lane", "C3": "lane256", "C4": "lane", "C5": "lane"}
     for c, eng in want.items():
         cfg = CONFIGS[c]
         assert B.k1_engine(cfg.gen.apps_per_trace, len(cfg.policies), cfg.ndev) == eng, c
@@ -45,5 +45,9 @@ def test_k1_engine_and_launch_count(monkeypatch):
     assert B.k1_engine(20, 4, 9) == "warp"        # more than 32 simulations per trace
     monkeypatch.setenv("SGPU_K1", "warp")
     assert B.k1_engine(64, 4) == "warp" and B.k1_launches(64, 4) == 1
+    assert B.k1_engine(300, 2) == "warp"          # beyond 256 apps
     monkeypatch.setenv("SGPU_K1", "lane")
     assert B.k1_engine(256, 2) == "lane"
+    monkeypatch.setenv("SGPU_K1", "octet")
+    assert B.k1_engine(256, 2) == "octet" and B.k1_launches(256, 2) == 1
+    assert B.K1_KERNELS["lane256"] == "trace_sim_lane256_kernel"
