@@ -482,19 +482,7 @@ int simulate_host(const sg_batch* in, const sg_out* out, int cuda_device, uint64
     // Pipeline buffers come from the device's stream-ordered memory pool
     // (cudaMallocAsync), kept cached between calls: repeated calls pay no
     // cudaMalloc/cudaFree or implicit device synchronisation.
-    {
-        static std::mutex mu;
-        static bool pool_tuned[64] = {false};
-        std::lock_guard<std::mutex> lk(mu);
-        if (cuda_device >= 0 && cuda_device < 64 && !pool_tuned[cuda_device]) {
-            cudaMemPool_t pool;
-            if (cudaDeviceGetDefaultMemPool(&pool, cuda_device) == cudaSuccess) {
-                uint64_t keep = ~0ull;
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-            }
-            pool_tuned[cuda_device] = true;
-        }
-    }
+    sg::keep_pool_memory();  // after cudaSetDevice(cuda_device)
     // The pipeline's streams persist per device (created once, reused by
     // every call: their work-counter slots stay theirs); one host-pipeline
     // call per device at a time (they would share PCIe and host memory

@@ -72,6 +72,11 @@ cudaError_t work_release(cudaStream_t stream, WorkLease& lease, cudaError_t err)
 // (kernel, device, smem) and the resulting resident blocks per SM, cached:
 // launches pay no attribute call or occupancy query.
 cudaError_t kernel_config(const void* kern, int threads, size_t smem, int* per_sm, int* sms);
+// Once per device: the current device's default memory pool keeps freed
+// memory (release threshold = max), so the per-launch cudaMallocAsync
+// scratch of the lane kernels is recycled instead of unmapped at each
+// synchronisation and mapped again by the next launch.
+void keep_pool_memory();
 
 // Shared-memory layout for one warp simulating traces of up to n_pad apps
 // (single_app_buf: one staged trace instead of the T0 double buffer, for the

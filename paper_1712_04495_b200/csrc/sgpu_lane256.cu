@@ -208,6 +208,7 @@ cudaError_t launch_sim_lane256(const SimParams& p, cudaStream_t stream, int* gri
     if (grid_out) *grid_out = (int)grid;
     // global staging scratch: one slot per trace of every resident warp
     const size_t scr_b = (size_t)grid * kL256WarpsPerBlock * L.G * L256Slot::BYTES;
+    keep_pool_memory();
     err = cudaMallocAsync(reinterpret_cast<void**>(&L.scratch), scr_b, stream);
     if (err != cudaSuccess) return err;
     WorkLease lease;

@@ -289,6 +289,21 @@ std::map<std::tuple<const void*, int, int, size_t>, KernelCfg> g_cfg;
 std::map<std::pair<const void*, int>, size_t> g_smem_max;
 }  // namespace
 
+void keep_pool_memory() {
+    static std::mutex mu;
+    static bool kept[64] = {false};
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+    std::lock_guard<std::mutex> lk(mu);
+    if (kept[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    kept[dev] = true;
+}
+
 cudaError_t kernel_config(const void* kern, int threads, size_t smem, int* per_sm, int* sms) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
