@@ -43,12 +43,11 @@ struct L256Slot {
     static constexpr uint32_t BW = (MEM + S32 + 15) & ~15u;
     static constexpr uint32_t POR = (BW + S32 + 15) & ~15u;
     static constexpr uint32_t LT = (POR + (kL256N + 4) * 2 + 15) & ~15u;
-    static constexpr uint32_t TBL = (LT + kL256LB * 2 + 12 + 15) & ~15u;
+    static constexpr uint32_t TBL = (LT + kL256LB * 4 + 12 + 15) & ~15u;  // packed u32 bucket entries + 3 u32
     static constexpr uint32_t CM = (TBL + (kL256N / kL256FS + 1) * 32 + 15) & ~15u;
     static constexpr uint32_t META = (CM + kStage256MaxCls * 32 + 15) & ~15u;
     static constexpr uint32_t MS = (META + 32 + 15) & ~15u;
-    static constexpr uint32_t RANK = (MS + (kL256N + 4) * 4 + 15) & ~15u;
-    static constexpr uint32_t BYTES = (RANK + kL256N * 2 + 127) & ~127u;
+    static constexpr uint32_t BYTES = (MS + (kL256N + 4) * 4 + 127) & ~127u;  // staging rank scratch: shared
 };
 
 struct L256Params {
@@ -69,7 +68,8 @@ __device__ __forceinline__ Slot256 l256_slot(uint8_t* base) {
     S.s_tbl = reinterpret_cast<uint32_t*>(base + L256Slot::TBL);
     S.s_cm = reinterpret_cast<uint32_t*>(base + L256Slot::CM);
     S.meta = reinterpret_cast<uint32_t*>(base + L256Slot::META);
-    S.s_rank = reinterpret_cast<uint16_t*>(base + L256Slot::RANK);
+    S.s_rank = nullptr;  // set by the caller (the warp's shared region while staging)
+    S.s_lt32 = reinterpret_cast<uint32_t*>(base + L256Slot::LT);
     S.s_ms = kL256Sorted ? reinterpret_cast<uint32_t*>(base + L256Slot::MS) : nullptr;
     return S;
 }
@@ -88,7 +88,8 @@ __device__ __forceinline__ bool l256_run(const SimParams& P, const Slot256& S, u
     sim.s_por = S.s_por;
     sim.s_lt = S.s_lt;
     sim.s_ms = S.s_ms;
-    const uint32_t* prm = reinterpret_cast<const uint32_t*>(S.s_lt + kL256LB);
+    sim.s_lt32 = S.s_lt32;
+    const uint32_t* prm = S.s_lt32 + kL256LB;
     sim.lt_lo = prm[0];
     sim.lt_hi = prm[1];
     sim.lt_scale = prm[2];
@@ -128,8 +129,11 @@ __global__ void __launch_bounds__(kL256WarpsPerBlock * 32, MB) trace_sim_lane256
         const uint64_t next = work_fetch(P.work, lane);
         const uint64_t t0 = grp * L.G;
         const uint32_t gcount = (uint32_t)min((uint64_t)L.G, P.n_traces - t0);
-        for (uint32_t s = 0; s < gcount; s++)
-            stage256<kL256LB, kL256FS>(P, L.need_cls != 0, l256_slot(scr + (size_t)s * L256Slot::BYTES), t0 + s, lane);
+        for (uint32_t s = 0; s < gcount; s++) {
+            Slot256 S = l256_slot(scr + (size_t)s * L256Slot::BYTES);
+            S.s_rank = reinterpret_cast<uint16_t*>(ws);  // the heaps are not in use yet
+            stage256<kL256LB, kL256FS>(P, L.need_cls != 0, S, t0 + s, lane);
+        }
         // 32-bit lane keys when every trace of the group allows them (warp-uniform)
         const uint32_t gi = min(g, gcount - 1);
         const Slot256 S = l256_slot(scr + (size_t)gi * L256Slot::BYTES);

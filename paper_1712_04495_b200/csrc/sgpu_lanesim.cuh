@@ -52,6 +52,7 @@ constexpr uint32_t kBusyBits = 21;          // busy < 2^21 on this path; app ind
 constexpr uint32_t kClsShift = 29;          // s_bw bits 29-31: priority class of the app within its device
 constexpr uint32_t kLaneMaxCls = 8;         // classes per device on this path (more: warp-kernel re-run)
 
+constexpr uint32_t kLtSat = (1u << 23) - 1u;  // packed bucket entry: request field saturated
 SG_HD uint32_t bw_busy(uint32_t bw) { return bw & ((1u << kBusyBits) - 1u); }
 SG_HD uint32_t bw_app(uint32_t bw) { return (bw >> kBusyBits) & 0xFFu; }
 SG_HD uint32_t bw_cls(uint32_t bw) { return bw >> kClsShift; }
@@ -135,6 +136,10 @@ struct LaneSim {
     const PT* s_por;         // position of the r-th smallest request (N past the end)
     const PT* s_lt;          // s_lt[j] = #requests in buckets < j (LBt buckets)
     const uint32_t* s_ms;    // requests in rank order (s_ms[N] = ~0), or nullptr: s_mem[s_por[r]]
+    // optional (with s_ms, K > 4): bucket entries packed as request << 9 |
+    // rank (kLtSat in the request field: saturated, load s_ms[rank]), so the
+    // first scan step needs no load of its own
+    const uint32_t* s_lt32;
     uint32_t lt_lo, lt_hi, lt_scale;
     const uint64_t* s_t4;    // T[FS j] (NW words): positions of the FS j smallest requests
     const uint64_t* s_cm;    // class masks (NW words each) of this lane's device, top class first
@@ -161,7 +166,7 @@ struct LaneSim {
     uint32_t gc, gbud, gb0, gg;
     uint64_t gcand[NW], grem[NW];  // unscanned candidates / waiting members of the round's class
 
-    SG_HD LaneSim(const SimParams& p) : P(p), s_ms(nullptr) {}
+    SG_HD LaneSim(const SimParams& p) : P(p), s_ms(nullptr), s_lt32(nullptr) {}
 
     SG_HD void mem_point(uint32_t now) {
         I += (uint64_t)used * (now - mem_t);
@@ -301,6 +306,19 @@ struct LaneSim {
         if (budget > lt_hi) return N;
         const uint32_t bi = budget < lt_lo ? 0u
                                            : min((uint32_t)(((uint64_t)(budget - lt_lo) * lt_scale) >> 32), LBt - 1u);
+        if constexpr (K > 4 && TB) {
+            if (s_lt32) {
+                const uint32_t e = s_lt32[bi];
+                uint32_t r = e & 0x1FFu;
+                const uint32_t v = e >> 9;
+                if (v != kLtSat) {
+                    if (v > budget) return r;
+                    r += 1;
+                }
+                while (s_ms[r] <= budget) r += 1;
+                return r;
+            }
+        }
         uint32_t r = s_lt[bi];
         if constexpr (K > 4 && TB) {
             if (s_ms) {  // one load per step

@@ -418,6 +418,7 @@ __device__ __forceinline__ void oct_stage(const OctParams& L, uint8_t* ws, uint3
     S.s_cm = reinterpret_cast<uint32_t*>(ws + L.off_cm) + g * OctSlot::CM;
     S.meta = reinterpret_cast<uint32_t*>(ws + L.off_meta) + g * OctSlot::META;
     S.s_rank = reinterpret_cast<uint16_t*>(ws + L.off_scr);
+    S.s_lt32 = nullptr;
     S.s_ms = nullptr;
     stage256<kOctLB>(L.sp, L.need_cls != 0, S, t, lane);
 }

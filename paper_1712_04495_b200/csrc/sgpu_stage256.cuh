@@ -23,6 +23,7 @@ struct Slot256 {
     uint16_t *s_por, *s_lt;        // N + 4 ranks; LB buckets + 3 u32
     uint32_t *s_tbl, *s_cm, *meta; // (N / FS + 1) x 8; classes x 8; 8
     uint16_t* s_rank;              // scratch, N entries
+    uint32_t* s_lt32;              // optional: packed bucket entries (request << 9 | rank), LB of them + 3 u32
 };
 
 template <uint32_t LB, uint32_t FS = kStage256FS>
@@ -162,11 +163,22 @@ __device__ __forceinline__ void stage256(const SimParams& P, bool need_cls, cons
                                  : LB + 1u;
         uint32_t bp = __shfl_up_sync(FULL, b, 1);
         if (lane == 0) bp = bcarry;
+        const uint32_t ent = (min(valid ? (uint32_t)(mk[k] >> 8) : kLtSat, kLtSat) << 9) | r;
         for (uint32_t j = bp; j < min(b, LB + 1u); j++)
-            if (j < LB) s_lt[j] = (uint16_t)r;
+            if (j < LB) {
+                if (S.s_lt32)
+                    S.s_lt32[j] = ent;
+                else
+                    s_lt[j] = (uint16_t)r;
+            }
         bcarry = __shfl_sync(FULL, b, 31);
     }
-    for (uint32_t j = bcarry + lane; j < LB; j += 32u) s_lt[j] = (uint16_t)N;
+    for (uint32_t j = bcarry + lane; j < LB; j += 32u) {
+        if (S.s_lt32)
+            S.s_lt32[j] = (kLtSat << 9) | N;
+        else
+            s_lt[j] = (uint16_t)N;
+    }
     __syncwarp();
     // rows R = 0..N/FS: word w of T[FS R] = positions 32w + b whose rank < FS R
     {
@@ -187,7 +199,7 @@ __device__ __forceinline__ void stage256(const SimParams& P, bool need_cls, cons
         }
     }
     if (lane == 0) {
-        uint32_t* prm = reinterpret_cast<uint32_t*>(s_lt + LB);
+        uint32_t* prm = S.s_lt32 ? S.s_lt32 + LB : reinterpret_cast<uint32_t*>(s_lt + LB);
         prm[0] = mn;
         prm[1] = mx;
         prm[2] = scale;
