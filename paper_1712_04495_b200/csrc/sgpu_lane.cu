@@ -735,6 +735,13 @@ static cudaError_t launch_lane_k(LaneParams& L, LaneParams& R, cudaStream_t stre
             lane_layout(R, HBR, 4u);
             return launch_pair<K, kLaneHiBlocks2, LaneMinBlocksR<K>::v, 4u>(L, R, stream, grid_out);
         }
+        // nine blocks (18 warps) with the 4-stride table (12.2 KB per warp,
+        // 96 registers) beat eight with the 2-stride one (13.4 KB): C2
+        // 13.65 -> 13.57 ms (profiles/r02_b9_ab.txt)
+        if (smem_blocks >= 9u) {
+            lane_layout(R, HBR, 4u);
+            return launch_pair<K, 9, LaneMinBlocksR<K>::v, 4u>(L, R, stream, grid_out);
+        }
     }
     constexpr uint32_t FS = FitStride<K>::v;
     lane_layout(L, HB, FS);
