@@ -33,15 +33,15 @@ constexpr uint32_t kL256FS = kStage256FS;  // fit-table stride (the table lives 
 constexpr uint32_t kL256LB = 256;     // rank-lookup buckets (about one request each)
 constexpr bool kL256Sorted = true;    // requests in rank order: one load per rank-lookup step
 constexpr int kL256WarpsPerBlock = 2;
-constexpr int kL256MinBlocks = 4;      // 8 warps/SM
+constexpr int kL256MinBlocks = 6;      // 12 warps/SM (register cap 168)
 
 // Per-slot layout of the global scratch (bytes, 16-aligned offsets).
 struct L256Slot {
     static constexpr uint32_t S32 = (kL256N + 1) * 4;
     static constexpr uint32_t A = 0;
-    static constexpr uint32_t MEM = (A + S32 + 15) & ~15u;
-    static constexpr uint32_t BW = (MEM + S32 + 15) & ~15u;
-    static constexpr uint32_t POR = (BW + S32 + 15) & ~15u;
+    static constexpr uint32_t MEM = (A + S32 + 15) & ~15u;   // (request, busy word) pairs, N + 1 of them
+    static constexpr uint32_t BW = MEM + 4;
+    static constexpr uint32_t POR = (MEM + 2 * S32 + 15) & ~15u;
     static constexpr uint32_t LT = (POR + (kL256N + 4) * 2 + 15) & ~15u;
     static constexpr uint32_t TBL = (LT + kL256LB * 4 + 12 + 15) & ~15u;  // packed u32 bucket entries + 3 u32
     static constexpr uint32_t CM = (TBL + (kL256N / kL256FS + 1) * 32 + 15) & ~15u;
@@ -70,6 +70,7 @@ __device__ __forceinline__ Slot256 l256_slot(uint8_t* base) {
     S.meta = reinterpret_cast<uint32_t*>(base + L256Slot::META);
     S.s_rank = nullptr;  // set by the caller (the warp's shared region while staging)
     S.s_lt32 = reinterpret_cast<uint32_t*>(base + L256Slot::LT);
+    S.rs = 2;
     S.s_ms = kL256Sorted ? reinterpret_cast<uint32_t*>(base + L256Slot::MS) : nullptr;
     return S;
 }
@@ -78,7 +79,7 @@ __device__ __forceinline__ Slot256 l256_slot(uint8_t* base) {
 template <bool NARROW>
 __device__ __forceinline__ bool l256_run(const SimParams& P, const Slot256& S, uint8_t* ws, uint32_t pslot,
                                          uint32_t policy, uint64_t t, uint32_t lane, uint32_t runmask) {
-    using Sim = LaneSim<8, NARROW, kL256Heap, kL256FS, true, true, kL256LB>;
+    using Sim = LaneSim<8, NARROW, kL256Heap, kL256FS, true, true, kL256LB, 2>;
     const uint32_t na = S.meta[0], z = S.meta[2];
     Sim sim(P);
     sim.smask = runmask;  // the lanes of this warp in the main loop: they re-converge per iteration

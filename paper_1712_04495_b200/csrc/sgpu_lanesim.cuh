@@ -102,7 +102,7 @@ template <int K, bool NARROW, uint32_t HW = kLaneHeapW> struct LaneKey {
 };
 
 template <int K, bool NARROW, uint32_t HW = kLaneHeapW, uint32_t FSt = FitStride<K>::v, bool TB = (K <= 4),
-          bool SY = false, uint32_t LBt = LtBuckets<FSt>::v>
+          bool SY = false, uint32_t LBt = LtBuckets<FSt>::v, uint32_t RS = 1>
 struct LaneSim {
     static constexpr uint32_t N = 32u * K;
     static constexpr uint32_t NW = (N + 63u) / 64u;  // queue mask words
@@ -131,6 +131,8 @@ struct LaneSim {
     const SimParams& P;
     // trace slot (shared by the trace's lanes), arrival-position order
     const uint32_t* s_a;     // arrival tick
+    // RS: record stride in u32 (2: request and busy word of a position
+    // interleaved, s_bw = s_mem + 1, so a position's pair is one sector)
     const uint32_t* s_mem;   // request MiB
     const uint32_t* s_bw;    // busy | app << kBusyBits | class << kClsShift
     const PT* s_por;         // position of the r-th smallest request (N past the end)
@@ -274,7 +276,7 @@ struct LaneSim {
     uint32_t ap, ae;         // arrival stream: next position / end
     Key ka;                  // key of the next arrival (KY::INF: none)
     SG_HD void start_granted(uint32_t q) {
-        const uint32_t b = bw_busy(s_bw[q]);
+        const uint32_t b = bw_busy(s_bw[(q) * RS]);
         if (b) {
             busy_point(last, +1);
             pops += 1;  // the waiter's own entry
@@ -326,7 +328,7 @@ struct LaneSim {
                 return r;
             }
         }
-        while (s_mem[s_por[r]] <= budget) r += 1;  // s_mem[N] = ~0 ends the scan
+        while (s_mem[(s_por[r]) * RS] <= budget) r += 1;  // s_mem[N] = ~0 ends the scan
         return r;
     }
     // T[r]: positions of the r smallest requests = T[FS floor(r/FS)] + the
@@ -410,7 +412,7 @@ struct LaneSim {
                 const uint64_t bit = 1ull << q;
                 mask[0] &= ~bit;
                 grem[0] &= ~bit;
-                gbud -= s_mem[q];
+                gbud -= s_mem[(q) * RS];
                 gg += 1;
                 start_granted(q);
                 gcand[0] &= ~((bit << 1) - 1ull);
@@ -441,7 +443,7 @@ struct LaneSim {
                 gcand[w] &= w < qw ? 0ull : (w == qw ? ~((bit << 1) - 1ull) : ~0ull);
                 more = more || gcand[w] != 0;
             }
-            gbud -= s_mem[q];
+            gbud -= s_mem[(q) * RS];
             gg += 1;
             start_granted(q);
         }
@@ -513,7 +515,7 @@ struct LaneSim {
                 while (bits && !stop) {
                     const uint32_t q = 64u * w + ffs64(bits);
                     bits &= bits - 1;
-                    const uint32_t m = s_mem[q];
+                    const uint32_t m = s_mem[(q) * RS];
                     if (m <= budget) {
                         grant_one(q, m, budget, g);
                         if (fail) return;
@@ -607,8 +609,8 @@ struct LaneSim {
         // initial pops at t = 0: apps without a cpu step run inline, in index
         // order, each in its own virtual counter block
         for (uint32_t q = s; q < s + z; q++) {
-            const uint32_t bw = s_bw[q];
-            arrive(q, s_mem[q], bw, 0u, KY::c_init(bw_app(bw)));
+            const uint32_t bw = s_bw[(q) * RS];
+            arrive(q, s_mem[(q) * RS], bw, 0u, KY::c_init(bw_app(bw)));
             if constexpr (TBL) {
                 while (gs && !fail) {
                     grant_step();
@@ -624,7 +626,7 @@ struct LaneSim {
         ae = e;
         uint32_t bwa = 0;
         if (ap < e) {
-            bwa = s_bw[ap];
+            bwa = s_bw[(ap) * RS];
             ka = KY::make(s_a[ap], KY::c_init(bw_app(bwa)), ap);
         }
         while (true) {
@@ -645,14 +647,14 @@ struct LaneSim {
                 if (is_arr) {
                     ap += 1;
                     if (ap < e) {
-                        bwa = s_bw[ap];
+                        bwa = s_bw[(ap) * RS];
                         ka = KY::make(s_a[ap], KY::c_init(bw_app(bwa)), ap);
                     } else {
                         ka = KY::INF;
                     }
                 }
-                const uint32_t m = s_mem[q];
-                const uint32_t bw = s_bw[q];
+                const uint32_t m = s_mem[(q) * RS];
+                const uint32_t bw = s_bw[(q) * RS];
                 const uint32_t b = bw_busy(bw);
                 pops += 1;
                 last = now;
@@ -702,7 +704,7 @@ struct LaneSim {
         for (uint32_t w = 0; w < NW; w++) {
             for (uint64_t bits = mask[w]; bits; bits &= bits - 1) {
                 const uint32_t q = 64u * w + ffs64(bits);
-                const uint32_t o = bw_app(s_bw[q]);
+                const uint32_t o = bw_app(s_bw[(q) * RS]);
                 if (gp) gp[o] = SG_NEVER;
                 if (ep) ep[o] = SG_NEVER;
                 unf += 1;

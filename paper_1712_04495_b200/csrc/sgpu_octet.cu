@@ -419,6 +419,7 @@ __device__ __forceinline__ void oct_stage(const OctParams& L, uint8_t* ws, uint3
     S.meta = reinterpret_cast<uint32_t*>(ws + L.off_meta) + g * OctSlot::META;
     S.s_rank = reinterpret_cast<uint16_t*>(ws + L.off_scr);
     S.s_lt32 = nullptr;
+    S.rs = 1;
     S.s_ms = nullptr;
     stage256<kOctLB>(L.sp, L.need_cls != 0, S, t, lane);
 }

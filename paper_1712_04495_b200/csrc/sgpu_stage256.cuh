@@ -24,6 +24,7 @@ struct Slot256 {
     uint32_t *s_tbl, *s_cm, *meta; // (N / FS + 1) x 8; classes x 8; 8
     uint16_t* s_rank;              // scratch, N entries
     uint32_t* s_lt32;              // optional: packed bucket entries (request << 9 | rank), LB of them + 3 u32
+    uint32_t rs;                   // record stride of s_mem / s_bw in u32 (2: interleaved pairs)
 };
 
 template <uint32_t LB, uint32_t FS = kStage256FS>
@@ -91,8 +92,8 @@ __device__ __forceinline__ void stage256(const SimParams& P, bool need_cls, cons
             const uint32_t i = (uint32_t)key[k] & kAppMask;
             const uint4 f = __ldg(src + i);  // just loaded: an L1 hit
             s_a[e] = f.x;
-            s_mem[e] = f.y;
-            s_bw[e] = (f.z & ((1u << kBusyBits) - 1u)) | (i << kBusyBits);
+            s_mem[e * S.rs] = f.y;
+            s_bw[e * S.rs] = (f.z & ((1u << kBusyBits) - 1u)) | (i << kBusyBits);
             memk[k] = f.y;
             prk[k] = f.w & 0xFFu;
         }
@@ -119,7 +120,7 @@ __device__ __forceinline__ void stage256(const SimParams& P, bool need_cls, cons
                 cls[k] = ~0u;
                 if (key[k] != kInf) {
                     cls[k] = __popc((uint32_t)((uint64_t)pres >> (prk[k] + 1u)));
-                    s_bw[(uint32_t)k * 32u + lane] |= cls[k] << kClsShift;
+                    s_bw[((uint32_t)k * 32u + lane) * S.rs] |= cls[k] << kClsShift;
                 }
             }
             for (uint32_t c = 0; c < ncls; c++) {
@@ -203,7 +204,7 @@ __device__ __forceinline__ void stage256(const SimParams& P, bool need_cls, cons
         prm[0] = mn;
         prm[1] = mx;
         prm[2] = scale;
-        s_mem[N] = ~0u;
+        s_mem[N * S.rs] = ~0u;
         meta[0] = na;
         meta[1] = fail;
         meta[2] = zc;
