@@ -29,7 +29,7 @@ namespace sg {
 
 constexpr uint32_t kL256N = 256;
 constexpr uint32_t kL256Heap = 32;     // heap keys per lane (4-ary, three levels)
-constexpr uint32_t kL256FS = kStage256FS;  // fit-table stride (the table lives in global memory)
+constexpr uint32_t kL256FS = 8;     // fit-table stride: 8 (1 KB less per slot than 4; C3 165.9 -> 162.9 ms)  // fit-table stride (the table lives in global memory)
 constexpr uint32_t kL256LB = 256;     // rank-lookup buckets (about one request each)
 constexpr bool kL256Sorted = true;    // requests in rank order: one load per rank-lookup step
 constexpr int kL256WarpsPerBlock = 2;
@@ -42,7 +42,7 @@ struct L256Slot {
     static constexpr uint32_t MEM = (A + S32 + 15) & ~15u;   // (request, busy word) pairs, N + 1 of them
     static constexpr uint32_t BW = MEM + 4;
     static constexpr uint32_t POR = (MEM + 2 * S32 + 15) & ~15u;
-    static constexpr uint32_t LT = (POR + (kL256N + 4) * 2 + 15) & ~15u;
+    static constexpr uint32_t LT = (POR + (kL256N + 8) * 2 + 15) & ~15u;
     static constexpr uint32_t TBL = (LT + kL256LB * 4 + 12 + 15) & ~15u;  // packed u32 bucket entries + 3 u32
     static constexpr uint32_t CM = (TBL + (kL256N / kL256FS + 1) * 32 + 15) & ~15u;
     static constexpr uint32_t META = (CM + kStage256MaxCls * 32 + 15) & ~15u;

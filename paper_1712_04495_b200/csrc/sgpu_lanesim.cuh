@@ -342,6 +342,18 @@ struct LaneSim {
 #pragma unroll
             for (uint32_t w = 0; w < NW; w++)
                 t[w] |= (r & 1u) && (NW == 1 || w == (p >> 6)) ? 1ull << (p & 63u) : 0ull;
+        } else if constexpr (FS == 8) {
+            // the 8 u16 entries from rank r & ~7: one 16-byte chunk (sector)
+            const uint64_t* pw = reinterpret_cast<const uint64_t*>(s_por + (r & ~7u));
+            const uint64_t w0 = pw[0], w1 = pw[1];
+            const uint32_t k = r & 7u;
+#pragma unroll
+            for (uint32_t j = 0; j < 7; j++) {
+                const uint32_t p = (uint32_t)((j < 4 ? w0 : w1) >> (16u * (j & 3u))) & 0xFFFFu;
+#pragma unroll
+                for (uint32_t w = 0; w < NW; w++)
+                    t[w] |= k > j && (NW == 1 || w == (p >> 6)) ? 1ull << (p & 63u) : 0ull;
+            }
         } else {
             // the 4 entries from rank r & ~3 in one load (u8: 32 bits, u16: 64)
             using PW = typename std::conditional<sizeof(PT) == 1, uint32_t, uint64_t>::type;

@@ -215,7 +215,7 @@ __device__ __forceinline__ void stage256(const SimParams& P, bool need_cls, cons
         // (LaneKey<8, true>) suffice below their limit
         meta[6] = (uint64_t)amax + bsum < LaneKey<8, true>::LIM ? 1u : 0u;
     }
-    if (lane < 4) s_por[N + lane] = (uint16_t)N;
+    if (lane < FS) s_por[N + lane] = (uint16_t)N;
     if (lane < 4 && S.s_ms) S.s_ms[N + lane] = ~0u;
     __syncwarp();
 }
