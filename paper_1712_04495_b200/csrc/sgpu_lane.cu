@@ -499,6 +499,12 @@ __device__ __forceinline__ bool lane_run(const LaneParams& L, uint8_t* ws, const
     return true;
 }
 
+// Main pass: pre-write the group's output rows with full-sector stores
+// (groups of >= 4 traces).  C2: DRAM traffic 7.48 -> 4.35 GB per launch
+// (reads 3.16 -> 1.25 GB: no sector fills) for +0.7 % time; with one trace
+// per warp (C5) it cost 7.7 % and is off (profiles/r02_prewrite_ab.txt).
+constexpr bool kPrewriteRows = true;
+
 // Main pass (RETRY = false): every trace in order.  A trace whose 64-bit-key
 // lanes overflow their heap (kLaneHeapW events), or could (its staged
 // busy-app bound exceeds kLaneHeapW: meta[2] == 2), is appended to P.retry.
@@ -547,6 +553,25 @@ __global__ void __launch_bounds__(kLaneWarpsPerBlock * 32, MB) trace_sim_lane_ke
             for (uint64_t off = (uint64_t)lane * 128u; off < nb; off += 32u * 128u) prefetch_l2(base + off);
         }
 
+        if (!RETRY && kPrewriteRows && L.G >= 4u && P.grant && P.end && !P.trace_offsets) {
+            // the group's grant / end rows written whole first (coalesced
+            // 16-byte stores of SG_NEVER): the lanes' later per-app stores
+            // then land in fully written L2 sectors instead of partial ones
+            // that cost a DRAM read to fill (every entry is overwritten by
+            // the lanes, the fallback or the retry pass)
+            const uint64_t a0g = t0 * P.apps_per_trace;
+            const uint32_t span = gcount * P.apps_per_trace;
+            if (((a0g | span | P.n_apps_total) & 3u) == 0 &&
+                ((reinterpret_cast<uintptr_t>(P.grant) | reinterpret_cast<uintptr_t>(P.end)) & 15u) == 0) {
+                const uint4 nv = make_uint4(SG_NEVER, SG_NEVER, SG_NEVER, SG_NEVER);
+                for (uint32_t x = 0; x < 2u * P.npol; x++) {
+                    const uint32_t arr = x >= P.npol ? 1u : 0u, p = x - arr * P.npol;
+                    uint4* d4 = reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(arr ? P.end : P.grant) +
+                                                         (uint64_t)p * P.n_apps_total + a0g);
+                    for (uint32_t j = lane; j < span / 4u; j += 32u) d4[j] = nv;
+                }
+            }
+        }
         bool fail = false, defer = false;
         const uint16_t* meta = reinterpret_cast<const uint16_t*>(ws + L.off_meta) + g * L.meta_stride;
         const uint64_t my_t = trace_of(t0 + min(g, gcount - 1));
